@@ -1,0 +1,126 @@
+/*
+ * pipeoptim.h — C-ABI of the B200 (sm_100a) PipeOptim weight-predictor and
+ * optimizer kernels (libpipeoptim.so).
+ *
+ * The reference (arXiv 2312.00839's `pipesim`, /root/reference/pkg) has no FFI:
+ * its hot path is the Python duck-typed optimizer/predictor interface in
+ * pkg/src/pipesim/optim.py. Each export below replaces one piece of it; the
+ * Python binding that mirrors the reference API is
+ * paper_2312_00839_b200/optim.py (ctypes), see INTEGRATION.md.
+ *
+ *   po_step            <- OptimizerState.step             optim.py:63-87
+ *                         (_sgdm_directions optim.py:89-99,
+ *                          _adam_directions optim.py:101-119)
+ *   po_direction       <- OptimizerState.prediction_direction optim.py:123-142
+ *   po_predict         <- prediction_direction + predict_weights fused,
+ *                         optim.py:123-155 as called by
+ *                         _PredictivePolicy.forward_view runtime.py:250-258
+ *   po_axpy_predict    <- predict_weights                 optim.py:145-155
+ *   po_step_predict    <- step followed by the next forward's prediction on the
+ *                         just-updated state (1F1B steady state "U_j F_{j+D-k}",
+ *                         runtime.py:449-463 then :411-413), one HBM pass
+ *   po_version_difference <- version_difference           optim.py:158-167
+ *
+ * Conventions:
+ *   - All buffers are caller-owned fp32 device arrays of n elements (flat
+ *     per-stage layout); the library allocates nothing and keeps no state
+ *     beyond a per-device SM-count cache.
+ *   - Every export returns int: 0 = ok, PO_EINVAL for bad arguments, otherwise
+ *     a cudaError_t from the launch. Nothing is thrown across the ABI.
+ *   - Stream-ordered, no host synchronisation inside; `stream` is a
+ *     cudaStream_t (NULL = legacy default stream).
+ *   - `step_count` is the optimizer's update count BEFORE the call, exactly as
+ *     OptimizerState.step_count. Bias corrections are evaluated on the host in
+ *     double precision as optim.py:106-108 (step, t = step_count + 1) and
+ *     optim.py:136-138 (read, t = step_count), then rounded to fp32.
+ *   - Scalar products lr*s are formed by the caller in double (optim.py:155
+ *     evaluates `lr * steps_ahead` first) and passed as `lr_times_s`.
+ *   - `nonfinite_index` (nullable) is a device int64 the caller initialises to
+ *     INT64_MAX; a step that produces a non-finite updated weight lowers it to
+ *     the smallest offending flat index (atomicMin), which the binding maps to
+ *     the parameter name to raise NumericError like optim.py:82-84.
+ *   - Updates are in place on w / state; predictions go to a separate staging
+ *     buffer w_hat, so live weights are never touched by prediction
+ *     (runtime.py:242-244, S10).
+ */
+#ifndef PIPEOPTIM_H_
+#define PIPEOPTIM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PO_ABI_VERSION 1
+#define PO_EINVAL (-22)
+
+/* optimizer kinds, OPTIMIZER_KINDS optim.py:17 */
+#define PO_SGDM 0
+#define PO_ADAM 1
+#define PO_ADAMW 2
+
+/* OptimizerConfig, optim.py:20-43 (fields in double, as Python floats) */
+typedef struct po_hparams {
+  int32_t kind;
+  int32_t _pad;
+  double momentum;        /* u,   default 0.9  */
+  double dampening;       /* tau, default 0.0  */
+  double weight_decay;    /* sgdm only, default 5e-4 */
+  double beta1;           /* default 0.9   */
+  double beta2;           /* default 0.999 */
+  double eps;             /* default 1e-8  */
+  double decoupled_decay; /* adamw lambda, default 1e-2 */
+} po_hparams;
+
+/* Optional launch shaping (nullable everywhere; NULL = tuned defaults). */
+typedef struct po_launch {
+  int32_t block;        /* threads per CTA (multiple of 32, <= 512), 0 = default */
+  int32_t ctas_per_sm;  /* persistent grid = SMs * ctas_per_sm, 0 = default */
+  int32_t vec;          /* floats per access: 4 (128-bit) or 8 (256-bit), 0 = default */
+  int32_t cache;        /* 0 = tuned default, 1 = streaming .cs, 2 = L1::no_allocate
+                           loads, 3 = plain ld/st */
+  int32_t unroll;       /* vectors per stream in flight per thread: 1, 2, 4; 0 = default */
+} po_launch;
+
+int po_abi_version(void);
+const char* po_strerror(int code);
+
+/* Eq. (4) D - rank - 1 with the reference's range errors -> PO_EINVAL. */
+int po_version_difference(int64_t depth, int64_t rank, int64_t* out);
+
+/* One optimizer update in place: w, state1 (sgdm buf | adam m), state2 (adam v;
+ * NULL for sgdm). g is read-only. dir_out (nullable) receives the applied
+ * direction d with w_new = w - lr*d (optim.py:64-68). */
+int po_step(const po_hparams* hp, float* w, const float* g, float* state1, float* state2,
+            float* dir_out, int64_t n, double lr, int64_t step_count,
+            int64_t* nonfinite_index, const po_launch* launch, void* stream);
+
+/* W_hat = W - (lr*s) * dir(state) with dir read at t = step_count; when
+ * step_count == 0 the direction is zero (optim.py:131-132). Pure read of
+ * w/state. */
+int po_predict(const po_hparams* hp, const float* w, const float* state1, const float* state2,
+               float* w_hat, int64_t n, double lr_times_s, int64_t step_count,
+               const po_launch* launch, void* stream);
+
+/* Fused: po_step, then W_hat = W_new - (lr_pred*s) * dir(state_new) read at
+ * t = step_count + 1, in one pass (32 B/param Adam, 24 B/param SGDM). */
+int po_step_predict(const po_hparams* hp, float* w, const float* g, float* state1,
+                    float* state2, float* w_hat, int64_t n, double lr,
+                    double lr_pred_times_s, int64_t step_count, int64_t* nonfinite_index,
+                    const po_launch* launch, void* stream);
+
+/* prediction_direction: dir_out = dir(state) at t = step_count (zeros when
+ * step_count == 0). */
+int po_direction(const po_hparams* hp, const float* state1, const float* state2, float* dir_out,
+                 int64_t n, int64_t step_count, const po_launch* launch, void* stream);
+
+/* predict_weights: w_hat = w - lr_times_s * d. */
+int po_axpy_predict(const float* w, const float* d, float* w_hat, int64_t n, double lr_times_s,
+                    const po_launch* launch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PIPEOPTIM_H_ */

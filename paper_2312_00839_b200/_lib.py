@@ -1,0 +1,122 @@
+"""ctypes binding of the C-ABI in include/pipeoptim.h (libpipeoptim.so).
+
+There is deliberately no CPU fallback: if the library is missing the product
+path raises immediately (`LibraryMissing`), and every call checks the
+returned status code.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .build import LIB_PATH
+
+PO_EINVAL = -22
+PO_SGDM, PO_ADAM, PO_ADAMW = 0, 1, 2
+KIND_CODES = {"sgdm": PO_SGDM, "adam": PO_ADAM, "adamw": PO_ADAMW}
+
+# Every symbol include/pipeoptim.h declares (tests check the .so exports them).
+EXPORTS = (
+    "po_abi_version",
+    "po_strerror",
+    "po_version_difference",
+    "po_step",
+    "po_predict",
+    "po_step_predict",
+    "po_direction",
+    "po_axpy_predict",
+)
+
+
+class LibraryMissing(RuntimeError):
+    """libpipeoptim.so is not built / not loadable: there is no fallback."""
+
+
+class KernelError(RuntimeError):
+    """A libpipeoptim call returned a non-zero status."""
+
+
+class po_hparams(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("momentum", ctypes.c_double),
+        ("dampening", ctypes.c_double),
+        ("weight_decay", ctypes.c_double),
+        ("beta1", ctypes.c_double),
+        ("beta2", ctypes.c_double),
+        ("eps", ctypes.c_double),
+        ("decoupled_decay", ctypes.c_double),
+    ]
+
+
+class po_launch(ctypes.Structure):
+    _fields_ = [
+        ("block", ctypes.c_int32),
+        ("ctas_per_sm", ctypes.c_int32),
+        ("vec", ctypes.c_int32),
+        ("cache", ctypes.c_int32),
+        ("unroll", ctypes.c_int32),
+    ]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_D = ctypes.c_double
+_HP = ctypes.POINTER(po_hparams)
+_LA = ctypes.POINTER(po_launch)
+
+_SIGNATURES = {
+    "po_abi_version": (ctypes.c_int, []),
+    "po_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "po_version_difference": (ctypes.c_int, [_I64, _I64, ctypes.POINTER(_I64)]),
+    "po_step": (ctypes.c_int, [_HP, _P, _P, _P, _P, _P, _I64, _D, _I64, _P, _LA, _P]),
+    "po_predict": (ctypes.c_int, [_HP, _P, _P, _P, _P, _I64, _D, _I64, _LA, _P]),
+    "po_step_predict": (ctypes.c_int, [_HP, _P, _P, _P, _P, _P, _I64, _D, _D, _I64, _P, _LA, _P]),
+    "po_direction": (ctypes.c_int, [_HP, _P, _P, _P, _I64, _I64, _LA, _P]),
+    "po_axpy_predict": (ctypes.c_int, [_P, _P, _P, _I64, _D, _LA, _P]),
+}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load(path: Path | str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the library; raises LibraryMissing if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise LibraryMissing(
+                f"{p} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback for the PipeOptim kernels)"
+            )
+        try:
+            lib = ctypes.CDLL(str(p))
+        except OSError as exc:
+            raise LibraryMissing(f"cannot load {p}: {exc}") from exc
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.po_abi_version() != 1:
+            raise LibraryMissing(f"{p}: ABI version {lib.po_abi_version()} != 1")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().po_strerror(rc).decode()
+        if rc == PO_EINVAL:
+            raise ValueError(f"{what}: {msg}")
+        raise KernelError(f"{what}: {msg} (status {rc})")
+
+
+def make_launch(block=0, ctas_per_sm=0, vec=0, cache=0, unroll=0):
+    return po_launch(block, ctas_per_sm, vec, cache, unroll)

@@ -1,0 +1,573 @@
+// pipeoptim_kernels.cu — sm_100a kernels + C-ABI for PipeOptim's
+// optimizer-dependent weight prediction (arXiv 2312.00839, Eq. (5)) and the
+// SGDM / Adam / AdamW update rules of the reference simulator
+// (/root/reference/pkg/src/pipesim/optim.py).
+//
+// Everything here is an HBM-bound elementwise stream over flat fp32 per-stage
+// buffers: no data reuse, ~1 flop/byte, so the design is the
+// streaming one — 128/256-bit vector LDG/STG (LDG.E.128 / LDG.E.256 on
+// sm_100a), a persistent grid sized in multiples of the SM count, several
+// independent vector loads in flight per thread before any use, streaming cache
+// hints so the 126 MB L2 is not polluted by data touched once, and the
+// optimizer step + next-forward prediction fused into ONE pass (K3), so each
+// parameter byte is read once per micro-step.
+//
+// Per-parameter algorithmic bytes (fp32):      SGDM   Adam/AdamW
+//   K1 predict       (r W,state  w W_hat)       12      16
+//   K2 step          (r W,g,state w W,state)     20      28
+//   K3 step+predict  (K2 + w W_hat)              24      32
+//
+// Numerics follow the reference formulas in fp32 with IEEE div/sqrt (no
+// fast-math): see Appendix A of SURVEY.md and the per-line citations below.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+#include <string.h>
+
+#include "pipeoptim.h"
+
+namespace {
+
+enum Mode : int {
+  MODE_STEP = 0,          // K2 (optionally also writes the applied direction)
+  MODE_STEP_DIR = 1,      // K2 + dir_out
+  MODE_PREDICT = 2,       // K1
+  MODE_PREDICT_ZERO = 3,  // K1 before the first step (direction == 0)
+  MODE_STEP_PREDICT = 4,  // K3
+  MODE_DIRECTION = 5,     // prediction_direction read
+  MODE_DIRECTION_ZERO = 6,
+  MODE_AXPY = 7,          // predict_weights(w, d)
+};
+
+// fp32 launch coefficients, derived on the host in double.
+struct Coef {
+  float lr;         // step learning rate
+  float c_pred;     // lr_pred * s  (K1 / K3 / AXPY)
+  float bc1, bc2;   // bias corrections at the t this launch reads/writes
+  float beta1, omb1, beta2, omb2, eps, lam;
+  float mom, omd, wd;
+};
+
+struct Args {
+  float* w;            // live weights (read, or read+write for steps)
+  const float* g;      // gradient (read only)
+  float* s1;           // sgdm momentum buffer | adam exp_avg | axpy direction
+  float* s2;           // adam exp_avg_sq
+  float* out;          // w_hat or dir_out
+  int64_t n;
+  unsigned long long* bad;  // smallest non-finite flat index (atomicMin)
+  Coef c;
+};
+
+__host__ __device__ constexpr bool uses_w(int mode) {
+  return mode == MODE_STEP || mode == MODE_STEP_DIR || mode == MODE_PREDICT ||
+         mode == MODE_PREDICT_ZERO || mode == MODE_STEP_PREDICT || mode == MODE_AXPY;
+}
+__host__ __device__ constexpr bool writes_w(int mode) {
+  return mode == MODE_STEP || mode == MODE_STEP_DIR || mode == MODE_STEP_PREDICT;
+}
+__host__ __device__ constexpr bool uses_g(int mode) { return writes_w(mode); }
+__host__ __device__ constexpr bool uses_s1(int mode) {
+  return mode == MODE_STEP || mode == MODE_STEP_DIR || mode == MODE_PREDICT ||
+         mode == MODE_STEP_PREDICT || mode == MODE_DIRECTION || mode == MODE_AXPY;
+}
+__host__ __device__ constexpr bool uses_s2(int kind, int mode) {
+  return kind != PO_SGDM && mode != MODE_AXPY && uses_s1(mode);
+}
+__host__ __device__ constexpr bool writes_state(int mode) { return writes_w(mode); }
+__host__ __device__ constexpr bool writes_out(int mode) { return mode != MODE_STEP; }
+
+// ---- vector memory access -------------------------------------------------
+
+template <int VEC>
+struct Vec {
+  float v[VEC];
+};
+
+// CACHE: 0 default, 1 streaming (.cs: evict-first in L1/L2, data touched once),
+//        2 loads bypass L1 allocation (.L1::no_allocate), default stores.
+template <int VEC, int CACHE, bool READ_ONLY>
+__device__ __forceinline__ Vec<VEC> vload(const float* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 8) {
+    if constexpr (CACHE == 1) {
+      asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                     "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                   : "l"(p));
+    } else if constexpr (CACHE == 2 && READ_ONLY) {
+      asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                     "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                   : "l"(p));
+    } else if constexpr (CACHE == 2) {
+      asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                     "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                   : "l"(p));
+    } else {
+      asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                     "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7])
+                   : "l"(p));
+    }
+  } else if constexpr (VEC == 4) {
+    if constexpr (CACHE == 1) {
+      asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                   : "l"(p));
+    } else if constexpr (CACHE == 2 && READ_ONLY) {
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                   : "l"(p));
+    } else if constexpr (CACHE == 2) {
+      asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                   : "l"(p));
+    } else {
+      asm volatile("ld.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+                   : "l"(p));
+    }
+  } else {
+    r.v[0] = CACHE == 1 ? __ldcs(p) : *p;
+  }
+  return r;
+}
+
+template <int VEC, int CACHE>
+__device__ __forceinline__ void vstore(float* p, const Vec<VEC>& r) {
+  if constexpr (VEC == 8) {
+    if constexpr (CACHE == 1) {
+      asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
+                   "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]),
+                   "f"(r.v[7])
+                   : "memory");
+    } else {
+      asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
+                   "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]),
+                   "f"(r.v[7])
+                   : "memory");
+    }
+  } else if constexpr (VEC == 4) {
+    if constexpr (CACHE == 1) {
+      asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]),
+                   "f"(r.v[2]), "f"(r.v[3])
+                   : "memory");
+    } else {
+      asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]),
+                   "f"(r.v[2]), "f"(r.v[3])
+                   : "memory");
+    }
+  } else {
+    if (CACHE == 1)
+      __stcs(p, r.v[0]);
+    else
+      *p = r.v[0];
+  }
+}
+
+// ---- the per-element rules --------------------------------------------------
+
+// Adam/AdamW moment-ratio direction (m/bc1) / (sqrt(v/bc2) + eps),
+// optim.py:115 (step) and optim.py:141 (read). IEEE div/sqrt.
+__device__ __forceinline__ float adam_dir(float m, float v, const Coef& c) {
+  return __fdiv_rn(__fdiv_rn(m, c.bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, c.bc2)), c.eps));
+}
+
+// One element. w/s1/s2 are updated in place for step modes; `out` receives
+// W_hat or the direction; `nonfinite` flags a non-finite updated weight
+// (optim.py:82-84 checks the new weights only).
+template <int KIND, int MODE>
+__device__ __forceinline__ void elem(const Coef& c, float& w, float g, float& s1, float& s2,
+                                     float& out, bool& nonfinite) {
+  if constexpr (MODE == MODE_AXPY) {
+    // predict_weights: w - (lr*s) * d, optim.py:155
+    out = __fsub_rn(w, __fmul_rn(c.c_pred, s1));
+  } else if constexpr (MODE == MODE_PREDICT_ZERO) {
+    // zero direction before the first step (optim.py:131-132), then Eq. (5)
+    out = __fsub_rn(w, __fmul_rn(c.c_pred, 0.0f));
+  } else if constexpr (MODE == MODE_DIRECTION_ZERO) {
+    out = 0.0f;
+  } else if constexpr (MODE == MODE_PREDICT || MODE == MODE_DIRECTION) {
+    // prediction_direction read (optim.py:133-141): sgdm -> buf; adam(w) -> ratio, no lambda*W
+    float d = (KIND == PO_SGDM) ? s1 : adam_dir(s1, s2, c);
+    if constexpr (MODE == MODE_PREDICT)
+      out = __fsub_rn(w, __fmul_rn(c.c_pred, d));
+    else
+      out = d;
+  } else {
+    // step (optim.py:63-119)
+    float d, dread;
+    if constexpr (KIND == PO_SGDM) {
+      // eff = g + wd*W ; v = u*v + (1-tau)*eff  (optim.py:95-96)
+      float eff = __fadd_rn(g, __fmul_rn(c.wd, w));
+      float nb = __fadd_rn(__fmul_rn(c.mom, s1), __fmul_rn(c.omd, eff));
+      s1 = nb;
+      d = nb;
+      dread = nb;  // read after the step is the buffer (optim.py:134-135)
+    } else {
+      // m = b1*m + (1-b1)*g ; v = b2*v + (1-b2)*g*g  (optim.py:111-112)
+      float m = __fadd_rn(__fmul_rn(c.beta1, s1), __fmul_rn(c.omb1, g));
+      float v = __fadd_rn(__fmul_rn(c.beta2, s2), __fmul_rn(c.omb2, __fmul_rn(g, g)));
+      s1 = m;
+      s2 = v;
+      // the read right after this step uses t = step_count_new == this step's t,
+      // so the step and read bias corrections coincide (S5)
+      dread = adam_dir(m, v, c);
+      d = (KIND == PO_ADAMW) ? __fadd_rn(dread, __fmul_rn(c.lam, w)) : dread;  // optim.py:116-117
+    }
+    float nw = __fsub_rn(w, __fmul_rn(c.lr, d));  // W - lr*d, optim.py:82
+    nonfinite |= !isfinite(nw);
+    w = nw;
+    if constexpr (MODE == MODE_STEP_DIR) out = d;
+    if constexpr (MODE == MODE_STEP_PREDICT) out = __fsub_rn(nw, __fmul_rn(c.c_pred, dread));
+  }
+}
+
+template <int KIND, int MODE, int VEC, int CACHE>
+__device__ __forceinline__ void do_vec(const Args& a, int64_t vi, int64_t& bad) {
+  const int64_t base = vi * VEC;
+  Vec<VEC> w{}, g{}, s1{}, s2{}, out{};
+  if constexpr (uses_w(MODE)) w = vload<VEC, CACHE, !writes_w(MODE)>(a.w + base);
+  if constexpr (uses_g(MODE)) g = vload<VEC, CACHE, true>(a.g + base);
+  if constexpr (uses_s1(MODE)) s1 = vload<VEC, CACHE, !writes_state(MODE)>(a.s1 + base);
+  if constexpr (uses_s2(KIND, MODE)) s2 = vload<VEC, CACHE, !writes_state(MODE)>(a.s2 + base);
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    bool e = false;
+    elem<KIND, MODE>(a.c, w.v[j], g.v[j], s1.v[j], s2.v[j], out.v[j], e);
+    if (e && bad == INT64_MAX) bad = base + j;
+  }
+  if constexpr (writes_w(MODE)) vstore<VEC, CACHE>(a.w + base, w);
+  if constexpr (writes_state(MODE)) {
+    vstore<VEC, CACHE>(a.s1 + base, s1);
+    if constexpr (KIND != PO_SGDM) vstore<VEC, CACHE>(a.s2 + base, s2);
+  }
+  if constexpr (writes_out(MODE)) vstore<VEC, CACHE>(a.out + base, out);
+}
+
+// Persistent grid-stride stream. Each thread issues UNROLL independent vector
+// loads per stream before the first use (memory-level parallelism: Little's law
+// at ~6.5 TB/s x ~0.8 us needs ~5 MB in flight chip-wide, ~35 KB per SM).
+template <int KIND, int MODE, int VEC, int CACHE, int UNROLL>
+__global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
+  const int64_t nv = a.n / VEC;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t bad = INT64_MAX;
+  int64_t i = tid;
+
+  for (; i + (UNROLL - 1) * stride < nv; i += UNROLL * stride) {
+    Vec<VEC> w[UNROLL], g[UNROLL], s1[UNROLL], s2[UNROLL], out[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t base = (i + u * stride) * VEC;
+      if constexpr (uses_w(MODE)) w[u] = vload<VEC, CACHE, !writes_w(MODE)>(a.w + base);
+      if constexpr (uses_g(MODE)) g[u] = vload<VEC, CACHE, true>(a.g + base);
+      if constexpr (uses_s1(MODE)) s1[u] = vload<VEC, CACHE, !writes_state(MODE)>(a.s1 + base);
+      if constexpr (uses_s2(KIND, MODE)) s2[u] = vload<VEC, CACHE, !writes_state(MODE)>(a.s2 + base);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t base = (i + u * stride) * VEC;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        bool e = false;
+        elem<KIND, MODE>(a.c, w[u].v[j], g[u].v[j], s1[u].v[j], s2[u].v[j], out[u].v[j], e);
+        if (e && bad == INT64_MAX) bad = base + j;
+      }
+      if constexpr (writes_w(MODE)) vstore<VEC, CACHE>(a.w + base, w[u]);
+      if constexpr (writes_state(MODE)) {
+        vstore<VEC, CACHE>(a.s1 + base, s1[u]);
+        if constexpr (KIND != PO_SGDM) vstore<VEC, CACHE>(a.s2 + base, s2[u]);
+      }
+      if constexpr (writes_out(MODE)) vstore<VEC, CACHE>(a.out + base, out[u]);
+    }
+  }
+  for (; i < nv; i += stride) do_vec<KIND, MODE, VEC, CACHE>(a, i, bad);
+
+  // scalar tail [nv*VEC, n): fewer than VEC elements
+  const int64_t t = nv * VEC + tid;
+  if (t < a.n) {
+    float w = 0.f, g = 0.f, s1 = 0.f, s2 = 0.f, out = 0.f;
+    if constexpr (uses_w(MODE)) w = a.w[t];
+    if constexpr (uses_g(MODE)) g = a.g[t];
+    if constexpr (uses_s1(MODE)) s1 = a.s1[t];
+    if constexpr (uses_s2(KIND, MODE)) s2 = a.s2[t];
+    bool e = false;
+    elem<KIND, MODE>(a.c, w, g, s1, s2, out, e);
+    if (e && bad == INT64_MAX) bad = t;
+    if constexpr (writes_w(MODE)) a.w[t] = w;
+    if constexpr (writes_state(MODE)) {
+      a.s1[t] = s1;
+      if constexpr (KIND != PO_SGDM) a.s2[t] = s2;
+    }
+    if constexpr (writes_out(MODE)) a.out[t] = out;
+  }
+  if (a.bad != nullptr && bad != INT64_MAX) atomicMin(a.bad, (unsigned long long)bad);
+}
+
+// ---- host side ---------------------------------------------------------------
+
+constexpr int kMaxDevices = 64;
+int g_sm_count[kMaxDevices] = {0};
+
+int sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  if (g_sm_count[dev] == 0) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+    g_sm_count[dev] = sms;
+  }
+  return g_sm_count[dev];
+}
+
+bool aligned(const void* p, int bytes) {
+  return p == nullptr || (reinterpret_cast<uintptr_t>(p) % (uintptr_t)bytes) == 0;
+}
+
+// Only the hot modes (K1/K2/K3) get every launch-shape variant; the
+// reference-compatibility reads use the default shape.
+__host__ __device__ constexpr bool tunable(int mode) {
+  return mode == MODE_STEP || mode == MODE_PREDICT || mode == MODE_STEP_PREDICT;
+}
+
+struct Shape {
+  int vec, cache, unroll;
+};
+
+template <int KIND, int MODE, int VEC, int CACHE>
+cudaError_t launch_unroll(const Args& a, const Shape& sh, dim3 grid, dim3 block, cudaStream_t s) {
+  if constexpr (tunable(MODE) && VEC > 1) {
+    switch (sh.unroll) {
+      case 1: po_stream_kernel<KIND, MODE, VEC, CACHE, 1><<<grid, block, 0, s>>>(a); break;
+      case 4: po_stream_kernel<KIND, MODE, VEC, CACHE, 4><<<grid, block, 0, s>>>(a); break;
+      default: po_stream_kernel<KIND, MODE, VEC, CACHE, 2><<<grid, block, 0, s>>>(a); break;
+    }
+  } else {
+    po_stream_kernel<KIND, MODE, VEC, CACHE, (VEC > 1 ? 2 : 4)><<<grid, block, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+template <int KIND, int MODE, int VEC>
+cudaError_t launch_cache(const Args& a, const Shape& sh, dim3 grid, dim3 block, cudaStream_t s) {
+  if constexpr (tunable(MODE) && VEC > 1) {
+    switch (sh.cache) {
+      case 0: return launch_unroll<KIND, MODE, VEC, 0>(a, sh, grid, block, s);
+      case 2: return launch_unroll<KIND, MODE, VEC, 2>(a, sh, grid, block, s);
+      default: return launch_unroll<KIND, MODE, VEC, 1>(a, sh, grid, block, s);
+    }
+  } else {
+    return launch_unroll<KIND, MODE, VEC, 1>(a, sh, grid, block, s);
+  }
+}
+
+template <int KIND, int MODE>
+cudaError_t launch_vec(const Args& a, const Shape& sh, dim3 grid, dim3 block, cudaStream_t s) {
+  switch (sh.vec) {
+    case 8: return launch_cache<KIND, MODE, 8>(a, sh, grid, block, s);
+    case 4: return launch_cache<KIND, MODE, 4>(a, sh, grid, block, s);
+    default: return launch_cache<KIND, MODE, 1>(a, sh, grid, block, s);
+  }
+}
+
+template <int MODE>
+cudaError_t launch_kind(int kind, const Args& a, const Shape& sh, dim3 grid, dim3 block,
+                        cudaStream_t s) {
+  switch (kind) {
+    case PO_SGDM: return launch_vec<PO_SGDM, MODE>(a, sh, grid, block, s);
+    case PO_ADAM: return launch_vec<PO_ADAM, MODE>(a, sh, grid, block, s);
+    default: return launch_vec<PO_ADAMW, MODE>(a, sh, grid, block, s);
+  }
+}
+
+cudaError_t dispatch(int kind, int mode, const Args& a, const Shape& sh, dim3 grid, dim3 block,
+                     cudaStream_t s) {
+  switch (mode) {
+    case MODE_STEP: return launch_kind<MODE_STEP>(kind, a, sh, grid, block, s);
+    case MODE_STEP_DIR: return launch_kind<MODE_STEP_DIR>(kind, a, sh, grid, block, s);
+    case MODE_PREDICT: return launch_kind<MODE_PREDICT>(kind, a, sh, grid, block, s);
+    case MODE_PREDICT_ZERO: return launch_vec<PO_SGDM, MODE_PREDICT_ZERO>(a, sh, grid, block, s);
+    case MODE_STEP_PREDICT: return launch_kind<MODE_STEP_PREDICT>(kind, a, sh, grid, block, s);
+    case MODE_DIRECTION: return launch_kind<MODE_DIRECTION>(kind, a, sh, grid, block, s);
+    case MODE_DIRECTION_ZERO:
+      return launch_vec<PO_SGDM, MODE_DIRECTION_ZERO>(a, sh, grid, block, s);
+    default: return launch_vec<PO_SGDM, MODE_AXPY>(a, sh, grid, block, s);
+  }
+}
+
+// Default launch shapes per (mode, kind), from the 2^30-element B200 sweep
+// (scripts/kernel_sweep.py --tune-all; profiles/r1_kernel_tune.md): all use
+// 256-bit vectors; `unroll` vectors per stream in flight per thread.
+struct DefaultShape {
+  int block, ctas_per_sm, unroll, cache;
+};
+
+DefaultShape default_shape(int kind, int mode) {
+  const bool sg = kind == PO_SGDM;
+  switch (mode) {
+    case MODE_PREDICT: return sg ? DefaultShape{256, 8, 2, 1} : DefaultShape{512, 2, 1, 1};
+    case MODE_STEP: return sg ? DefaultShape{512, 1, 1, 1} : DefaultShape{512, 1, 2, 0};
+    case MODE_STEP_PREDICT:
+      if (sg) return DefaultShape{384, 1, 1, 1};
+      return kind == PO_ADAM ? DefaultShape{512, 1, 1, 1} : DefaultShape{256, 8, 2, 0};
+    default: return DefaultShape{256, 4, 2, 1};
+  }
+}
+constexpr int kDefaultVec = 8;
+
+int run(int kind, int mode, Args a, const po_launch* L, cudaStream_t s) {
+  if (a.n < 0) return PO_EINVAL;
+  if (a.n == 0) return 0;
+  const DefaultShape d = default_shape(kind, mode);
+  int block = (L && L->block > 0) ? L->block : d.block;
+  int cps = (L && L->ctas_per_sm > 0) ? L->ctas_per_sm : d.ctas_per_sm;
+  int vec = (L && L->vec > 0) ? L->vec : kDefaultVec;
+  int cache = (L && L->cache > 0 && L->cache <= 2) ? L->cache : d.cache;
+  if (L && L->cache == 3) cache = 0;  // explicit plain ld/st request
+  int unroll = (L && L->unroll > 0) ? L->unroll : d.unroll;
+  if (block % 32 != 0 || block > 512) return PO_EINVAL;
+  if (unroll != 1 && unroll != 2 && unroll != 4) return PO_EINVAL;
+  if (vec != 8 && vec != 4 && vec != 1) return PO_EINVAL;
+  // fall back to narrower vectors when any stream is misaligned
+  const void* ptrs[5] = {a.w, a.g, a.s1, a.s2, a.out};
+  while (vec > 1) {
+    bool ok = true;
+    for (const void* p : ptrs) ok = ok && aligned(p, vec * 4);
+    if (ok) break;
+    vec = vec == 8 ? 4 : 1;
+  }
+  const int64_t nv = a.n / vec;
+  const int64_t tail = a.n - nv * vec;
+  int64_t want = (nv + block - 1) / block;
+  if (want < 1) want = 1;
+  const int64_t tail_blocks = (tail + block - 1) / block;
+  if (want < tail_blocks) want = tail_blocks;
+  int64_t cap = (int64_t)sm_count() * cps;
+  int64_t grid = want < cap ? want : cap;
+  const Shape sh{vec, cache, unroll};
+  cudaError_t e = dispatch(kind, mode, a, sh, dim3((unsigned)grid), dim3(block), s);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+bool valid_hp(const po_hparams* hp) {
+  if (hp == nullptr) return false;
+  if (hp->kind != PO_SGDM && hp->kind != PO_ADAM && hp->kind != PO_ADAMW) return false;
+  return true;
+}
+
+// Host-side coefficient derivation in double, mirroring the reference's
+// Python float arithmetic, then rounded once to fp32.
+Coef coef(const po_hparams* hp, double lr, double c_pred, int64_t t) {
+  Coef c;
+  memset(&c, 0, sizeof(c));
+  c.lr = (float)lr;
+  c.c_pred = (float)c_pred;
+  if (t >= 1) {
+    c.bc1 = (float)(1.0 - pow(hp->beta1, (double)t));  // optim.py:107 / :137
+    c.bc2 = (float)(1.0 - pow(hp->beta2, (double)t));  // optim.py:108 / :138
+  } else {
+    c.bc1 = 1.f;
+    c.bc2 = 1.f;
+  }
+  c.beta1 = (float)hp->beta1;
+  c.omb1 = (float)(1.0 - hp->beta1);
+  c.beta2 = (float)hp->beta2;
+  c.omb2 = (float)(1.0 - hp->beta2);
+  c.eps = (float)hp->eps;
+  c.lam = (float)hp->decoupled_decay;
+  c.mom = (float)hp->momentum;
+  c.omd = (float)(1.0 - hp->dampening);
+  c.wd = (float)hp->weight_decay;
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int po_abi_version(void) { return PO_ABI_VERSION; }
+
+const char* po_strerror(int code) {
+  if (code == 0) return "ok";
+  if (code == PO_EINVAL) return "invalid argument";
+  return cudaGetErrorString((cudaError_t)code);
+}
+
+int po_version_difference(int64_t depth, int64_t rank, int64_t* out) {
+  // optim.py:158-167
+  if (out == nullptr || depth < 1 || rank < 0 || rank >= depth) return PO_EINVAL;
+  *out = depth - rank - 1;
+  return 0;
+}
+
+int po_step(const po_hparams* hp, float* w, const float* g, float* state1, float* state2,
+            float* dir_out, int64_t n, double lr, int64_t step_count, int64_t* nonfinite_index,
+            const po_launch* launch, void* stream) {
+  if (!valid_hp(hp) || step_count < 0) return PO_EINVAL;
+  if (n > 0 && (w == nullptr || g == nullptr || state1 == nullptr)) return PO_EINVAL;
+  if (n > 0 && hp->kind != PO_SGDM && state2 == nullptr) return PO_EINVAL;
+  Args a{w, g, state1, hp->kind == PO_SGDM ? nullptr : state2, dir_out, n,
+         reinterpret_cast<unsigned long long*>(nonfinite_index),
+         coef(hp, lr, 0.0, step_count + 1)};
+  return run(hp->kind, dir_out ? MODE_STEP_DIR : MODE_STEP, a, launch, (cudaStream_t)stream);
+}
+
+int po_predict(const po_hparams* hp, const float* w, const float* state1, const float* state2,
+               float* w_hat, int64_t n, double lr_times_s, int64_t step_count,
+               const po_launch* launch, void* stream) {
+  if (!valid_hp(hp) || step_count < 0) return PO_EINVAL;
+  if (n > 0 && (w == nullptr || w_hat == nullptr)) return PO_EINVAL;
+  const bool zero = step_count == 0;
+  if (!zero && n > 0 && (state1 == nullptr || (hp->kind != PO_SGDM && state2 == nullptr)))
+    return PO_EINVAL;
+  Args a{const_cast<float*>(w), nullptr,
+         zero ? nullptr : const_cast<float*>(state1),
+         (zero || hp->kind == PO_SGDM) ? nullptr : const_cast<float*>(state2), w_hat, n, nullptr,
+         coef(hp, 0.0, lr_times_s, step_count)};
+  return run(hp->kind, zero ? MODE_PREDICT_ZERO : MODE_PREDICT, a, launch, (cudaStream_t)stream);
+}
+
+int po_step_predict(const po_hparams* hp, float* w, const float* g, float* state1, float* state2,
+                    float* w_hat, int64_t n, double lr, double lr_pred_times_s, int64_t step_count,
+                    int64_t* nonfinite_index, const po_launch* launch, void* stream) {
+  if (!valid_hp(hp) || step_count < 0) return PO_EINVAL;
+  if (n > 0 && (w == nullptr || g == nullptr || state1 == nullptr || w_hat == nullptr))
+    return PO_EINVAL;
+  if (n > 0 && hp->kind != PO_SGDM && state2 == nullptr) return PO_EINVAL;
+  Args a{w, g, state1, hp->kind == PO_SGDM ? nullptr : state2, w_hat, n,
+         reinterpret_cast<unsigned long long*>(nonfinite_index),
+         coef(hp, lr, lr_pred_times_s, step_count + 1)};
+  return run(hp->kind, MODE_STEP_PREDICT, a, launch, (cudaStream_t)stream);
+}
+
+int po_direction(const po_hparams* hp, const float* state1, const float* state2, float* dir_out,
+                 int64_t n, int64_t step_count, const po_launch* launch, void* stream) {
+  if (!valid_hp(hp) || step_count < 0) return PO_EINVAL;
+  if (n > 0 && dir_out == nullptr) return PO_EINVAL;
+  const bool zero = step_count == 0;
+  if (!zero && n > 0 && (state1 == nullptr || (hp->kind != PO_SGDM && state2 == nullptr)))
+    return PO_EINVAL;
+  Args a{nullptr, nullptr, zero ? nullptr : const_cast<float*>(state1),
+         (zero || hp->kind == PO_SGDM) ? nullptr : const_cast<float*>(state2), dir_out, n, nullptr,
+         coef(hp, 0.0, 0.0, step_count)};
+  return run(hp->kind, zero ? MODE_DIRECTION_ZERO : MODE_DIRECTION, a, launch,
+             (cudaStream_t)stream);
+}
+
+int po_axpy_predict(const float* w, const float* d, float* w_hat, int64_t n, double lr_times_s,
+                    const po_launch* launch, void* stream) {
+  if (n > 0 && (w == nullptr || d == nullptr || w_hat == nullptr)) return PO_EINVAL;
+  Coef c;
+  memset(&c, 0, sizeof(c));
+  c.c_pred = (float)lr_times_s;
+  Args a{const_cast<float*>(w), nullptr, const_cast<float*>(d), nullptr, w_hat, n, nullptr, c};
+  return run(PO_SGDM, MODE_AXPY, a, launch, (cudaStream_t)stream);
+}
+
+}  // extern "C"

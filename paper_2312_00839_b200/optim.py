@@ -1,0 +1,486 @@
+"""Optimizer rules and optimizer-dependent weight prediction on B200.
+
+Drop-in for the reference's predictor interface (pkg/src/pipesim/optim.py):
+`OptimizerConfig`, `OptimizerState(config, names)` with `.step(params, grads,
+lr) -> (new_params, dirs)`, `.prediction_direction(params)`, `.step_count`,
+`.momentum_buf / .exp_avg / .exp_avg_sq`, plus `predict_weights` and
+`version_difference` — same names, argument meaning and errors.
+
+What changes underneath: per-stage state lives in FLAT fp32 device buffers
+(`FlatLayout`), and every arithmetic pass is one of the sm_100a kernels in
+csrc/pipeoptim_kernels.cu called through the C-ABI (include/pipeoptim.h).
+Besides the reference-shaped list API, the runtime uses the in-place fast
+paths on a `FlatParams`:
+
+  step_(flat, lr)                                   K2  (28 / 20 B per param)
+  predict_(flat, lr, steps_ahead, out)              K1  (16 / 12 B per param)
+  step_predict_(flat, lr, lr_pred, steps_ahead, out) K3 (32 / 24 B per param)
+
+There is no CPU fallback: CPU tensors are accepted only as HOST buffers that
+are staged through the device (the end-to-end path), and a missing
+libpipeoptim.so raises `LibraryMissing`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .errors import NumericError
+
+OPTIMIZER_KINDS = ("sgdm", "adam", "adamw")
+
+_INT64_MAX = (1 << 63) - 1
+
+
+@dataclass(frozen=True)
+class OptimizerConfig:
+    """Validated hyper-parameters; defaults and ranges as optim.py:20-43."""
+
+    kind: str
+    momentum: float = 0.9
+    dampening: float = 0.0
+    weight_decay: float = 5e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    decoupled_decay: float = 1e-2
+
+    def __post_init__(self):
+        if self.kind not in OPTIMIZER_KINDS:
+            raise ValueError(f"unknown optimizer kind: {self.kind!r}")
+        if not 0.0 <= self.momentum < 1.0:
+            raise ValueError(f"momentum must be in [0, 1), got {self.momentum}")
+        if not 0.0 <= self.dampening <= 1.0:
+            raise ValueError(f"dampening must be in [0, 1], got {self.dampening}")
+        for name in ("beta1", "beta2"):
+            v = getattr(self, name)
+            if not 0.0 <= v < 1.0:
+                raise ValueError(f"{name} must be in [0, 1), got {v}")
+        if self.eps <= 0.0:
+            raise ValueError(f"eps must be positive, got {self.eps}")
+
+    def hparams(self) -> _lib.po_hparams:
+        return _lib.po_hparams(
+            _lib.KIND_CODES[self.kind],
+            0,
+            float(self.momentum),
+            float(self.dampening),
+            float(self.weight_decay),
+            float(self.beta1),
+            float(self.beta2),
+            float(self.eps),
+            float(self.decoupled_decay),
+        )
+
+
+# ---- flat per-stage layout ----------------------------------------------------
+
+
+class FlatLayout:
+    """Parameters [w0, b0, w1, b1, ...] (stages.py:133-138) packed into one flat
+    fp32 buffer. Each parameter starts on a 64-element (256 B) boundary so every
+    view is aligned for the 256-bit vector path; padding stays zero under all
+    three rules (g = 0, W = 0 => state and W remain 0).
+    """
+
+    ALIGN = 64
+
+    def __init__(self, names: Sequence[str], shapes: Sequence[Sequence[int]]):
+        if len(names) != len(shapes):
+            raise ValueError(f"{len(names)} names vs {len(shapes)} shapes")
+        self.names = list(names)
+        self.shapes = [tuple(int(d) for d in s) for s in shapes]
+        self.offsets: list[int] = []
+        self.sizes: list[int] = []
+        off = 0
+        for s in self.shapes:
+            n = math.prod(s)
+            self.offsets.append(off)
+            self.sizes.append(n)
+            off += -(-n // self.ALIGN) * self.ALIGN if n else 0
+        self.numel = off
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, FlatLayout) and self.shapes == other.shapes
+
+    def views(self, buf: torch.Tensor) -> list[torch.Tensor]:
+        return [buf[o : o + n].view(s) for o, n, s in zip(self.offsets, self.sizes, self.shapes)]
+
+    def empty(self, device, zero: bool = False) -> torch.Tensor:
+        if zero:
+            return torch.zeros(self.numel, dtype=torch.float32, device=device)
+        buf = torch.empty(self.numel, dtype=torch.float32, device=device)
+        # keep the alignment padding deterministic (zero) without a full memset
+        pad_ranges = self._padding()
+        for lo, hi in pad_ranges:
+            buf[lo:hi].zero_()
+        return buf
+
+    def _padding(self) -> list[tuple[int, int]]:
+        out = []
+        for i, (o, n) in enumerate(zip(self.offsets, self.sizes)):
+            end = self.offsets[i + 1] if i + 1 < len(self.offsets) else self.numel
+            if o + n < end:
+                out.append((o + n, end))
+        return out
+
+    def pack(self, tensors: Sequence[torch.Tensor], device) -> torch.Tensor:
+        """Copy a list of tensors (any device/dtype) into a new flat fp32 buffer."""
+        buf = self.empty(device)
+        for v, t in zip(self.views(buf), tensors):
+            if tuple(t.shape) != v.shape:
+                raise ValueError(f"shape {tuple(t.shape)} does not match layout {tuple(v.shape)}")
+            v.copy_(t, non_blocking=True)
+        return buf
+
+    def locate(self, flat_index: int) -> str:
+        for name, o, n in zip(self.names, self.offsets, self.sizes):
+            if o <= flat_index < o + n:
+                return name
+        return "<padding>"
+
+    def as_flat(self, tensors: Sequence[torch.Tensor]) -> torch.Tensor | None:
+        """The flat buffer `tensors` are views of, if they are exactly this
+        layout's views of one contiguous fp32 CUDA buffer; else None."""
+        if len(tensors) != len(self.shapes) or not tensors:
+            return None
+        t0 = tensors[0]
+        if t0.dtype != torch.float32 or not t0.is_cuda:
+            return None
+        st = t0.untyped_storage()
+        base_ptr = t0.data_ptr() - self.offsets[0] * 4
+        for t, o, s in zip(tensors, self.offsets, self.shapes):
+            if (
+                t.dtype != torch.float32
+                or tuple(t.shape) != s
+                or not t.is_contiguous()
+                or t.untyped_storage().data_ptr() != st.data_ptr()
+                or t.data_ptr() != base_ptr + 4 * o
+            ):
+                return None
+        start = (base_ptr - st.data_ptr()) // 4
+        if start < 0 or (start + self.numel) * 4 > st.nbytes():
+            return None
+        return torch.empty(0, dtype=torch.float32, device=t0.device).set_(
+            st, start, (self.numel,), (1,)
+        )
+
+
+class FlatParams:
+    """Live weights + gradient of one stage in flat device buffers."""
+
+    def __init__(self, layout: FlatLayout, device, data: torch.Tensor | None = None):
+        self.layout = layout
+        self.device = torch.device(device)
+        self.data = data if data is not None else layout.empty(self.device, zero=True)
+        self.grad = layout.empty(self.device, zero=True)
+
+    @classmethod
+    def from_tensors(cls, names, tensors, device) -> "FlatParams":
+        layout = FlatLayout(names, [tuple(t.shape) for t in tensors])
+        return cls(layout, device, layout.pack(tensors, device))
+
+    @property
+    def params(self) -> list[torch.Tensor]:
+        return self.layout.views(self.data)
+
+    @property
+    def grads(self) -> list[torch.Tensor]:
+        return self.layout.views(self.grad)
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+# ---- the optimizer state ---------------------------------------------------------
+
+
+class OptimizerState:
+    """Per-stage optimizer state (optim.py:46-59) over a named list of params.
+
+    step_count is the number of updates applied so far; the flat moment
+    buffers are lazily zero-initialised on the first step (optim.py:91-92,
+    103-105). `eager_checks=True` reproduces the reference's immediate
+    NumericError on a non-finite step (one host sync per step); with False
+    the flag accumulates on the device and `check_finite()` raises later.
+    """
+
+    def __init__(
+        self,
+        config: OptimizerConfig,
+        names: list[str],
+        *,
+        device: torch.device | str | None = None,
+        eager_checks: bool = True,
+        launch: _lib.po_launch | None = None,
+    ):
+        self.config = config
+        self.names = list(names)
+        self.step_count = 0
+        self.eager_checks = eager_checks
+        self._device = torch.device(device) if device is not None else None
+        self._layout: FlatLayout | None = None
+        self._s1: torch.Tensor | None = None  # sgdm buf | adam exp_avg
+        self._s2: torch.Tensor | None = None  # adam exp_avg_sq
+        self._bad: torch.Tensor | None = None
+        self._hp = config.hparams()
+        self._launch = launch
+        self._lib = _lib.load()
+        self._pending_check_step: int | None = None
+
+    # -- state plumbing ---------------------------------------------------------
+
+    @property
+    def device(self) -> torch.device:
+        if self._device is None:
+            if not torch.cuda.is_available():
+                raise _lib.LibraryMissing("PipeOptim kernels need a CUDA device (no CPU fallback)")
+            self._device = torch.device("cuda", torch.cuda.current_device())
+        return self._device
+
+    def _bind(self, layout: FlatLayout) -> None:
+        if self._layout is None:
+            if len(layout.shapes) != len(self.names):
+                raise ValueError(
+                    f"{len(layout.shapes)} params vs {len(self.names)} names"
+                )
+            self._layout = FlatLayout(self.names, layout.shapes)
+        elif self._layout != layout:
+            raise ValueError("parameter shapes changed between optimizer calls")
+
+    def _ensure_state(self) -> None:
+        if self._s1 is None:
+            self._s1 = self._layout.empty(self.device, zero=True)
+            if self.config.kind != "sgdm":
+                self._s2 = self._layout.empty(self.device, zero=True)
+        if self._bad is None:
+            self._bad = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=self.device)
+
+    def _state_views(self, buf):
+        if buf is None or self._layout is None:
+            return None
+        return self._layout.views(buf)
+
+    def _set_state(self, which: str, values) -> None:
+        if values is None:
+            setattr(self, which, None)
+            return
+        vals = [torch.as_tensor(v.a if hasattr(v, "a") else v) for v in values]
+        self._bind(FlatLayout(self.names, [tuple(v.shape) for v in vals]))
+        buf = getattr(self, which)
+        if buf is None:
+            buf = self._layout.empty(self.device, zero=True)
+            setattr(self, which, buf)
+        for dst, src in zip(self._layout.views(buf), vals):
+            dst.copy_(src)
+
+    @property
+    def momentum_buf(self):
+        return self._state_views(self._s1) if self.config.kind == "sgdm" else None
+
+    @momentum_buf.setter
+    def momentum_buf(self, values):
+        self._set_state("_s1", values)
+
+    @property
+    def exp_avg(self):
+        return self._state_views(self._s1) if self.config.kind != "sgdm" else None
+
+    @exp_avg.setter
+    def exp_avg(self, values):
+        self._set_state("_s1", values)
+
+    @property
+    def exp_avg_sq(self):
+        return self._state_views(self._s2) if self.config.kind != "sgdm" else None
+
+    @exp_avg_sq.setter
+    def exp_avg_sq(self, values):
+        self._set_state("_s2", values)
+
+    # -- non-finite reporting (optim.py:82-84) -----------------------------------
+
+    def _after_step(self) -> None:
+        if self.eager_checks:
+            self.check_finite()
+
+    def check_finite(self) -> None:
+        """Raise NumericError naming the first parameter whose update went
+        non-finite (flag set by the kernel); synchronises with the device."""
+        if self._bad is None:
+            return
+        idx = int(self._bad.item())
+        if idx != _INT64_MAX:
+            self._bad.fill_(_INT64_MAX)
+            name = self._layout.locate(idx)
+            raise NumericError(f"optimizer step produced non-finite values in {name}")
+
+    # -- fast in-place paths on a FlatParams (the runtime's hot path) ------------
+
+    def step_(self, flat: FlatParams, lr: float) -> None:
+        """K2: one update in place on flat.data from flat.grad."""
+        self._bind(flat.layout)
+        self._ensure_state()
+        rc = self._lib.po_step(
+            ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1),
+            _ptr(self._s2), None, flat.layout.numel, float(lr), self.step_count,
+            _ptr(self._bad), self._launch_ref(), _stream(flat.data.device),
+        )
+        _lib.check(rc, "po_step")
+        self._after_step()
+        self.step_count += 1
+
+    def predict_(self, flat: FlatParams, lr: float, steps_ahead: int, out: torch.Tensor) -> None:
+        """K1: out = W - (lr*s) * dir(state), dir read at t = step_count."""
+        if steps_ahead < 0:
+            raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
+        self._bind(flat.layout)
+        if self.step_count > 0:
+            self._ensure_state()
+        rc = self._lib.po_predict(
+            ctypes.byref(self._hp), _ptr(flat.data), _ptr(self._s1), _ptr(self._s2), _ptr(out),
+            flat.layout.numel, float(lr) * steps_ahead, self.step_count, self._launch_ref(),
+            _stream(flat.data.device),
+        )
+        _lib.check(rc, "po_predict")
+
+    def step_predict_(
+        self, flat: FlatParams, lr: float, lr_pred: float, steps_ahead: int, out: torch.Tensor
+    ) -> None:
+        """K3: step_ then predict_ on the just-updated state, in one HBM pass."""
+        if steps_ahead < 0:
+            raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
+        self._bind(flat.layout)
+        self._ensure_state()
+        rc = self._lib.po_step_predict(
+            ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1),
+            _ptr(self._s2), _ptr(out), flat.layout.numel, float(lr), float(lr_pred) * steps_ahead,
+            self.step_count, _ptr(self._bad), self._launch_ref(), _stream(flat.data.device),
+        )
+        _lib.check(rc, "po_step_predict")
+        self._after_step()
+        self.step_count += 1
+
+    def _launch_ref(self):
+        return ctypes.byref(self._launch) if self._launch is not None else None
+
+    # -- reference-shaped list API ------------------------------------------------
+
+    def _out(self, buf: torch.Tensor, host) -> list[torch.Tensor]:
+        views = self._layout.views(buf)
+        if host is None:
+            return views
+        return [v.to(host) for v in views]
+
+    def step(self, params, grads, lr: float):
+        """Apply one update; returns (new params, applied directions) with
+        new = old - lr*d (optim.py:63-87). Inputs are not mutated."""
+        if len(params) != len(grads) or len(params) != len(self.names):
+            raise ValueError(
+                f"step: got {len(params)} params, {len(grads)} grads, "
+                f"{len(self.names)} names"
+            )
+        params = [_as_tensor(p) for p in params]
+        grads = [_as_tensor(g) for g in grads]
+        layout = FlatLayout(self.names, [tuple(p.shape) for p in params])
+        self._bind(layout)
+        host = None if params[0].is_cuda else params[0].device
+        dev = params[0].device if params[0].is_cuda else self.device
+        w = self._layout.pack(params, dev)  # a new buffer: inputs stay untouched
+        g = self._layout.as_flat(grads) if host is None else None
+        if g is None:
+            g = self._layout.pack(grads, dev)
+        self._ensure_state()
+        dirs = self._layout.empty(dev)
+        rc = self._lib.po_step(
+            ctypes.byref(self._hp), _ptr(w), _ptr(g), _ptr(self._s1), _ptr(self._s2), _ptr(dirs),
+            self._layout.numel, float(lr), self.step_count, _ptr(self._bad), self._launch_ref(),
+            _stream(w.device),
+        )
+        _lib.check(rc, "po_step")
+        self.check_finite()  # the list API always raises like the reference
+        self.step_count += 1
+        return self._out(w, host), self._out(dirs, host)
+
+    def prediction_direction(self, params):
+        """Direction the next update is expected to take, read from the
+        buffers (optim.py:123-142): zeros before the first step, the momentum
+        buffer for sgdm, (m/bc1)/(sqrt(v/bc2)+eps) at t = step_count for
+        adam/adamw (no decoupled-decay term). Pure read."""
+        params = [_as_tensor(p) for p in params]
+        self._bind(FlatLayout(self.names, [tuple(p.shape) for p in params]))
+        host = None if params[0].is_cuda else params[0].device
+        dev = params[0].device if params[0].is_cuda else self.device
+        if self.step_count > 0 and self._s1 is None:
+            raise RuntimeError("prediction_direction: step_count > 0 but no optimizer state")
+        out = self._layout.empty(dev)
+        rc = self._lib.po_direction(
+            ctypes.byref(self._hp), _ptr(self._s1), _ptr(self._s2), _ptr(out),
+            self._layout.numel, self.step_count, self._launch_ref(), _stream(dev),
+        )
+        _lib.check(rc, "po_direction")
+        return self._out(out, host)
+
+
+def _as_tensor(x) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x
+    a = getattr(x, "a", x)  # a reference Matrix carries its array in .a
+    return torch.as_tensor(a)
+
+
+def predict_weights(params, lr: float, steps_ahead: int, directions) -> list[torch.Tensor]:
+    """Extrapolate parameters steps_ahead updates into the future: each w
+    becomes w - lr * steps_ahead * d (optim.py:145-155, Eq. (5)). Inputs are
+    not mutated."""
+    if steps_ahead < 0:
+        raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
+    if len(params) != len(directions):
+        raise ValueError(
+            f"predict_weights: {len(params)} params vs {len(directions)} directions"
+        )
+    if not params:
+        return []
+    params = [_as_tensor(p) for p in params]
+    directions = [_as_tensor(d) for d in directions]
+    names = [f"p{i}" for i in range(len(params))]
+    layout = FlatLayout(names, [tuple(p.shape) for p in params])
+    host = None if params[0].is_cuda else params[0].device
+    dev = params[0].device if params[0].is_cuda else torch.device("cuda", torch.cuda.current_device())
+    w = layout.as_flat(params) if host is None else None
+    if w is None:
+        w = layout.pack(params, dev)
+    d = layout.as_flat(directions) if host is None else None
+    if d is None:
+        d = layout.pack(directions, dev)
+    out = layout.empty(dev)
+    lib = _lib.load()
+    rc = lib.po_axpy_predict(
+        _ptr(w), _ptr(d), _ptr(out), layout.numel, float(lr) * steps_ahead, None, _stream(dev)
+    )
+    _lib.check(rc, "po_axpy_predict")
+    views = layout.views(out)
+    return views if host is None else [v.to(host) for v in views]
+
+
+def version_difference(depth: int, rank: int) -> int:
+    """Eq. (4): updates a stage applies between a mini-batch's forward and its
+    backward in 1F1B steady state, depth - rank - 1 (optim.py:158-167)."""
+    if depth < 1:
+        raise ValueError(f"depth must be >= 1, got {depth}")
+    if not 0 <= rank < depth:
+        raise ValueError(f"rank must be in [0, {depth}), got {rank}")
+    out = ctypes.c_int64(0)
+    _lib.check(_lib.load().po_version_difference(depth, rank, ctypes.byref(out)), "version_difference")
+    return int(out.value)

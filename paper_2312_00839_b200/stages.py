@@ -1,0 +1,304 @@
+"""Dense-MLP pipeline stages on the device, with the reference's weight-view
+semantics.
+
+Mirrors pkg/src/pipesim/stages.py: `LayerSpec`, `build_layers`,
+`partition_layers` (contiguous, earlier stages take the extra layer),
+`StageModel` (params [w0, b0, w1, b1, ...], w shaped (in, out) used as
+x @ w + b, version starting at 1), the per-(mb, micro) `ActivationStash`, and
+`stage_forward` / `stage_backward`.
+
+The semantics that matter for parity: the forward runs on
+whatever weights view the policy hands it (live or predicted W_hat) and
+stashes layer inputs and pre-activations; the backward computes
+dW = x^T dpre and db = colsum(dpre) from the stash, and the input gradient
+with the weights view given at BACKWARD time (live weights under PipeOptim,
+runtime.py:260-261, stages.py:200-208).
+
+B200 layout: a stage's parameters live in one flat fp32 buffer (FlatParams)
+so the optimizer/predictor kernels stream the whole stage in one launch; the
+backward writes parameter gradients straight into the flat gradient buffer's
+views (no separate accumulation pass for one micro-batch per update).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+
+from .errors import DimensionError, NumericError, StashError
+from .optim import FlatParams
+
+ACTIVATIONS = ("tanh", "relu", "linear")
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    index: int
+    in_dim: int
+    out_dim: int
+    activation: str
+
+    def __post_init__(self):
+        if self.activation not in ACTIVATIONS:
+            raise ValueError(f"unknown activation kind: {self.activation!r}")
+        if self.in_dim < 1 or self.out_dim < 1:
+            raise ValueError(
+                f"layer {self.index}: dims must be positive, got {self.in_dim}x{self.out_dim}"
+            )
+
+
+def build_layers(layer_dims: list[int], activations: list[str]) -> list[LayerSpec]:
+    """MLP layer specs from a dim chain (stages.py:48-60)."""
+    if len(layer_dims) < 2:
+        raise ValueError("layer_dims needs at least an input and an output dim")
+    if len(activations) != len(layer_dims) - 1:
+        raise ValueError(
+            f"expected {len(layer_dims) - 1} activations for {len(layer_dims)} dims, "
+            f"got {len(activations)}"
+        )
+    return [LayerSpec(i, a, b, act) for i, (a, b, act) in enumerate(zip(layer_dims, layer_dims[1:], activations))]
+
+
+def partition_layers(layers: list[LayerSpec], depth: int) -> list[list[LayerSpec]]:
+    """Contiguous split, sizes differ by <= 1, earlier stages take the extra
+    layer (stages.py:63-80)."""
+    if depth < 1:
+        raise ValueError(f"depth must be >= 1, got {depth}")
+    if depth > len(layers):
+        raise ValueError(f"cannot split {len(layers)} layers across {depth} stages")
+    q, r = divmod(len(layers), depth)
+    bounds = [0]
+    for k in range(depth):
+        bounds.append(bounds[-1] + q + (1 if k < r else 0))
+    return [layers[bounds[k] : bounds[k + 1]] for k in range(depth)]
+
+
+# An init provider maps a LayerSpec to (w (in, out), b (1, out)) — e.g. the
+# reference's per-layer Philox substreams for parity runs (stages.py:83-91),
+# or `torch_init` for synthetic throughput runs.
+InitFn = Callable[[LayerSpec], tuple]
+
+
+def torch_init(seed: int = 0, device="cpu") -> InitFn:
+    """N(0, 1) * in_dim^-1/2 weights, zero bias, one generator per layer so the
+    values do not depend on the partition (same distribution as stages.py:83-91,
+    different RNG)."""
+
+    def init(spec: LayerSpec):
+        g = torch.Generator(device=device)
+        g.manual_seed(seed * 1_000_003 + spec.index)
+        w = torch.randn(spec.in_dim, spec.out_dim, generator=g, device=device) * spec.in_dim ** -0.5
+        return w, torch.zeros(1, spec.out_dim, device=device)
+
+    return init
+
+
+@dataclass
+class StashEntry:
+    version: int
+    layer_inputs: list
+    pre_acts: list
+
+
+class ActivationStash:
+    """Forward context per (mb, micro) until the matching backward (stages.py:101-120)."""
+
+    def __init__(self):
+        self._entries: dict[tuple[int, int], StashEntry] = {}
+        self.peak = 0
+
+    def put(self, key, entry: StashEntry) -> None:
+        if key in self._entries:
+            raise StashError(f"stash already holds an entry for {key}")
+        self._entries[key] = entry
+        self.peak = max(self.peak, len(self._entries))
+
+    def pop(self, key) -> StashEntry:
+        try:
+            return self._entries.pop(key)
+        except KeyError:
+            raise StashError(f"no stash entry for {key}") from None
+
+    def __len__(self) -> int:
+        return len(self._entries)
+
+
+class StageModel:
+    """One pipeline stage: its layers, live parameters in a flat device buffer,
+    a version counter (starts at 1, +1 per update) and the activation stash."""
+
+    def __init__(self, rank: int, layers: list[LayerSpec], init: InitFn, device=None):
+        self.rank = rank
+        self.layers = list(layers)
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        names, tensors = [], []
+        for spec in self.layers:
+            w, b = init(spec)
+            w = torch.as_tensor(getattr(w, "a", w))
+            b = torch.as_tensor(getattr(b, "a", b))
+            if tuple(w.shape) != (spec.in_dim, spec.out_dim) or tuple(b.shape) != (1, spec.out_dim):
+                raise DimensionError(
+                    f"layer {spec.index}: init shapes {tuple(w.shape)}, {tuple(b.shape)} "
+                    f"vs ({spec.in_dim}, {spec.out_dim}), (1, {spec.out_dim})"
+                )
+            names += [f"layer{spec.index}.w", f"layer{spec.index}.b"]
+            tensors += [w, b]
+        self.param_names = names
+        self.flat = FlatParams.from_tensors(names, tensors, self.device)
+        self.version = 1
+        self.stash = ActivationStash()
+
+    @property
+    def params(self) -> list[torch.Tensor]:
+        return self.flat.params
+
+    @params.setter
+    def params(self, values) -> None:
+        for dst, src in zip(self.flat.params, values):
+            if dst.data_ptr() != src.data_ptr():
+                dst.copy_(src)
+
+    @property
+    def in_dim(self) -> int:
+        return self.layers[0].in_dim
+
+    @property
+    def out_dim(self) -> int:
+        return self.layers[-1].out_dim
+
+    @property
+    def numel(self) -> int:
+        return self.flat.layout.numel
+
+
+def build_stages(layers: list[LayerSpec], depth: int, init: InitFn, device=None) -> list[StageModel]:
+    return [StageModel(k, group, init, device) for k, group in enumerate(partition_layers(layers, depth))]
+
+
+def _activate(pre: torch.Tensor, kind: str) -> torch.Tensor:
+    if kind == "tanh":
+        return torch.tanh(pre)
+    if kind == "relu":
+        return torch.relu(pre)
+    return pre
+
+
+def _activation_grad_mul(g: torch.Tensor, pre: torch.Tensor, kind: str) -> torch.Tensor:
+    """g * act'(pre) (linalg.py:185-194 then hadamard)."""
+    if kind == "tanh":
+        t = torch.tanh(pre)
+        return g * (1.0 - t * t)
+    if kind == "relu":
+        return g * (pre > 0.0).to(g.dtype)
+    return g
+
+
+def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int,
+                  check_finite: bool = True, finite_flags: torch.Tensor | None = None,
+                  flag_index: int = 0) -> torch.Tensor:
+    """Run the stage's layers on x with the given weights view; stash the
+    per-layer inputs and pre-activations (stages.py:156-184).
+
+    check_finite=True raises NumericError immediately (host sync); otherwise,
+    if `finite_flags` is given, a device-side all-finite bit is recorded at
+    `flag_index` and checked later by the runtime.
+    """
+    if x.shape[1] != stage.in_dim:
+        raise DimensionError(f"stage {stage.rank}: input has {x.shape[1]} cols, expected {stage.in_dim}")
+    inputs, pres = [], []
+    h = x
+    for i, spec in enumerate(stage.layers):
+        w, b = weights[2 * i], weights[2 * i + 1]
+        inputs.append(h)
+        pre = torch.addmm(b, h, w)
+        pres.append(pre)
+        h = _activate(pre, spec.activation)
+    if check_finite:
+        if not bool(torch.isfinite(h).all()):
+            bad = torch.nonzero(~torch.isfinite(h))[0].tolist()
+            raise NumericError(
+                f"non-finite value in stage {stage.rank} forward output at entry ({bad[0]}, {bad[1]})"
+            )
+    elif finite_flags is not None:
+        finite_flags[flag_index] = torch.isfinite(h).all()
+    stage.stash.put(key, StashEntry(version, inputs, pres))
+    return h
+
+
+def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
+                   accumulate: bool = False, need_input_grad: bool = True):
+    """Backpropagate through the stash (stages.py:187-209). Parameter grads go
+    into stage.flat.grad's views (overwritten, or added when `accumulate`);
+    the input gradient uses `weights` — the view at BACKWARD time.
+    Returns (grad wrt stage input or None, list of parameter-grad views)."""
+    entry = stage.stash.pop(key)
+    gviews = stage.flat.grads
+    g = grad_out
+    for i in reversed(range(len(stage.layers))):
+        spec = stage.layers[i]
+        dpre = _activation_grad_mul(g, entry.pre_acts[i], spec.activation)
+        x = entry.layer_inputs[i]
+        gw, gb = gviews[2 * i], gviews[2 * i + 1]
+        if accumulate:
+            gw.addmm_(x.t(), dpre)
+            gb.add_(dpre.sum(dim=0, keepdim=True))
+        else:
+            torch.mm(x.t(), dpre, out=gw)
+            torch.sum(dpre, dim=0, keepdim=True, out=gb)
+        if i > 0 or need_input_grad:
+            g = torch.mm(dpre, weights[2 * i].t())
+        else:
+            g = None
+    return g, gviews
+
+
+def network_forward(stages: list[StageModel], params_per_stage, x: torch.Tensor) -> torch.Tensor:
+    """Chained forward over all stages with explicit weights; no stash (stages.py:212-218)."""
+    h = x
+    for stage, weights in zip(stages, params_per_stage):
+        for i, spec in enumerate(stage.layers):
+            h = _activate(torch.addmm(weights[2 * i + 1], h, weights[2 * i]), spec.activation)
+    return h
+
+
+def params_by_layer(stages: list[StageModel]) -> dict[int, tuple[torch.Tensor, torch.Tensor]]:
+    """Live (w, b) per global layer index, partition independent (stages.py:221-227)."""
+    out = {}
+    for stage in stages:
+        p = stage.params
+        for i, spec in enumerate(stage.layers):
+            out[spec.index] = (p[2 * i], p[2 * i + 1])
+    return out
+
+
+# ---- losses (linalg.py:212-241) ----------------------------------------------------------------
+
+LOSS_KINDS = ("mse", "softmax_xent")
+
+
+def loss_and_grad(pred: torch.Tensor, target: torch.Tensor, kind: str):
+    """(loss as a 0-d device tensor, grad wrt pred).
+
+    mse: mean over all entries of (pred - target)^2, grad 2*(pred - target)/numel.
+    softmax_xent: logits vs one-hot target, row-max-shifted softmax, mean row
+    cross-entropy, grad (softmax - target)/rows.
+    """
+    if pred.shape != target.shape:
+        raise DimensionError(f"loss_and_grad: shapes differ: {tuple(pred.shape)} vs {tuple(target.shape)}")
+    if kind == "mse":
+        diff = pred - target
+        n = diff.numel()
+        loss = (diff * diff).sum() / n
+        grad = 2.0 * diff / n
+    elif kind == "softmax_xent":
+        z = pred - pred.max(dim=1, keepdim=True).values
+        ez = torch.exp(z)
+        sm = ez / ez.sum(dim=1, keepdim=True)
+        picked = (sm * target).sum(dim=1)
+        loss = (-torch.log(picked)).mean()
+        grad = (sm - target) / pred.shape[0]
+    else:
+        raise ValueError(f"unknown loss kind: {kind!r}")
+    return loss, grad
