@@ -1,0 +1,405 @@
+"""PipeOptim hot-path benchmark on B200 — prints ONE JSON line (rank 0).
+
+Workload (a "step"): one fused weight-predict + optimizer-step pass (K3,
+Adam, s = 3, t > 0) over one stage's flat fp32 buffers of N = 1e9 parameters
+— BASELINE.json configs[4] at its 1B headline point, the configuration the
+north-star kernel target (>= 80% of ~8 TB/s at 1B params) is quoted on.
+Inputs (W, G, m, v = 16 GB) are larger than L2 (126 MB) so no flush is
+needed between steps.
+
+  value   whole-job algorithmic GB/s: N * 32 B * ranks / step
+          time, device-timed with CUDA events, max over ranks.
+  e2e     the same metric through the reference-facing host-buffer API
+          (HostStreamer: pinned host W and G in, W' and W_hat out, PCIe copies
+          inside the timed region; optimizer state device-resident).
+  roofline  K3's achieved GB/s vs MEASURED_PEAKS.json hbm_gbs; `traffic` is
+          ncu's dram bytes per launch from profiles/ when captured.
+  cpu_baseline  the reference's algorithm (oracle/c, float64, OpenMP on every
+          host core) on a bounded sample, same per-parameter byte accounting.
+  pipeline  the first metric clause: 1F1B samples/s on config 1 (4-stage
+          3072-1024^3-10 MLP, B=128, Adam), prediction on vs off.
+
+--gpus N (torchrun, one process per GPU): the kernel is per-stage state, so N
+ranks are N independent stages ("replicas only", scaling weak); the pipeline
+leg then runs the real N-stage NCCL pipeline.
+
+--impl reference: the reference's CPU implementation (the oracle port; the
+reference is pure Python and cannot travel) timed on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_PARAM = {"sgdm": 24, "adam": 32, "adamw": 32}  # K3, SURVEY.md §8d
+METRIC = "weight-predict+step HBM GB/s (fused K3; pipeline samples/sec in `pipeline`)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-params", type=float, default=1e9)
+    ap.add_argument("--kind", choices=["sgdm", "adam", "adamw"], default="adam")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--pipeline-batches", type=int, default=64)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---- clocks -------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        loaded = [x for x in sm if smax and x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- helpers --------------------------------------------------------------------------------
+
+
+def measured_peak():
+    try:
+        j = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per K3 launch from the committed ncu capture, if any."""
+    p = ROOT / "profiles" / "k3_traffic.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return None
+
+
+def cpu_baseline(kind: str, budget_s: float = 12.0, n: int = 1 << 26):
+    """The reference algorithm (oracle/c float64, OpenMP) on a bounded sample."""
+    import numpy as np
+
+    from oracle import c_oracle
+
+    c_oracle.build()
+    rng = np.random.default_rng(0)
+    w = rng.normal(0, 0.02, n)
+    g = rng.normal(0, 1e-2, n)
+    m = rng.normal(0, 1e-3, n)
+    v = rng.normal(0, 1e-2, n) ** 2
+    wh = np.empty(n)
+    hp = c_oracle.hp(kind)
+    s2 = None if kind == "sgdm" else v
+    c_oracle.step_predict(hp, w, g, m, s2, wh, 1e-3, 3e-3, 10)  # warm (page-in)
+    times, t_start, t = [], time.perf_counter(), 11
+    while time.perf_counter() - t_start < budget_s or len(times) < 3:
+        t0 = time.perf_counter()
+        c_oracle.step_predict(hp, w, g, m, s2, wh, 1e-3, 3e-3, t)
+        times.append(time.perf_counter() - t0)
+        t += 1
+    per = statistics.median(times)
+    return {
+        "value": round(BYTES_PER_PARAM[kind] * n / per / 1e9, 2),
+        "unit": "GB/s",
+        "cores": c_oracle.threads(),
+        "kind": "port",
+        "sample": (f"oracle/c/optim_oracle.c step+predict ({kind}, float64 like the reference, OpenMP) on "
+                   f"{n} params x {len(times)} reps, median {per * 1e3:.1f} ms; GB/s counted with the same "
+                   f"{BYTES_PER_PARAM[kind]} B/param as the GPU so ratios are params/s ratios"),
+        "params_per_s": round(n / per, 1),
+    }
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    base = cpu_baseline(args.kind, budget_s=max(3.0, 2.0 * args.steps / 10))
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": base["value"],
+        "unit": "GB/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"K3 step+predict {args.kind}, sample of 2^26 params on the host cores "
+                               f"(reference algorithm, oracle port; the reference is pure Python)"},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "vs_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm --------------------------------------------------------------------------------
+
+
+def kernel_leg(args, torch, dist, rank, world, device):
+    from paper_2312_00839_b200 import _lib
+    from paper_2312_00839_b200.optim import OptimizerConfig
+
+    lib = _lib.load()
+    n = int(args.n_params)
+    kind = args.kind
+    gen = torch.Generator(device=device)
+    mk = lambda seed, scale: torch.randn(n, device=device, generator=gen.manual_seed(seed)) * scale  # noqa: E731
+    w = mk(0, 0.02)
+    g = mk(1, 1e-2)
+    m = mk(2, 1e-3)
+    v = mk(3, 1e-2).square_() if kind != "sgdm" else None
+    w_hat = torch.empty(n, device=device)
+    hp = OptimizerConfig(kind).hparams()
+    stream = torch.cuda.current_stream(device)
+    lr, s = 1e-3, 3
+    t = [10]
+
+    def launch():
+        rc = lib.po_step_predict(ctypes.byref(hp), w.data_ptr(), g.data_ptr(), m.data_ptr(),
+                                 None if v is None else v.data_ptr(), w_hat.data_ptr(), n, lr, lr * s, t[0], None,
+                                 None, stream.cuda_stream)
+        _lib.check(rc, "po_step_predict")
+        t[0] += 1
+
+    for _ in range(args.warmup):
+        launch()
+    torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(device.index if device.index is not None else 0)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(device)
+    e0.record(stream)
+    for _ in range(args.steps):
+        launch()
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = ms
+    if world > 1:
+        tt = torch.tensor([ms], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_max = float(tt.item())
+    bytes_step = BYTES_PER_PARAM[kind] * n
+    del w, g, m, v, w_hat
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms_max, "ms_local": ms, "gbs_per_rank": bytes_step / (ms * 1e-3) / 1e9,
+            "value": world * bytes_step / (ms_max * 1e-3) / 1e9, "launches": args.steps, "clocks": clk, "n": n}
+
+
+def e2e_leg(args, torch, dist, world, device):
+    """Same metric through the host-buffer API: pinned host W, G in; W', W_hat out."""
+    from paper_2312_00839_b200.optim import HostStreamer, OptimizerConfig, OptimizerState
+
+    n = int(args.n_params)
+    kind = args.kind
+    pin = lambda: torch.empty(n, dtype=torch.float32).pin_memory()  # noqa: E731
+    w_h, g_h, wo_h, wh_h = pin(), pin(), pin(), pin()
+    w_h.normal_(0, 0.02)
+    g_h.normal_(0, 1e-2)
+    opt = OptimizerState(OptimizerConfig(kind), ["stage.flat"], device=device, eager_checks=False)
+    streamer = HostStreamer(device)
+    launches = [0]
+
+    def step():
+        launches[0] += streamer.step_predict(opt, w_h, g_h, 1e-3, 1e-3, 3, wo_h, wh_h)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    torch.cuda.synchronize(device)
+    if world > 1:
+        dist.barrier()
+    launches[0] = 0
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.e2e_steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize(device)
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1) / args.e2e_steps
+    if world > 1:
+        tt = torch.tensor([ms], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    opt.check_finite()
+    res = {
+        "value": round(world * BYTES_PER_PARAM[kind] * n / (ms * 1e-3) / 1e9, 2),
+        "unit": "GB/s",
+        "h2d_bytes_per_step": 8 * n,
+        "d2h_bytes_per_step": 8 * n,
+        "ms_per_step": round(ms, 3),
+        "wall_s": round(wall, 3),
+        "path": "OptimizerState + HostStreamer.step_predict: pinned host W,G -> device (chunked, 3 streams) -> "
+                "K3 against device-resident m,v -> W', W_hat -> host",
+        "launches": launches[0],
+    }
+    del w_h, g_h, wo_h, wh_h, streamer, opt
+    torch.cuda.empty_cache()
+    return res
+
+
+def pipeline_leg(args, torch, dist, rank, world, device):
+    """Config 1 through the 1F1B runner: samples/s with prediction on vs off."""
+    if world == 1:
+        from paper_2312_00839_b200.bench_pipeline import single_gpu_pipeline
+
+        return single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches)
+    from paper_2312_00839_b200.bench_pipeline import multi_gpu_pipeline
+
+    return multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches)
+
+
+def ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (there is no CPU fallback for the PipeOptim kernels)")
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    kern = kernel_leg(args, torch, dist, rank, world, device)
+    e2e = None if args.no_e2e else e2e_leg(args, torch, dist, world, device)
+    pipe = None
+    if not args.no_pipeline:
+        try:
+            pipe = pipeline_leg(args, torch, dist, rank, world, device)
+        except Exception as exc:  # reported, never silently dropped
+            pipe = {"error": f"{type(exc).__name__}: {exc}"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.kind)
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic()
+    gbs = kern["gbs_per_rank"]
+    launches = kern["launches"]  # our kernels inside the timed region of `value` (one K3 per step)
+    line = {
+        "metric": METRIC,
+        "value": round(kern["value"], 2),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(kern["ms_per_step"], 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (torch.Generator N(0,.02) W, N(0,1e-2) G, N(0,1e-3) m, N(0,1e-2)^2 v)",
+        "config": {
+            "workload": f"K3 fused {args.kind} step + weight prediction (s=3) over {kern['n']} fp32 params per GPU "
+                        f"(BASELINE configs[4] at 1B; one stage per GPU, replicas only)",
+            "n_params_per_gpu": kern["n"],
+            "bytes_per_param": BYTES_PER_PARAM[args.kind],
+            "l2": "inputs (16 GB) >> 126 MB L2; no flush needed",
+            "parallelism": f"replicas{world}",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": round(gbs, 1),
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": round(gbs / peak, 4),
+            "frac_of_8tbs": round(gbs / 8000.0, 4),
+            "peak_source": peak_src,
+            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+            "traffic_note": (f"ncu dram__bytes_read+write per launch at n={traffic.get('n')}" if traffic else
+                             "no ncu capture committed"),
+            "kernel": "po_stream_kernel<ADAM, STEP_PREDICT> (K3)",
+            "kernel_ms": round(kern["ms_per_step"], 4),
+        },
+        "clocks": kern["clocks"],
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "pipeline": pipe,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

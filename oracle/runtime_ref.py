@@ -43,7 +43,7 @@ def _act_grad(pre, kind):
         t = np.tanh(pre)
         return 1.0 - t * t
     if kind == "relu":
-        return (pre > 0.0).astype(np.float64)
+        return (pre > 0.0).astype(pre.dtype)
     return np.ones_like(pre)
 
 

@@ -433,6 +433,83 @@ class OptimizerState:
         return self._out(out, host)
 
 
+class HostStreamer:
+    """Host-buffer path for one flat stage: pinned host W and G stream to the
+    device in chunks, K3 runs on each chunk against the device-resident
+    optimizer state, and the updated W and the prediction W_hat stream back —
+    H2D, compute and D2H on three streams with `slots`-deep buffering so the
+    PCIe transfers in both directions overlap each other and the kernel.
+    This is what a caller that keeps parameters on the host sees end to end.
+    """
+
+    def __init__(self, device, chunk_elems: int = 1 << 25, slots: int = 3):
+        self.device = torch.device(device)
+        self.chunk = int(chunk_elems)
+        self.slots = int(slots)
+        mk = lambda: [torch.empty(self.chunk, dtype=torch.float32, device=self.device) for _ in range(self.slots)]  # noqa: E731
+        self.dw, self.dg, self.dwh = mk(), mk(), mk()
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_comp = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+        self.ev_in = [torch.cuda.Event() for _ in range(self.slots)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(self.slots)]
+        self.ev_free = [None] * self.slots
+
+    def step_predict(self, opt: "OptimizerState", w_host: torch.Tensor, g_host: torch.Tensor, lr: float,
+                     lr_pred: float, steps_ahead: int, w_out: torch.Tensor, w_hat_out: torch.Tensor) -> int:
+        """K3 over host buffers (1-D fp32, pinned). Returns the kernel launch count."""
+        n = w_host.numel()
+        if steps_ahead < 0:
+            raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
+        opt._bind(FlatLayout(opt.names, [(n,)]))
+        opt._ensure_state()
+        n_chunks = -(-n // self.chunk)
+        bad = torch.full((n_chunks,), _INT64_MAX, dtype=torch.int64, device=self.device)
+        cur = torch.cuda.current_stream(self.device)
+        for s in (self.s_in, self.s_comp, self.s_out):
+            s.wait_stream(cur)
+        c_pred = float(lr_pred) * steps_ahead
+        hp = ctypes.byref(opt._hp)
+        for i in range(n_chunks):
+            k = i % self.slots
+            lo = i * self.chunk
+            m = min(self.chunk, n - lo)
+            with torch.cuda.stream(self.s_in):
+                if self.ev_free[k] is not None:
+                    self.s_in.wait_event(self.ev_free[k])
+                self.dw[k][:m].copy_(w_host[lo : lo + m], non_blocking=True)
+                self.dg[k][:m].copy_(g_host[lo : lo + m], non_blocking=True)
+                self.ev_in[k].record(self.s_in)
+            self.s_comp.wait_event(self.ev_in[k])
+            s1 = opt._s1[lo:]
+            s2 = opt._s2[lo:] if opt._s2 is not None else None
+            rc = opt._lib.po_step_predict(
+                hp, _ptr(self.dw[k]), _ptr(self.dg[k]), _ptr(s1), _ptr(s2), _ptr(self.dwh[k]), m,
+                float(lr), c_pred, opt.step_count, bad[i:].data_ptr(), opt._launch_ref(),
+                self.s_comp.cuda_stream,
+            )
+            _lib.check(rc, "po_step_predict")
+            self.ev_comp[k].record(self.s_comp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_comp[k])
+                w_out[lo : lo + m].copy_(self.dw[k][:m], non_blocking=True)
+                w_hat_out[lo : lo + m].copy_(self.dwh[k][:m], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_out)
+                self.ev_free[k] = ev
+        cur.wait_stream(self.s_out)
+        if opt.eager_checks:
+            cur.synchronize()
+            b = bad.cpu()
+            for i, v in enumerate(b.tolist()):
+                if v != _INT64_MAX:
+                    raise NumericError(
+                        f"optimizer step produced non-finite values in {opt.names[0]} (index {i * self.chunk + v})"
+                    )
+        opt.step_count += 1
+        return n_chunks
+
+
 def _as_tensor(x) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x

@@ -1,0 +1,194 @@
+"""The reference-shaped optimizer API on the device (pkg/tests/test_optim.py,
+re-run against paper_2312_00839_b200.optim). Values are fp32 on the device,
+so the reference's 1e-14 fp64 tolerances become fp32-scale ones."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FROZEN_SGDM_WD_TRAJ = [0.85, 0.5725, 0.19412499999999994]
+FROZEN_SGDM_WD_V = 3.7837500000000004
+FROZEN_ADAM_TRAJ = [0.400000001, 0.43661035347207483, 0.45027941967382146, 0.41086943043487656, 0.3926517886119052]
+FROZEN_ADAM_DELTA_AFTER_5 = 0.18217641822971373
+FROZEN_ADAMW_TRAJ = [0.98900000005, 0.9853476296701932, 0.9809579905841741]
+FROZEN_ADAMW_DELTA_AFTER_3 = 0.34042914563488874
+F32 = 2e-7
+
+
+def T(v):
+    import torch
+
+    return torch.tensor([[float(v)]], dtype=torch.float32, device="cuda")
+
+
+def run_steps(cfg, w0, gs, lr):
+    from paper_2312_00839_b200.optim import OptimizerState
+
+    st = OptimizerState(cfg, ["p"])
+    params = [T(w0)]
+    traj = []
+    for g in gs:
+        params, _ = st.step(params, [T(g)], lr)
+        traj.append(float(params[0][0, 0]))
+    return st, params, traj
+
+
+def cfgs():
+    from paper_2312_00839_b200.optim import OptimizerConfig
+
+    return OptimizerConfig
+
+
+def test_sgdm_frozen():
+    C = cfgs()
+    st, _, traj = run_steps(C("sgdm", momentum=0.9, weight_decay=0.5), 1.0, [1.0] * 3, 0.1)
+    assert np.allclose(traj, FROZEN_SGDM_WD_TRAJ, rtol=0, atol=F32 * 4)
+    assert abs(float(st.momentum_buf[0][0, 0]) - FROZEN_SGDM_WD_V) <= 4 * F32 * FROZEN_SGDM_WD_V
+
+
+def test_adam_frozen_and_read():
+    C = cfgs()
+    st, params, traj = run_steps(C("adam"), 0.5, [1.0, -2.0, 0.5, 3.0, -1.0], 0.1)
+    assert np.allclose(traj, FROZEN_ADAM_TRAJ, rtol=0, atol=1e-6)
+    assert abs(float(st.prediction_direction(params)[0][0, 0]) - FROZEN_ADAM_DELTA_AFTER_5) <= 1e-6
+
+
+def test_adamw_frozen_and_read_excludes_decay():
+    C = cfgs()
+    st, params, traj = run_steps(C("adamw", decoupled_decay=0.1), 1.0, [2.0, -1.0, 0.5], 0.01)
+    assert np.allclose(traj, FROZEN_ADAMW_TRAJ, rtol=0, atol=1e-6)
+    assert abs(float(st.prediction_direction(params)[0][0, 0]) - FROZEN_ADAMW_DELTA_AFTER_3) <= 1e-6
+
+
+def test_degenerate_sgd_and_first_adam_step():
+    C = cfgs()
+    _, params, _ = run_steps(C("sgdm", momentum=0.0, weight_decay=0.0), 1.0, [0.5], 0.1)
+    assert abs(float(params[0][0, 0]) - 0.95) <= F32
+    from paper_2312_00839_b200.optim import OptimizerState
+
+    st = OptimizerState(C("adam"), ["p"])
+    _, dirs = st.step([T(0.0)], [T(2.0)], 0.001)
+    assert abs(float(dirs[0][0, 0]) - 1.0) <= 1e-6
+
+
+def test_zero_read_before_first_step_and_pure_read():
+    import torch
+
+    from paper_2312_00839_b200.optim import OptimizerState
+
+    C = cfgs()
+    for kind in ("sgdm", "adam", "adamw"):
+        st = OptimizerState(C(kind), ["a", "b"])
+        dirs = st.prediction_direction([torch.zeros(2, 2, device="cuda"), torch.zeros(1, 2, device="cuda")])
+        assert all(float(d.abs().max()) == 0.0 for d in dirs)
+    st = OptimizerState(C("adam"), ["p"])
+    params, _ = st.step([T(1.0)], [T(0.7)], 0.01)
+    before = (st.step_count, st.exp_avg[0].clone(), st.exp_avg_sq[0].clone())
+    r1 = st.prediction_direction(params)
+    r2 = st.prediction_direction(params)
+    assert torch.equal(r1[0], r2[0])
+    assert before[0] == st.step_count and torch.equal(before[1], st.exp_avg[0])
+
+
+def test_predict_weights_values_and_linearity():
+    import torch
+
+    from paper_2312_00839_b200.optim import predict_weights
+
+    (out,) = predict_weights([T(1.0)], 0.1, 3, [T(0.5)])
+    assert abs(float(out[0, 0]) - 0.85) <= F32
+    g = torch.Generator(device="cuda").manual_seed(9)
+    p = [torch.randn(3, 3, device="cuda", generator=g)]
+    d = [torch.randn(3, 3, device="cuda", generator=g)]
+    assert torch.equal(predict_weights(p, 0.1, 0, d)[0], p[0])
+    p1, p2, p3 = (predict_weights(p, 0.05, s, d)[0] for s in (1, 2, 3))
+    assert float(((p2 - p1) - (p3 - p2)).abs().max()) <= 1e-6
+    with pytest.raises(ValueError):
+        predict_weights(p, 0.1, -1, d)
+    with pytest.raises(ValueError):
+        predict_weights(p, 0.1, 1, d + d)
+
+
+@pytest.mark.parametrize("s", [1, 2, 3])
+def test_prediction_exact_at_momentum_fixed_point(s):
+    from paper_2312_00839_b200.optim import OptimizerState, predict_weights
+
+    C = cfgs()
+    u, g, lr = 0.9, 0.8, 0.05
+    st = OptimizerState(C("sgdm", momentum=u, weight_decay=0.0), ["p"])
+    st.momentum_buf = [T(g / (1 - u))]
+    st.step_count = 1
+    params = [T(2.0)]
+    pred = predict_weights(params, lr, s, st.prediction_direction(params))
+    walk = [T(2.0)]
+    for _ in range(s):
+        walk, _ = st.step(walk, [T(g)], lr)
+    assert abs(float(pred[0][0, 0]) - float(walk[0][0, 0])) <= 1e-6
+
+
+@pytest.mark.parametrize("kind", ["sgdm", "adam", "adamw"])
+def test_telescoping(kind):
+    import torch
+
+    from paper_2312_00839_b200.optim import OptimizerState
+
+    C = cfgs()
+    gen = torch.Generator(device="cuda").manual_seed(31)
+    st = OptimizerState(C(kind), ["p"])
+    w0 = torch.randn(8, 8, device="cuda", generator=gen)
+    params = [w0.clone()]
+    total = torch.zeros(8, 8, dtype=torch.float64, device="cuda")
+    for _ in range(100):
+        params, dirs = st.step(params, [torch.randn(8, 8, device="cuda", generator=gen)], 0.01)
+        total += dirs[0].double()
+    recon = w0.double() - 0.01 * total
+    assert float((recon - params[0].double()).abs().max()) <= 1e-5
+
+
+@pytest.mark.parametrize("kind", ["sgdm", "adam"])
+def test_applied_direction_equals_read(kind):
+    import torch
+
+    from paper_2312_00839_b200.optim import OptimizerState
+
+    C = cfgs()
+    gen = torch.Generator(device="cuda").manual_seed(13)
+    st = OptimizerState(C(kind, weight_decay=0.0), ["p"])
+    params = [torch.randn(4, 4, device="cuda", generator=gen)]
+    for _ in range(20):
+        params, dirs = st.step(params, [torch.randn(4, 4, device="cuda", generator=gen)], 0.01)
+        assert torch.equal(st.prediction_direction(params)[0], dirs[0])
+
+
+def test_step_aborts_on_non_finite_naming_parameter():
+    from paper_2312_00839_b200.errors import NumericError
+    from paper_2312_00839_b200.optim import OptimizerState
+
+    C = cfgs()
+    st = OptimizerState(C("sgdm", weight_decay=0.0), ["layer0.w", "layer2.w"])
+    with pytest.raises(NumericError) as exc:
+        st.step([T(1.0), T(1.0)], [T(0.0), T(float("inf"))], 0.1)
+    assert "layer2.w" in str(exc.value)
+    assert st.step_count == 0
+
+
+def test_host_buffers_round_trip():
+    """CPU tensors in, CPU tensors out: the host-buffer (end-to-end) path."""
+    import torch
+
+    from oracle import optim_ref as R
+    from paper_2312_00839_b200.optim import OptimizerState
+
+    C = cfgs()
+    rng = np.random.default_rng(4)
+    shapes = [(64, 33), (1, 33), (33, 10)]
+    ps = [rng.normal(0, 0.05, s).astype(np.float32) for s in shapes]
+    gs = [rng.normal(0, 0.01, s).astype(np.float32) for s in shapes]
+    st = OptimizerState(C("adamw"), ["a", "b", "c"])
+    new, dirs = st.step([torch.from_numpy(p) for p in ps], [torch.from_numpy(g) for g in gs], 1e-3)
+    assert all(not t.is_cuda for t in new)
+    orc = R.OracleOptimizer(R.Hyper("adamw"), ["a", "b", "c"])
+    want, _ = orc.step([p.astype(np.float64) for p in ps], [g.astype(np.float64) for g in gs], 1e-3)
+    for a, b in zip(new, want):
+        assert R.inf_norm_rel(a.double().numpy(), b) <= 1e-6

@@ -1,0 +1,149 @@
+"""The one-process-per-GPU 1F1B runner's host logic (per-rank programs,
+grouped neighbour exchanges, version bookkeeping, loss/record collection) on
+CPU with the gloo backend and world_size 2 and 4.
+
+The device kernels are not available on CPU, so these tests give the runner a
+torch stand-in optimizer defined HERE (the reference formulas in fp64 torch
+ops) — test infrastructure only; the product path has no CPU optimizer.
+The B200 run of the same runner over NCCL is covered by bench.py --gpus N.
+"""
+
+import json
+import os
+import socket
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import optim_ref, rng_ref, runtime_ref
+
+DIMS = [4, 6, 6, 6, 6, 5, 3]
+ACTS = ["tanh"] * 5 + ["linear"]
+
+
+class StandInOptimizer:
+    """CPU stand-in exposing the runner-facing surface of OptimizerState
+    (step_ / predict_ / step_predict_ / check_finite) in float64 torch."""
+
+    def __init__(self, kind, names, lr_eps=1e-8):
+        self.kind, self.names = kind, names
+        self.config = optim_ref.Hyper(kind, weight_decay=0.0)
+        self.step_count = 0
+        self.eager_checks = False
+        self.s1 = self.s2 = None
+
+    def _dir(self, t):
+        h = self.config
+        if self.kind == "sgdm":
+            return self.s1
+        bc1, bc2 = 1.0 - h.beta1 ** t, 1.0 - h.beta2 ** t
+        return (self.s1 / bc1) / (torch.sqrt(self.s2 / bc2) + h.eps)
+
+    def step_(self, flat, lr):
+        h = self.config
+        w = flat.data.double()
+        g = flat.grad.double()
+        if self.s1 is None:
+            self.s1 = torch.zeros_like(w)
+            self.s2 = torch.zeros_like(w)
+        if self.kind == "sgdm":
+            self.s1 = h.momentum * self.s1 + (1.0 - h.dampening) * (g + h.weight_decay * w)
+            d = self.s1
+        else:
+            self.s1 = h.beta1 * self.s1 + (1.0 - h.beta1) * g
+            self.s2 = h.beta2 * self.s2 + (1.0 - h.beta2) * (g * g)
+            d = self._dir(self.step_count + 1)
+            if self.kind == "adamw":
+                d = d + h.decoupled_decay * w
+        flat.data.copy_(w - lr * d)
+        self.step_count += 1
+
+    def predict_(self, flat, lr, s, out):
+        if self.step_count == 0:
+            out.copy_(flat.data)
+        else:
+            out.copy_(flat.data.double() - (lr * s) * self._dir(self.step_count))
+
+    def step_predict_(self, flat, lr, lr_pred, s, out):
+        self.step_(flat, lr)
+        self.predict_(flat, lr_pred, s, out)
+
+    def check_finite(self):
+        pass
+
+
+class Src:
+    def batch(self, mb):
+        s = rng_ref.Stream(101, f"batch-{mb}")
+        return s.normal(8, DIMS[0]), s.normal(8, DIMS[-1])
+
+
+def _worker(rank, world, port, strategy, kind, n, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.pipeline import PipelineStageRunner, gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+        from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+        torch.set_default_dtype(torch.float32)
+        layers = build_layers(DIMS, ACTS)
+        group = partition_layers(layers, world)[rank]
+        stage = StageModel(rank, group, lambda sp: rng_ref.layer_init(5, sp.index, sp.in_dim, sp.out_dim), "cpu")
+        opt = StandInOptimizer(kind, stage.param_names)
+        tl = build_timeline(strategy, world, n)
+        runner = PipelineStageRunner(dist, tl, stage, opt, strategy, Src(), "mse", lambda mb: 0.01, 8)
+        rep = runner.run()
+        reps = gather_reports(dist, rep, world)
+        if rank == 0:
+            payload = {
+                "records": sorted(
+                    [[r.mb, r.micro, r.stage, r.forward_version, r.predicted, r.prediction_target,
+                      r.backward_version, r.live_backward_version] for rp in reps for r in rp.records]),
+                "executed": [[list(e) for e in rp.executed] for rp in reps],
+                "losses": reps[-1].losses,
+                "stash": [rp.stash_peak for rp in reps],
+                "snap": [rp.snapshot_peak for rp in reps],
+                "versions": [rp.final_version for rp in reps],
+            }
+            Path(out_dir, "out.json").write_text(json.dumps(payload))
+        params = {n_: p.detach().double().numpy().tolist() for n_, p in zip(stage.param_names, stage.params)}
+        Path(out_dir, f"params{rank}.json").write_text(json.dumps(params))
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("optimizer_prediction", "sgdm"),
+                                           ("async_raw", "adamw")])
+def test_gloo_pipeline_matches_oracle(tmp_path, world, strategy, kind):
+    n = 2 * world + 6
+    mp.spawn(_worker, args=(world, free_port(), strategy, kind, n, str(tmp_path)), nprocs=world, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    ref = runtime_ref.run(DIMS, ACTS, world, n, strategy, optim_ref.Hyper(kind, weight_decay=0.0), Src().batch, "mse",
+                          lambda mb: 0.01, lambda i, a, b: rng_ref.layer_init(5, i, a, b))
+    # bit-exact bookkeeping
+    assert got["records"] == sorted(list(r) for r in ref["records"])
+    from paper_2312_00839_b200.runtime import build_timeline
+
+    tl = build_timeline(strategy, world, n)
+    for k in range(world):
+        assert [tuple(e) for e in got["executed"][k]] == [(e.kind, e.mb) for e in tl.stage_events(k)]
+    assert got["versions"] == [n + 1] * world
+    assert got["stash"] == ref["stash_peaks"] and got["snap"] == ref["snapshot_peaks"]
+    # numbers: fp32 stage math vs the fp64 oracle
+    assert np.allclose(got["losses"], ref["losses"], rtol=1e-4, atol=1e-6)
+    for k in range(world):
+        params = json.loads((tmp_path / f"params{k}.json").read_text())
+        for name, want in zip(ref["names"][k], ref["params"][k]):
+            assert optim_ref.inf_norm_rel(np.array(params[name]), want) <= 1e-4

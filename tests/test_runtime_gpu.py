@@ -1,0 +1,227 @@
+"""Single-GPU 1F1B runner vs the reference (golden fixtures made by the
+reference's execute/run_experiment) and vs the live oracle.
+
+Parity contract (BASELINE.json north_star):
+  * schedule order and per-stage version indices: bit-exact (VersionRecords
+    compared as integer tuples);
+  * losses: |l_b200 - l_ref| <= 1e-4 * |l_ref| + 1e-6 per mini-batch (fp32
+    device vs the fp64 reference; strict fp32 GEMMs, TF32 off) — except
+    config 1 WITH prediction, which is ill-conditioned: rounding only the
+    reference's inputs (init + data) to fp32 and computing in fp64 already
+    moves its mb-40 loss by 1.36e-3 relative (tests/test_oracle.py::
+    test_config1_prediction_is_ill_conditioned). There the stated tolerance
+    is 1e-4 for mini-batches 1-10 and 5e-3 for all 40;
+  * final weights: inf-norm-relative <= 1e-4 after the whole run (the
+    per-step 1e-6 contract is checked on the kernels themselves).
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import data_ref, optim_ref, rng_ref, runtime_ref
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = json.loads((Path(__file__).resolve().parent / "golden" / "runtime_golden.json").read_text())
+LOSS_RTOL, LOSS_ATOL, PARAM_TOL = 1e-4, 1e-6, 1e-4
+
+
+@pytest.fixture(autouse=True, scope="module")
+def strict_fp32():
+    import torch
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    yield
+
+
+class Source:
+    """Reference-seeded regression batches (pkg/tests/test_runtime.py:22-31)."""
+
+    def __init__(self, seed, rows, din, dout):
+        self.seed, self.rows, self.din, self.dout = seed, rows, din, dout
+
+    def batch(self, mb):
+        s = rng_ref.Stream(self.seed, f"batch-{mb}")
+        return s.normal(self.rows, self.din), s.normal(self.rows, self.dout)
+
+
+class ArraySource:
+    def __init__(self, batches):
+        self.b = batches
+
+    def batch(self, mb):
+        return self.b.batch(mb)
+
+
+def build(case, strategy=None, device="cuda"):
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import build_timeline
+    from paper_2312_00839_b200.stages import build_layers, build_stages
+
+    layers = build_layers(case["dims"], case["acts"])
+    seed = case["init_seed"]
+    stages = build_stages(layers, case["depth"],
+                          lambda sp: rng_ref.layer_init(seed, sp.index, sp.in_dim, sp.out_dim), device=device)
+    kw = {"weight_decay": case.get("weight_decay", 5e-4)} if case["kind"] == "sgdm" else {}
+    cfg = OptimizerConfig(case["kind"], **kw)
+    opts = [OptimizerState(cfg, s.param_names) for s in stages]
+    tl = build_timeline(strategy or case["strategy"], case["depth"], case["n"])
+    return tl, stages, opts
+
+
+def run_case(case, checks="eager", fuse=True, strategy=None):
+    from paper_2312_00839_b200.runtime import execute
+
+    tl, stages, opts = build(case, strategy)
+    if case["name"] == "small":
+        src = Source(case["data_seed"], case["rows"], case["dims"][0], case["dims"][-1])
+        loss = "mse"
+    else:
+        batches, loss = data_ref.config1(seed=case["data_seed"])
+        src = ArraySource(batches)
+    rep = execute(tl, stages, opts, strategy or case["strategy"], src, loss, lambda mb, lr=case["lr"]: lr,
+                  checks=checks, fuse=fuse)
+    return rep, stages
+
+
+def rec_tuples(rep):
+    return [[r.mb, r.micro, r.stage, r.forward_version, r.predicted, r.prediction_target,
+             r.backward_version, r.live_backward_version] for r in rep.records]
+
+
+def check_losses(got, want, rtol=LOSS_RTOL):
+    got, want = np.array(got), np.array(want)
+    err = np.abs(got - want)
+    assert np.all(err <= rtol * np.abs(want) + LOSS_ATOL), float(np.max(err / np.abs(want)))
+
+
+SMALL = [c for c in GOLDEN if c["name"] == "small"]
+
+
+@pytest.mark.parametrize("case", SMALL, ids=lambda c: f"D{c['depth']}-{c['strategy']}-{c['kind']}")
+def test_small_runs_match_reference(case):
+    rep, stages = run_case(case)
+    assert rec_tuples(rep) == case["records"]
+    assert rep.snapshot_peaks == case["snapshot_peaks"]
+    assert rep.stash_peaks == case["stash_peaks"]
+    assert rep.final_versions == case["final_versions"]
+    assert rep.bubble_overall == case["bubble_overall"] and rep.makespan_unit == case["makespan_unit"]
+    check_losses(rep.losses, case["losses"])
+    for stage, want_stage in zip(stages, case["params"]):
+        for p, want in zip(stage.params, want_stage):
+            assert optim_ref.inf_norm_rel(p.detach().cpu().double().numpy(), np.array(want)) <= PARAM_TOL
+
+
+CONFIG1 = [c for c in GOLDEN if c["name"] == "config1"]
+
+
+@pytest.mark.parametrize("case", CONFIG1, ids=lambda c: c["strategy"])
+def test_config1_matches_reference(case):
+    """Config 1: 4-stage 3072-1024^3-10 MLP on CIFAR-10-shaped batches, Adam
+    lr 1e-4, 40 mini-batches — records bit-exact, losses within 1e-4 rel."""
+    rep, stages = run_case(case)
+    assert rec_tuples(rep) == case["records"]
+    if case["strategy"] == "optimizer_prediction":
+        check_losses(rep.losses[:10], case["losses"][:10])
+        check_losses(rep.losses, case["losses"], rtol=5e-3)
+    else:
+        check_losses(rep.losses, case["losses"])
+        for stage, amax in zip(stages, case["param_absmax"]):
+            for p, a in zip(stage.params, amax):
+                assert abs(float(p.double().abs().max()) - a) <= 1e-4 * a
+
+
+def test_fused_and_unfused_are_bit_identical():
+    """K3 (step+predict fused at the update) == K2 then K1 at the forward."""
+    import torch
+
+    case = next(c for c in SMALL if c["depth"] == 4 and c["strategy"] == "optimizer_prediction" and c["kind"] == "adamw")
+    a, sa = run_case(case, fuse=True)
+    b, sb = run_case(case, fuse=False)
+    assert a.losses == b.losses
+    for x, y in zip(sa, sb):
+        assert torch.equal(x.flat.data, y.flat.data)
+
+
+def test_deferred_checks_same_numbers():
+    case = next(c for c in SMALL if c["depth"] == 4 and c["strategy"] == "optimizer_prediction" and c["kind"] == "adam")
+    a, _ = run_case(case, checks="eager")
+    b, _ = run_case(case, checks="deferred")
+    assert a.losses == pytest.approx(b.losses, rel=0, abs=0)
+    assert rec_tuples(a) == rec_tuples(b)
+
+
+def test_matches_live_oracle_on_fp32_inputs():
+    """Same run through the fp64 oracle fed the fp32-cast init and data."""
+    case = dict(next(c for c in SMALL if c["depth"] == 2 and c["strategy"] == "optimizer_prediction" and c["kind"] == "sgdm"))
+    rep, _ = run_case(case)
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    src = Source(case["data_seed"], case["rows"], case["dims"][0], case["dims"][-1])
+    out = runtime_ref.run(case["dims"], case["acts"], case["depth"], case["n"], case["strategy"],
+                          optim_ref.Hyper("sgdm", weight_decay=case["weight_decay"]),
+                          lambda mb: tuple(f32(v) for v in src.batch(mb)), "mse", lambda mb: case["lr"],
+                          lambda i, din, dout: tuple(f32(v) for v in rng_ref.layer_init(case["init_seed"], i, din, dout)))
+    check_losses(rep.losses, out["losses"])
+    assert rec_tuples(rep) == [list(r) for r in out["records"]]
+
+
+def test_peaks_match_reference_pins():
+    """pkg/tests/test_runtime.py:210-226: prediction [2,2,2,1], async [1,1,1,1], stash [4,3,2,1]."""
+    base = next(c for c in SMALL if c["depth"] == 4 and c["kind"] == "sgdm" and c["strategy"] == "optimizer_prediction")
+    rep_p, _ = run_case(base)
+    rep_a, _ = run_case(base, strategy="async_raw")
+    assert rep_p.snapshot_peaks == [2, 2, 2, 1]
+    assert rep_a.snapshot_peaks == [1, 1, 1, 1]
+    assert rep_a.stash_peaks == [4, 3, 2, 1]
+    for r in rep_p.records:
+        if r.stage == 3:
+            assert not r.predicted
+        else:
+            assert r.predicted and r.prediction_target == r.live_backward_version
+        assert not r.inconsistent and r.staleness == 0
+
+
+def test_prediction_never_mutates_live_params():
+    import torch
+
+    from paper_2312_00839_b200.runtime import _PredictivePolicy, _StageRt
+
+    case = next(c for c in SMALL if c["depth"] == 2 and c["kind"] == "sgdm")
+    _, stages, opts = build(case)
+    rt = _StageRt(stages[0], opts[0], 2)
+    before = stages[0].flat.data.clone()
+    ptrs = [p.data_ptr() for p in stages[0].params]
+    weights, fv, predicted, target = _PredictivePolicy({(1, 0): 1}).forward_view(rt, 1, 0, 0.1)
+    assert predicted and target == 2 and fv == 1
+    assert torch.equal(stages[0].flat.data, before)
+    assert all(w.data_ptr() != p for w, p in zip(weights, ptrs))
+
+
+def test_numeric_abort_carries_context():
+    from paper_2312_00839_b200.errors import NumericError
+
+    case = dict(next(c for c in SMALL if c["depth"] == 4 and c["kind"] == "sgdm"), lr=float("inf"))
+    with pytest.raises(NumericError) as exc:
+        run_case(case, strategy="async_raw")
+    assert "mb" in str(exc.value) and "stage" in str(exc.value)
+
+
+def test_execute_rejects_bad_inputs():
+    from paper_2312_00839_b200.runtime import build_timeline, execute
+
+    case = next(c for c in SMALL if c["depth"] == 4 and c["kind"] == "sgdm")
+    _, stages, opts = build(case)
+    src = Source(1, 8, 4, 3)
+    with pytest.raises(ValueError):
+        execute(build_timeline("naive", 4, 4), stages, opts, "async_raw", src, "mse", lambda mb: 0.01)
+    with pytest.raises(ValueError):
+        execute(build_timeline("async_raw", 2, 4), stages, opts, "async_raw", src, "mse", lambda mb: 0.01)
+    with pytest.raises(ValueError):
+        build_timeline("serial", 4, 8)
+    with pytest.raises(ValueError):
+        execute(build_timeline("spectrain", 4, 4), stages, [type(o)(type(o.config)("adam"), o.names) for o in opts],
+                "spectrain", src, "mse", lambda mb: 0.01)
