@@ -89,7 +89,7 @@ class Rec:
 
 
 class _Stage:
-    def __init__(self, rank, layer_ids, dims, acts, init):
+    def __init__(self, rank, layer_ids, dims, acts, init, dtype=np.float64):
         self.rank = rank
         self.layer_ids = layer_ids
         self.acts = [acts[i] for i in layer_ids]
@@ -97,7 +97,7 @@ class _Stage:
         self.names = []
         for i in layer_ids:
             w, b = init(i, dims[i], dims[i + 1])
-            self.params += [np.array(w, dtype=np.float64), np.array(b, dtype=np.float64)]
+            self.params += [np.array(w, dtype=dtype), np.array(b, dtype=dtype)]
             self.names += [f"layer{i}.w", f"layer{i}.b"]
         self.version = 1
         self.stash = {}
@@ -128,17 +128,18 @@ class _Stage:
 
 
 def run(dims, acts, depth, n_batches, strategy, opt_hyper: Hyper, batch_fn, loss_kind, lr_for_mb,
-        init):
+        init, dtype=np.float64):
     """Execute a 1F1B (or serial, depth 1) run. `init(i, din, dout)` -> (w, b);
-    `batch_fn(mb)` -> (x, y) float64. Strategies: async_raw,
-    optimizer_prediction, spectrain, serial."""
+    `batch_fn(mb)` -> (x, y). Strategies: async_raw, optimizer_prediction,
+    spectrain, serial. dtype=float64 is the reference; dtype=float32
+    evaluates the same algorithm in fp32 (used only to size fp32 drift)."""
     if strategy == "serial" and depth != 1:
         raise ValueError("serial requires depth 1")
     predictive = strategy in ("optimizer_prediction", "spectrain")
     if strategy == "spectrain" and opt_hyper.kind != "sgdm":
         raise ValueError("spectrain requires the sgdm optimizer")
     groups = partition(len(dims) - 1, depth)
-    stages = [_Stage(k, ids, dims, acts, init) for k, ids in enumerate(groups)]
+    stages = [_Stage(k, ids, dims, acts, init, dtype) for k, ids in enumerate(groups)]
     opts = [OracleOptimizer(opt_hyper, s.names) for s in stages]
     gap = schedule_ref.gaps(depth, n_batches)
     order = schedule_ref.global_order(depth, n_batches)
@@ -153,7 +154,7 @@ def run(dims, acts, depth, n_batches, strategy, opt_hyper: Hyper, batch_fn, loss
     def batch(mb):
         if mb not in cache:
             x, y = batch_fn(mb)
-            cache[mb] = (np.asarray(x, dtype=np.float64), np.asarray(y, dtype=np.float64))
+            cache[mb] = (np.asarray(x, dtype=dtype), np.asarray(y, dtype=dtype))
         return cache[mb]
 
     for _slot, k, kind, mb in order:
