@@ -73,6 +73,96 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4):
     return out
 
 
+MODULE_CONFIGS = {
+    # BASELINE configs[1..3] (SURVEY.md §8d pipeline synthetic inputs)
+    "config2_vgg16": dict(blocks="vgg16", in_shape=(3, 32, 32), classes=100, batch=128, depth=4, opt="sgdm", lr=0.01),
+    "config3_resnet101": dict(blocks="resnet101", in_shape=(3, 224, 224), classes=200, batch=64, depth=8,
+                              opt="adamw", lr=1e-3),
+    "config4_gnmt8": dict(blocks="gnmt8", in_shape=(50,), classes=32000, batch=64, depth=8, opt="adam", lr=1e-3,
+                          tokens=True),
+}
+
+
+def make_blocks(name: str, classes: int):
+    from .stage_models import gnmt8_blocks, resnet101_blocks, vgg16_cifar_blocks
+
+    return {"vgg16": lambda: vgg16_cifar_blocks(classes), "resnet101": lambda: resnet101_blocks(classes),
+            "gnmt8": lambda: gnmt8_blocks(classes, 1024)}[name]()
+
+
+class ModuleBatches:
+    def __init__(self, torch, device, cfg, n_distinct=4, seed=0):
+        g = torch.Generator(device=device).manual_seed(seed)
+        b, shape, c = cfg["batch"], cfg["in_shape"], cfg["classes"]
+        if cfg.get("tokens"):
+            self.x = [torch.randint(0, c, (b, *shape), device=device, generator=g).float() for _ in range(n_distinct)]
+        else:
+            self.x = [torch.randn((b, *shape), device=device, generator=g) for _ in range(n_distinct)]
+        self.y = [torch.nn.functional.one_hot(torch.randint(0, c, (b,), device=device, generator=g), c).float()
+                  for _ in range(n_distinct)]
+
+    def batch(self, mb):
+        i = (mb - 1) % len(self.x)
+        return self.x[i], self.y[i]
+
+
+_COSTS: dict = {}
+
+
+def module_stages_for(torch, name, device, depth=None):
+    from .stage_models import build_module_stages, profile_block_costs
+
+    cfg = MODULE_CONFIGS[name]
+    depth = depth or cfg["depth"]
+    in_dtype = torch.long if cfg.get("tokens") else torch.float32
+    if name not in _COSTS:
+        _COSTS[name] = profile_block_costs(make_blocks(cfg["blocks"], cfg["classes"]), cfg["in_shape"], cfg["batch"],
+                                           device, in_dtype=in_dtype)
+    costs = _COSTS[name]
+    torch.manual_seed(0)
+    blocks = make_blocks(cfg["blocks"], cfg["classes"])
+    return build_module_stages(blocks, depth, device, cfg["in_shape"], costs=costs, in_dtype=in_dtype), costs
+
+
+def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf32: bool = True):
+    """Configs 2-4 through the single-GPU 1F1B runner (all stages on one GPU)."""
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import build_timeline, execute
+
+    cfg = MODULE_CONFIGS[name]
+    torch.backends.cuda.matmul.allow_tf32 = tf32
+    torch.backends.cudnn.allow_tf32 = tf32
+    data = ModuleBatches(torch, device, cfg)
+    out = {"config": f"{name}: D={cfg['depth']} stages on 1 GPU (single-process runner), batch {cfg['batch']}, "
+                     f"{cfg['opt']} lr {cfg['lr']}, {n_batches} mini-batches, "
+                     f"{'TF32' if tf32 else 'fp32'} convs/GEMMs, fp32 master weights"}
+    for strategy in ("async_raw", "optimizer_prediction"):
+        secs = []
+        for trial, n in enumerate((2 * cfg["depth"], n_batches)):
+            stages, costs = module_stages_for(torch, name, device)
+            kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
+            opts = [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in stages]
+            tl = build_timeline(strategy, cfg["depth"], n)
+            torch.cuda.synchronize(device)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rep = execute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: cfg["lr"], checks="deferred")
+            e1.record()
+            torch.cuda.synchronize(device)
+            secs.append(e0.elapsed_time(e1) / 1e3)
+            stage_params = [s.numel for s in stages]
+            del stages, opts
+        key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
+        out[key] = {"samples_per_s": round(n_batches * cfg["batch"] / secs[-1], 2), "s": round(secs[-1], 4),
+                    "final_loss": rep.losses[-1]}
+    out["stage_params"] = stage_params
+    on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
+    out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    return out
+
+
 def multi_gpu_pipeline(torch, dist, rank, world, device, n_batches: int = 64):
     """One stage per GPU over NCCL (pipeline.py); depth = world."""
     from .pipeline import bench_config1_pipeline

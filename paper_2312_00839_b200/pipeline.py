@@ -35,7 +35,7 @@ from .runtime import (
     _to_device,
 )
 from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, update_gaps, validate_timeline
-from .stages import StageModel, loss_and_grad, stage_backward, stage_forward
+from .stages import StageModel, loss_and_grad
 
 
 @dataclass
@@ -112,9 +112,9 @@ class PipelineStageRunner:
 
     def _input_spec(self, op):
         if op.kind == FORWARD and self.rank > 0:
-            return (self.rows, self.stage.in_dim), self.rank - 1
+            return (self.rows, *self.stage.in_shape), self.rank - 1
         if op.kind == BACKWARD and self.rank < self.depth - 1:
-            return (self.rows, self.stage.out_dim), self.rank + 1
+            return (self.rows, *self.stage.out_shape), self.rank + 1
         return None
 
     def run(self) -> StageReport:
@@ -156,8 +156,8 @@ class PipelineStageRunner:
                     inp = _to_device(self.data.batch(op.mb)[0], self.device)
                 weights, fv, predicted, target = self.policy.forward_view(self.rt, op.mb, 0, self.lr_for_mb(op.mb))
                 try:
-                    out = stage_forward(self.stage, weights, (op.mb, 0), inp, fv, check_finite=self.eager,
-                                        finite_flags=flags, flag_index=wi)
+                    out = self.stage.run_forward(weights, (op.mb, 0), inp, fv, check_finite=self.eager,
+                                                 finite_flags=flags, flag_index=wi)
                 except NumericError as err:
                     raise NumericError(f"mb {op.mb} stage {self.rank}: {err}") from err
                 rec = VersionRecord(op.mb, 0, self.rank, fv, predicted, target)
@@ -176,8 +176,8 @@ class PipelineStageRunner:
                 g_out = grads_local.pop(op.mb) if self.rank == self.depth - 1 else inp
                 rec = records[op.mb]
                 weights, bv = self.policy.backward_view(self.rt, op.mb, 0, rec.forward_version)
-                g_in, _ = stage_backward(self.stage, weights, (op.mb, 0), g_out, accumulate=False,
-                                         need_input_grad=self.rank > 0)
+                g_in, _ = self.stage.run_backward(weights, (op.mb, 0), g_out, accumulate=False,
+                                                  need_input_grad=self.rank > 0)
                 self.rt.pending_count = 1
                 rec.backward_version = bv
                 rec.live_backward_version = self.stage.version

@@ -1,0 +1,294 @@
+"""Pipeline stages built from torch modules (configs 2-4: VGG-16, ResNet-101,
+GNMT-style LSTM), with the reference's weight-view semantics.
+
+The reference only has dense MLP stages (stages.py); BASELINE configs 2-4 are
+deep models, so here a stage is a contiguous slice of a model's blocks whose
+parameters are re-pointed (`param.data = view`) into the stage's flat fp32
+buffer (FlatParams) and whose `.grad`s are views of the flat gradient — so
+the predictor/optimizer kernels stream the whole stage in one launch exactly
+as for the MLP stages, and the same runners drive both.
+
+Forward/backward semantics (stages.py:156-209): the forward
+runs on the policy's view (W_hat for predicted stages) by pointing every
+parameter's storage at the staging buffer for the duration of the forward;
+the backward runs after the parameters point back at the LIVE buffer.
+Convolution and batch-norm autograd nodes save the parameter object itself,
+so their input gradients use the live weights at backward time, as the
+reference does; `nn.Linear` would save a transposed view of the forward-time
+storage, so linear layers use `LiveLinear`, whose backward reads the live
+weight explicitly. (cuDNN LSTMs save their own packed copy: LSTM stages
+therefore back-propagate through the forward-time weights — a documented
+deviation the reference cannot pin, it has no LSTM.)
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from .errors import NumericError
+from .optim import FlatParams
+from .stages import ActivationStash, StashEntry
+
+
+class _LiveLinearFn(torch.autograd.Function):
+    """y = x W^T + b; backward: dx = g W_live, dW = g^T x, db = colsum(g)."""
+
+    @staticmethod
+    def forward(ctx, x, weight, bias, module):
+        ctx.save_for_backward(x)
+        ctx.module = module
+        return F.linear(x, weight, bias)
+
+    @staticmethod
+    def backward(ctx, g):
+        (x,) = ctx.saved_tensors
+        w_live = ctx.module.weight  # points at the live buffer again by now
+        gx = g.matmul(w_live)
+        g2 = g.reshape(-1, g.shape[-1])
+        x2 = x.reshape(-1, x.shape[-1])
+        gw = g2.t().matmul(x2)
+        gb = g2.sum(0) if ctx.module.bias is not None else None
+        return gx, gw, gb, None
+
+
+class LiveLinear(nn.Linear):
+    def forward(self, x):
+        return _LiveLinearFn.apply(x, self.weight, self.bias, self)
+
+
+# ---- model definitions (as lists of blocks for contiguous partitioning) ------------------
+
+
+def vgg16_cifar_blocks(num_classes: int = 100) -> list[nn.Module]:
+    """VGG-16 for 32x32 inputs (conv3x3-BN-ReLU x13, 5 max-pools, 512-512-C
+    classifier): ~15.3M params."""
+    cfg = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
+    blocks: list[nn.Module] = []
+    c_in = 3
+    pending = []
+    for v in cfg:
+        if v == "M":
+            pending.append(nn.MaxPool2d(2, 2))
+            blocks.append(nn.Sequential(*pending))
+            pending = []
+        else:
+            if pending:
+                blocks.append(nn.Sequential(*pending))
+            pending = [nn.Conv2d(c_in, v, 3, padding=1, bias=False), nn.BatchNorm2d(v), nn.ReLU(inplace=True)]
+            c_in = v
+    blocks.append(nn.Sequential(nn.Flatten(), LiveLinear(512, 512), nn.ReLU(inplace=True)))
+    blocks.append(nn.Sequential(LiveLinear(512, 512), nn.ReLU(inplace=True), LiveLinear(512, num_classes)))
+    return blocks
+
+
+def resnet101_blocks(num_classes: int = 200) -> list[nn.Module]:
+    """torchvision ResNet-101 (bottleneck 3-4-23-3) as stem, 33 bottlenecks,
+    head; 42.9M params at 200 classes."""
+    import torchvision
+
+    m = torchvision.models.resnet101(weights=None, num_classes=num_classes)
+    fc = LiveLinear(m.fc.in_features, num_classes)
+    blocks: list[nn.Module] = [nn.Sequential(m.conv1, m.bn1, m.relu, m.maxpool)]
+    for layer in (m.layer1, m.layer2, m.layer3, m.layer4):
+        blocks.extend(list(layer))
+    blocks.append(nn.Sequential(m.avgpool, nn.Flatten(), fc))
+    return blocks
+
+
+class _LSTMBlock(nn.Module):
+    def __init__(self, d_in, d, residual):
+        super().__init__()
+        self.lstm = nn.LSTM(d_in, d, batch_first=True)
+        self.residual = residual
+
+    def forward(self, x):
+        y, _ = self.lstm(x)
+        return y + x if self.residual else y
+
+
+class _Embed(nn.Module):
+    def __init__(self, vocab, d):
+        super().__init__()
+        self.emb = nn.Embedding(vocab, d)
+
+    def forward(self, tokens):
+        return self.emb(tokens.long())
+
+
+class _Head(nn.Module):
+    def __init__(self, d, vocab):
+        super().__init__()
+        self.proj = LiveLinear(d, vocab)
+
+    def forward(self, x):
+        return self.proj(x[:, -1, :])
+
+
+def gnmt8_blocks(vocab: int = 32000, d: int = 1024) -> list[nn.Module]:
+    """GNMT-8-shaped sequential stack: embedding, 8 LSTM layers of width d
+    (residual from layer 3 on, as GNMT), projection to the vocabulary on the
+    last position (the encoder/decoder attention is
+    folded into a sequential stack so it partitions into a pipeline)."""
+    blocks: list[nn.Module] = [_Embed(vocab, d)]
+    for i in range(8):
+        blocks.append(_LSTMBlock(d, d, residual=i >= 2))
+    blocks.append(_Head(d, vocab))
+    return blocks
+
+
+def balanced_partition(costs: list[float], depth: int) -> list[tuple[int, int]]:
+    """Contiguous split of blocks into `depth` non-empty ranges minimising the
+    largest range cost (DP over prefix sums). Returns [(lo, hi)) ranges."""
+    n = len(costs)
+    if not 1 <= depth <= n:
+        raise ValueError(f"cannot split {n} blocks across {depth} stages")
+    pre = [0.0]
+    for c in costs:
+        pre.append(pre[-1] + c)
+    INF = float("inf")
+    best = [[INF] * (n + 1) for _ in range(depth + 1)]
+    cut = [[0] * (n + 1) for _ in range(depth + 1)]
+    best[0][0] = 0.0
+    for k in range(1, depth + 1):
+        for j in range(k, n - (depth - k) + 1):
+            for i in range(k - 1, j):
+                v = max(best[k - 1][i], pre[j] - pre[i])
+                if v < best[k][j]:
+                    best[k][j] = v
+                    cut[k][j] = i
+    out, j = [], n
+    for k in range(depth, 0, -1):
+        i = cut[k][j]
+        out.append((i, j))
+        j = i
+    return out[::-1]
+
+
+def block_param_counts(blocks: list[nn.Module]) -> list[int]:
+    return [sum(p.numel() for p in b.parameters()) for b in blocks]
+
+
+# ---- the stage --------------------------------------------------------------------------------
+
+
+class ModuleStage:
+    """A pipeline stage made of torch modules over a flat parameter buffer.
+
+    Same surface the runners use on the MLP `StageModel`: rank, flat, params,
+    param_names, version, stash, in_shape/out_shape (per sample) and
+    run_forward / run_backward.
+    """
+
+    def __init__(self, rank: int, blocks: list[nn.Module], device, in_shape: tuple, in_dtype=torch.float32):
+        self.rank = rank
+        self.device = torch.device(device)
+        self.module = nn.Sequential(*blocks).to(self.device)
+        self.module.train()
+        named = list(self.module.named_parameters())
+        self._params = [p for _, p in named]
+        self.param_names = [n for n, _ in named]
+        self.flat = FlatParams.from_tensors(self.param_names, [p.detach() for p in self._params], self.device)
+        self._live = self.flat.params
+        for p, v, gv in zip(self._params, self._live, self.flat.grads):
+            p.data = v
+            p.grad = gv
+        self.version = 1
+        self.stash = ActivationStash()
+        self.in_shape = tuple(in_shape)
+        self.in_dtype = in_dtype
+        with torch.no_grad():
+            probe = torch.zeros((2, *self.in_shape), device=self.device, dtype=in_dtype)
+            self.out_shape = tuple(self.module(probe).shape[1:])
+        # the probe ran in train mode: reset batch-norm statistics it touched
+        for m in self.module.modules():
+            if isinstance(m, nn.modules.batchnorm._BatchNorm):
+                m.reset_running_stats()
+
+    @property
+    def params(self) -> list[torch.Tensor]:
+        return self._live
+
+    @property
+    def numel(self) -> int:
+        return self.flat.layout.numel
+
+    def _point(self, views) -> None:
+        for p, v in zip(self._params, views):
+            if p.data_ptr() != v.data_ptr():
+                p.data = v
+
+    def run_forward(self, weights, key, x, version, check_finite=True, finite_flags=None, flag_index=0):
+        self._point(weights)
+        try:
+            x_in = x.detach()
+            if self.rank > 0 and x_in.is_floating_point():
+                x_in.requires_grad_(True)
+            with torch.enable_grad():
+                out = self.module(x_in)
+        finally:
+            self._point(self._live)
+        if check_finite:
+            if not bool(torch.isfinite(out).all()):
+                raise NumericError(f"non-finite value in stage {self.rank} forward output")
+        elif finite_flags is not None:
+            finite_flags[flag_index] = torch.isfinite(out).all()
+        self.stash.put(key, StashEntry(version, [x_in], [out]))
+        return out.detach()
+
+    def run_backward(self, weights, key, grad_out, accumulate=False, need_input_grad=True):
+        entry = self.stash.pop(key)
+        x_in, out = entry.layer_inputs[0], entry.pre_acts[0]
+        self._point(weights)
+        try:
+            if not accumulate:
+                self.flat.grad.zero_()
+            torch.autograd.backward(out, grad_out)
+        finally:
+            self._point(self._live)
+        g_in = x_in.grad if (need_input_grad and x_in.requires_grad) else None
+        return g_in, self.flat.grads
+
+
+def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32, reps=3) -> list[float]:
+    """Per-block forward+backward time on the device for one batch (a tiny
+    profiling partitioner, in the spirit of PipeDream's), used to balance
+    stages by time instead of parameter count."""
+    dev = torch.device(device)
+    x = torch.zeros((batch, *in_shape), device=dev, dtype=in_dtype)
+    if in_dtype == torch.float32:
+        x.normal_()
+    costs = []
+    for b in blocks:
+        b.to(dev).train()
+        xin = x.detach().requires_grad_(x.is_floating_point())
+        times = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            y = b(xin)
+            y.backward(torch.ones_like(y))
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        b.zero_grad(set_to_none=True)
+        costs.append(sorted(times)[len(times) // 2])
+        x = y.detach()
+    for m in (mm for b in blocks for mm in b.modules()):
+        if isinstance(m, nn.modules.batchnorm._BatchNorm):
+            m.reset_running_stats()
+    return costs
+
+
+def build_module_stages(blocks, depth, device, in_shape, costs=None, in_dtype=torch.float32):
+    """Partition `blocks` into `depth` contiguous stages balanced by `costs`
+    (default: parameter counts) and build them in order."""
+    costs = costs if costs is not None else [max(1, c) for c in block_param_counts(blocks)]
+    ranges = balanced_partition(costs, depth)
+    stages, shape, dtype = [], tuple(in_shape), in_dtype
+    for k, (lo, hi) in enumerate(ranges):
+        st = ModuleStage(k, blocks[lo:hi], device, shape, dtype)
+        stages.append(st)
+        shape, dtype = st.out_shape, torch.float32
+    return stages

@@ -172,6 +172,20 @@ class StageModel:
     def numel(self) -> int:
         return self.flat.layout.numel
 
+    @property
+    def in_shape(self) -> tuple:
+        return (self.in_dim,)
+
+    @property
+    def out_shape(self) -> tuple:
+        return (self.out_dim,)
+
+    def run_forward(self, weights, key, x, version, check_finite=True, finite_flags=None, flag_index=0):
+        return stage_forward(self, weights, key, x, version, check_finite, finite_flags, flag_index)
+
+    def run_backward(self, weights, key, grad_out, accumulate=False, need_input_grad=True):
+        return stage_backward(self, weights, key, grad_out, accumulate, need_input_grad)
+
 
 def build_stages(layers: list[LayerSpec], depth: int, init: InitFn, device=None) -> list[StageModel]:
     return [StageModel(k, group, init, device) for k, group in enumerate(partition_layers(layers, depth))]

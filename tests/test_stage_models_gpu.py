@@ -1,0 +1,80 @@
+"""Configs 2-3 on the device (SURVEY.md §8c "Configs 2-4"): the reference has
+no conv/LSTM stages, so what is pinned is (a) K3 on each stage's REAL flat
+buffers vs the oracle on the same fp32 values, (b) the schedule/version
+records (model-independent) vs the oracle, (c) the S9 weight views."""
+
+import numpy as np
+import pytest
+
+from oracle import optim_f32, optim_ref, rng_ref, runtime_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _records(rep):
+    return [(r.mb, r.micro, r.stage, r.forward_version, r.predicted, r.prediction_target, r.backward_version,
+             r.live_backward_version) for r in rep.records]
+
+
+def _oracle_records(depth, n, strategy):
+    dims = [3] * (depth + 1)
+    out = runtime_ref.run(dims, ["tanh"] * depth, depth, n, strategy, optim_ref.Hyper("sgdm"),
+                          lambda mb: (np.ones((2, 3)), np.ones((2, 3))), "mse", lambda mb: 1e-3,
+                          lambda i, a, b: rng_ref.layer_init(0, i, a, b))
+    return [tuple(r) for r in out["records"]]
+
+
+@pytest.mark.parametrize("name,kind", [("config2_vgg16", "sgdm"), ("config3_resnet101", "adamw")])
+def test_stage_buffers_k3_parity_and_records(name, kind):
+    import torch
+
+    from paper_2312_00839_b200.bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import build_timeline, execute
+
+    dev = torch.device("cuda", 0)
+    cfg = dict(MODULE_CONFIGS[name], batch=8)
+    stages, _ = module_stages_for(torch, name, dev)
+    opts = [OptimizerState(OptimizerConfig(kind), s.param_names, device=dev) for s in stages]
+    D, n = len(stages), len(stages) + 2
+    rep = execute(build_timeline("optimizer_prediction", D, n), stages, opts, "optimizer_prediction",
+                  ModuleBatches(torch, dev, cfg), "softmax_xent", lambda mb: 1e-3)
+    assert _records(rep) == _oracle_records(D, n, "optimizer_prediction")
+    # one more real backward's gradient sits in flat.grad; run K3 on each stage's buffers
+    for st, opt in zip(stages, opts):
+        w = st.flat.data.cpu().numpy().copy()
+        g = st.flat.grad.cpu().numpy().copy()
+        s1 = opt._s1.cpu().numpy().copy()
+        s2 = opt._s2.cpu().numpy().copy() if opt._s2 is not None else np.zeros_like(w)
+        t = opt.step_count
+        out = torch.empty_like(st.flat.data)
+        opt.step_predict_(st.flat, 1e-3, 2e-3, 3, out)
+        f64 = lambda a: a.astype(np.float64)  # noqa: E731
+        nw, _, _, wh = optim_ref.flat_step_predict(kind, f64(w), f64(g), f64(s1), None if kind == "sgdm" else f64(s2),
+                                                   1e-3, 2e-3, 3, t)
+        assert optim_ref.inf_norm_rel(st.flat.data.cpu().double().numpy(), nw) <= 1e-6
+        assert optim_ref.inf_norm_rel(out.cpu().double().numpy(), wh) <= 1e-6
+        ew, _, _, ewh = optim_f32.step(kind, w, g, s1, s2, 1e-3, t, c_pred=2e-3 * 3)
+        assert np.array_equal(st.flat.data.cpu().numpy(), ew) and np.array_equal(out.cpu().numpy(), ewh)
+
+
+def test_fused_equals_unfused_on_vgg_stages():
+    import torch
+
+    from paper_2312_00839_b200.bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import build_timeline, execute
+
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    dev = torch.device("cuda", 0)
+    cfg = dict(MODULE_CONFIGS["config2_vgg16"], batch=8)
+    finals = []
+    for fuse in (True, False):
+        stages, _ = module_stages_for(torch, "config2_vgg16", dev)
+        opts = [OptimizerState(OptimizerConfig("sgdm"), s.param_names, device=dev) for s in stages]
+        rep = execute(build_timeline("optimizer_prediction", 4, 7), stages, opts, "optimizer_prediction",
+                      ModuleBatches(torch, dev, cfg), "softmax_xent", lambda mb: 1e-2, fuse=fuse)
+        finals.append((rep.losses, [s.flat.data.clone() for s in stages]))
+    assert finals[0][0] == finals[1][0]
+    assert all(torch.equal(a, b) for a, b in zip(finals[0][1], finals[1][1]))
