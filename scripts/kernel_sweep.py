@@ -1,6 +1,6 @@
 """Kernel sweep: K1/K2/K3 x {sgdm, adam, adamw} x N, achieved algorithmic GB/s
 against the measured HBM copy peak (MEASURED_PEAKS.json), CUDA-event timed
-per launch with an L2 flush (256 MB write) between launches.
+per launch with an L2 flush (256 MB read) between launches.
 
   python scripts/kernel_sweep.py                 # default sweep
   python scripts/kernel_sweep.py --tune          # launch-shape search at 2^28
@@ -72,12 +72,14 @@ def call(lib, kernel, kind, b: Buffers, launch, stream, t=10, s=3, lr=1e-3):
 
 def time_kernel(lib, kernel, kind, b, launch=None, reps=20, warmup=5):
     stream = torch.cuda.current_stream()
-    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    # L2 flush by READING 256 MB (2x L2): clean lines, so the timed kernel does
+    # not pay for write-backs of the flush itself
+    flush = torch.ones(256 * 1024 * 1024 // 4, device="cuda")
     for _ in range(warmup):
         call(lib, kernel, kind, b, launch, stream.cuda_stream)
     times = []
     for _ in range(reps):
-        flush.zero_()
+        flush.sum()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
