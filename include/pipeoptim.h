@@ -83,6 +83,22 @@ typedef struct po_launch {
   int32_t unroll;       /* vectors per stream in flight per thread: 1, 2, 4; 0 = default */
 } po_launch;
 
+/* One launch's step-dependent fp32 scalars, for graph-captured launches
+ * (po_*_dc): the host refreshes an array of these in device memory before
+ * each CUDA-graph replay, so replays continue training with the right
+ * learning rate and bias corrections. Filled by po_coef_fill exactly as the
+ * by-value entry points derive them. */
+typedef struct po_coef {
+  float lr;     /* step learning rate */
+  float c_pred; /* lr_pred * s */
+  float bc1;    /* 1 - beta1^t (1 when t == 0) */
+  float bc2;    /* 1 - beta2^t (1 when t == 0) */
+} po_coef;
+
+#define PO_COEF_STEP 0
+#define PO_COEF_PREDICT 1
+#define PO_COEF_STEP_PREDICT 2
+
 int po_abi_version(void);
 const char* po_strerror(int code);
 
@@ -118,6 +134,24 @@ int po_direction(const po_hparams* hp, const float* state1, const float* state2,
 /* predict_weights: w_hat = w - lr_times_s * d. */
 int po_axpy_predict(const float* w, const float* d, float* w_hat, int64_t n, double lr_times_s,
                     const po_launch* launch, void* stream);
+
+/* Host-only: the coefficients po_step / po_predict / po_step_predict would
+ * use for (lr, lr_times_s, step_count); `which` is PO_COEF_*. For
+ * PO_COEF_PREDICT at step_count == 0 the bias corrections are 1 and, with the
+ * optimizer state still zero, the predicted weights equal W (optim.py:131-132). */
+int po_coef_fill(const po_hparams* hp, int32_t which, double lr, double lr_times_s, int64_t step_count,
+                 po_coef* out);
+
+/* Graph-capturable variants: identical arithmetic, scalars read from
+ * `coef_dev` (device pointer) at kernel start. po_predict_dc always reads the
+ * state buffers (they must exist, zero before the first step). */
+int po_step_dc(const po_hparams* hp, float* w, const float* g, float* state1, float* state2, int64_t n,
+               const po_coef* coef_dev, int64_t* nonfinite_index, const po_launch* launch, void* stream);
+int po_predict_dc(const po_hparams* hp, const float* w, const float* state1, const float* state2, float* w_hat,
+                  int64_t n, const po_coef* coef_dev, const po_launch* launch, void* stream);
+int po_step_predict_dc(const po_hparams* hp, float* w, const float* g, float* state1, float* state2,
+                       float* w_hat, int64_t n, const po_coef* coef_dev, int64_t* nonfinite_index,
+                       const po_launch* launch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,13 @@ EXPORTS = (
     "po_step_predict",
     "po_direction",
     "po_axpy_predict",
+    "po_coef_fill",
+    "po_step_dc",
+    "po_predict_dc",
+    "po_step_predict_dc",
 )
+
+PO_COEF_STEP, PO_COEF_PREDICT, PO_COEF_STEP_PREDICT = 0, 1, 2
 
 
 class LibraryMissing(RuntimeError):
@@ -62,6 +68,10 @@ class po_launch(ctypes.Structure):
     ]
 
 
+class po_coef(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("c_pred", ctypes.c_float), ("bc1", ctypes.c_float), ("bc2", ctypes.c_float)]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _D = ctypes.c_double
@@ -77,6 +87,10 @@ _SIGNATURES = {
     "po_step_predict": (ctypes.c_int, [_HP, _P, _P, _P, _P, _P, _I64, _D, _D, _I64, _P, _LA, _P]),
     "po_direction": (ctypes.c_int, [_HP, _P, _P, _P, _I64, _I64, _LA, _P]),
     "po_axpy_predict": (ctypes.c_int, [_P, _P, _P, _I64, _D, _LA, _P]),
+    "po_coef_fill": (ctypes.c_int, [_HP, ctypes.c_int32, _D, _D, _I64, _P]),
+    "po_step_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _I64, _P, _P, _LA, _P]),
+    "po_predict_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _I64, _P, _LA, _P]),
+    "po_step_predict_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _P, _I64, _P, _P, _LA, _P]),
 }
 
 _lock = threading.Lock()

@@ -49,26 +49,55 @@ def _run_once(torch, device, strategy, depth, n_batches, data, seed=0, dims=CONF
     return rep, e0.elapsed_time(e1) / 1e3, wall
 
 
-def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4):
+def _graphed(torch, device, strategy, depth, n_batches, data, replays, seed=0, dims=CONFIG1_DIMS,
+             acts=CONFIG1_ACTS):
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import GraphedExecute, build_timeline
+    from .stages import build_layers, build_stages, torch_init
+
+    stages = build_stages(build_layers(dims, acts), depth, torch_init(seed, device), device=device)
+    opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=device) for s in stages]
+    tl = build_timeline(strategy, depth, n_batches)
+    g = GraphedExecute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: 1e-4, warmup_runs=1)
+    g.replay()  # first replay: graph upload
+    torch.cuda.synchronize(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(replays):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize(device)
+    rep = g.report()
+    return rep, e0.elapsed_time(e1) / 1e3 / replays, g.launches
+
+
+def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, replays: int = 5):
     """All `depth` stages on one GPU, events in timeline order (the single-GPU
-    1F1B runner). Reports samples/s with prediction on and off."""
+    1F1B runner). Each measured unit is one full run of the 1F1B timeline
+    (n_batches mini-batches, warm-up and drain included), replayed from a CUDA
+    graph (`GraphedExecute`); the eager (Python-driven) runner is reported
+    beside it. Samples/s with prediction on and off."""
     torch.backends.cuda.matmul.allow_tf32 = False
     data = DeviceBatches(torch, device)
     out = {"config": f"config1 MLP {CONFIG1_DIMS}, B={BATCH}, Adam lr 1e-4, 1F1B D={depth} on 1 GPU "
-                     f"(single-process runner), {n_batches} mini-batches, fp32 GEMMs (TF32 off)"}
+                     f"(single-process runner, CUDA-graph replay of whole {n_batches}-mini-batch runs), "
+                     f"fp32 GEMMs (TF32 off)"}
     launches = 0
     for strategy in ("async_raw", "optimizer_prediction"):
-        _run_once(torch, device, strategy, depth, min(n_batches, 2 * depth + 2), data)  # warm-up
-        rep, sec, wall = _run_once(torch, device, strategy, depth, n_batches, data)
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
-        out[key] = {"samples_per_s": round(n_batches * BATCH / sec, 1), "s": round(sec, 4),
-                    "wall_s": round(wall, 4), "final_loss": rep.losses[-1]}
-        # predictor/optimizer launches: one per update (K2/K3) + K1 per unfused predicted forward
-        launches += n_batches * depth + (n_batches if strategy == "optimizer_prediction" else 0)
+        rep, sec, n_launch = _graphed(torch, device, strategy, depth, n_batches, data, replays)
+        _run_once(torch, device, strategy, depth, min(n_batches, 2 * depth + 2), data)  # eager warm-up
+        _, esec, _ = _run_once(torch, device, strategy, depth, n_batches, data)
+        out[key] = {"samples_per_s": round(n_batches * BATCH / sec, 1), "s_per_run": round(sec, 5),
+                    "eager_samples_per_s": round(n_batches * BATCH / esec, 1), "final_loss": rep.losses[-1],
+                    "optimizer_launches_per_run": n_launch}
+        launches += n_launch * replays
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out["value"] = on
     out["unit"] = "samples/s"
     out["prediction_overhead"] = round(1.0 - on / off, 4)
+    out["eager_prediction_overhead"] = round(
+        1.0 - out["pred_on"]["eager_samples_per_s"] / out["pred_off"]["eager_samples_per_s"], 4)
     out["launches"] = launches
     return out
 

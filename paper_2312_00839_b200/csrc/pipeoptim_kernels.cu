@@ -56,8 +56,25 @@ struct Args {
   float* out;          // w_hat or dir_out
   int64_t n;
   unsigned long long* bad;  // smallest non-finite flat index (atomicMin)
+  const po_coef* dc;   // nullable: per-launch scalars read from device memory
+                       // (CUDA-graph replays), overriding c.{lr,c_pred,bc1,bc2}
   Coef c;
 };
+
+// The launch's coefficients: by value, or — for graph-captured launches whose
+// step count / learning rate change between replays — from a device po_coef
+// the host refreshes before each replay.
+__device__ __forceinline__ Coef load_coef(const Args& a) {
+  Coef c = a.c;
+  if (a.dc != nullptr) {
+    const po_coef d = *a.dc;
+    c.lr = d.lr;
+    c.c_pred = d.c_pred;
+    c.bc1 = d.bc1;
+    c.bc2 = d.bc2;
+  }
+  return c;
+}
 
 __host__ __device__ constexpr bool uses_w(int mode) {
   return mode == MODE_STEP || mode == MODE_STEP_DIR || mode == MODE_PREDICT ||
@@ -226,7 +243,7 @@ __device__ __forceinline__ void elem(const Coef& c, float& w, float g, float& s1
 }
 
 template <int KIND, int MODE, int VEC, int CACHE>
-__device__ __forceinline__ void do_vec(const Args& a, int64_t vi, int64_t& bad) {
+__device__ __forceinline__ void do_vec(const Args& a, const Coef& c, int64_t vi, int64_t& bad) {
   const int64_t base = vi * VEC;
   Vec<VEC> w{}, g{}, s1{}, s2{}, out{};
   if constexpr (uses_w(MODE)) w = vload<VEC, CACHE, !writes_w(MODE)>(a.w + base);
@@ -236,7 +253,7 @@ __device__ __forceinline__ void do_vec(const Args& a, int64_t vi, int64_t& bad) 
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
     bool e = false;
-    elem<KIND, MODE>(a.c, w.v[j], g.v[j], s1.v[j], s2.v[j], out.v[j], e);
+    elem<KIND, MODE>(c, w.v[j], g.v[j], s1.v[j], s2.v[j], out.v[j], e);
     if (e && bad == INT64_MAX) bad = base + j;
   }
   if constexpr (writes_w(MODE)) vstore<VEC, CACHE>(a.w + base, w);
@@ -257,6 +274,7 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t bad = INT64_MAX;
   int64_t i = tid;
+  const Coef c = load_coef(a);
 
   for (; i + (UNROLL - 1) * stride < nv; i += UNROLL * stride) {
     Vec<VEC> w[UNROLL], g[UNROLL], s1[UNROLL], s2[UNROLL], out[UNROLL];
@@ -274,7 +292,7 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
         bool e = false;
-        elem<KIND, MODE>(a.c, w[u].v[j], g[u].v[j], s1[u].v[j], s2[u].v[j], out[u].v[j], e);
+        elem<KIND, MODE>(c, w[u].v[j], g[u].v[j], s1[u].v[j], s2[u].v[j], out[u].v[j], e);
         if (e && bad == INT64_MAX) bad = base + j;
       }
       if constexpr (writes_w(MODE)) vstore<VEC, CACHE>(a.w + base, w[u]);
@@ -285,7 +303,7 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
       if constexpr (writes_out(MODE)) vstore<VEC, CACHE>(a.out + base, out[u]);
     }
   }
-  for (; i < nv; i += stride) do_vec<KIND, MODE, VEC, CACHE>(a, i, bad);
+  for (; i < nv; i += stride) do_vec<KIND, MODE, VEC, CACHE>(a, c, i, bad);
 
   // scalar tail [nv*VEC, n): fewer than VEC elements
   const int64_t t = nv * VEC + tid;
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
     if constexpr (uses_s1(MODE)) s1 = a.s1[t];
     if constexpr (uses_s2(KIND, MODE)) s2 = a.s2[t];
     bool e = false;
-    elem<KIND, MODE>(a.c, w, g, s1, s2, out, e);
+    elem<KIND, MODE>(c, w, g, s1, s2, out, e);
     if (e && bad == INT64_MAX) bad = t;
     if constexpr (writes_w(MODE)) a.w[t] = w;
     if constexpr (writes_state(MODE)) {
@@ -513,7 +531,7 @@ int po_step(const po_hparams* hp, float* w, const float* g, float* state1, float
   if (n > 0 && (w == nullptr || g == nullptr || state1 == nullptr)) return PO_EINVAL;
   if (n > 0 && hp->kind != PO_SGDM && state2 == nullptr) return PO_EINVAL;
   Args a{w, g, state1, hp->kind == PO_SGDM ? nullptr : state2, dir_out, n,
-         reinterpret_cast<unsigned long long*>(nonfinite_index),
+         reinterpret_cast<unsigned long long*>(nonfinite_index), nullptr,
          coef(hp, lr, 0.0, step_count + 1)};
   return run(hp->kind, dir_out ? MODE_STEP_DIR : MODE_STEP, a, launch, (cudaStream_t)stream);
 }
@@ -528,7 +546,7 @@ int po_predict(const po_hparams* hp, const float* w, const float* state1, const 
     return PO_EINVAL;
   Args a{const_cast<float*>(w), nullptr,
          zero ? nullptr : const_cast<float*>(state1),
-         (zero || hp->kind == PO_SGDM) ? nullptr : const_cast<float*>(state2), w_hat, n, nullptr,
+         (zero || hp->kind == PO_SGDM) ? nullptr : const_cast<float*>(state2), w_hat, n, nullptr, nullptr,
          coef(hp, 0.0, lr_times_s, step_count)};
   return run(hp->kind, zero ? MODE_PREDICT_ZERO : MODE_PREDICT, a, launch, (cudaStream_t)stream);
 }
@@ -541,7 +559,7 @@ int po_step_predict(const po_hparams* hp, float* w, const float* g, float* state
     return PO_EINVAL;
   if (n > 0 && hp->kind != PO_SGDM && state2 == nullptr) return PO_EINVAL;
   Args a{w, g, state1, hp->kind == PO_SGDM ? nullptr : state2, w_hat, n,
-         reinterpret_cast<unsigned long long*>(nonfinite_index),
+         reinterpret_cast<unsigned long long*>(nonfinite_index), nullptr,
          coef(hp, lr, lr_pred_times_s, step_count + 1)};
   return run(hp->kind, MODE_STEP_PREDICT, a, launch, (cudaStream_t)stream);
 }
@@ -554,7 +572,7 @@ int po_direction(const po_hparams* hp, const float* state1, const float* state2,
   if (!zero && n > 0 && (state1 == nullptr || (hp->kind != PO_SGDM && state2 == nullptr)))
     return PO_EINVAL;
   Args a{nullptr, nullptr, zero ? nullptr : const_cast<float*>(state1),
-         (zero || hp->kind == PO_SGDM) ? nullptr : const_cast<float*>(state2), dir_out, n, nullptr,
+         (zero || hp->kind == PO_SGDM) ? nullptr : const_cast<float*>(state2), dir_out, n, nullptr, nullptr,
          coef(hp, 0.0, 0.0, step_count)};
   return run(hp->kind, zero ? MODE_DIRECTION_ZERO : MODE_DIRECTION, a, launch,
              (cudaStream_t)stream);
@@ -566,8 +584,58 @@ int po_axpy_predict(const float* w, const float* d, float* w_hat, int64_t n, dou
   Coef c;
   memset(&c, 0, sizeof(c));
   c.c_pred = (float)lr_times_s;
-  Args a{const_cast<float*>(w), nullptr, const_cast<float*>(d), nullptr, w_hat, n, nullptr, c};
+  Args a{const_cast<float*>(w), nullptr, const_cast<float*>(d), nullptr, w_hat, n, nullptr, nullptr, c};
   return run(PO_SGDM, MODE_AXPY, a, launch, (cudaStream_t)stream);
+}
+
+int po_coef_fill(const po_hparams* hp, int32_t which, double lr, double lr_times_s, int64_t step_count,
+                 po_coef* out) {
+  if (!valid_hp(hp) || out == nullptr || step_count < 0) return PO_EINVAL;
+  Coef c;
+  switch (which) {
+    case PO_COEF_STEP: c = coef(hp, lr, 0.0, step_count + 1); break;
+    case PO_COEF_PREDICT: c = coef(hp, 0.0, lr_times_s, step_count); break;  // t = 0 -> bc = 1
+    case PO_COEF_STEP_PREDICT: c = coef(hp, lr, lr_times_s, step_count + 1); break;
+    default: return PO_EINVAL;
+  }
+  out->lr = c.lr;
+  out->c_pred = c.c_pred;
+  out->bc1 = c.bc1;
+  out->bc2 = c.bc2;
+  return 0;
+}
+
+int po_step_dc(const po_hparams* hp, float* w, const float* g, float* state1, float* state2, int64_t n,
+               const po_coef* coef_dev, int64_t* nonfinite_index, const po_launch* launch, void* stream) {
+  if (!valid_hp(hp) || coef_dev == nullptr) return PO_EINVAL;
+  if (n > 0 && (w == nullptr || g == nullptr || state1 == nullptr)) return PO_EINVAL;
+  if (n > 0 && hp->kind != PO_SGDM && state2 == nullptr) return PO_EINVAL;
+  Args a{w, g, state1, hp->kind == PO_SGDM ? nullptr : state2, nullptr, n,
+         reinterpret_cast<unsigned long long*>(nonfinite_index), coef_dev, coef(hp, 0.0, 0.0, 1)};
+  return run(hp->kind, MODE_STEP, a, launch, (cudaStream_t)stream);
+}
+
+int po_predict_dc(const po_hparams* hp, const float* w, const float* state1, const float* state2, float* w_hat,
+                  int64_t n, const po_coef* coef_dev, const po_launch* launch, void* stream) {
+  if (!valid_hp(hp) || coef_dev == nullptr) return PO_EINVAL;
+  if (n > 0 && (w == nullptr || w_hat == nullptr || state1 == nullptr ||
+                (hp->kind != PO_SGDM && state2 == nullptr)))
+    return PO_EINVAL;
+  Args a{const_cast<float*>(w), nullptr, const_cast<float*>(state1),
+         hp->kind == PO_SGDM ? nullptr : const_cast<float*>(state2), w_hat, n, nullptr, coef_dev,
+         coef(hp, 0.0, 0.0, 1)};
+  return run(hp->kind, MODE_PREDICT, a, launch, (cudaStream_t)stream);
+}
+
+int po_step_predict_dc(const po_hparams* hp, float* w, const float* g, float* state1, float* state2,
+                       float* w_hat, int64_t n, const po_coef* coef_dev, int64_t* nonfinite_index,
+                       const po_launch* launch, void* stream) {
+  if (!valid_hp(hp) || coef_dev == nullptr) return PO_EINVAL;
+  if (n > 0 && (w == nullptr || g == nullptr || state1 == nullptr || w_hat == nullptr)) return PO_EINVAL;
+  if (n > 0 && hp->kind != PO_SGDM && state2 == nullptr) return PO_EINVAL;
+  Args a{w, g, state1, hp->kind == PO_SGDM ? nullptr : state2, w_hat, n,
+         reinterpret_cast<unsigned long long*>(nonfinite_index), coef_dev, coef(hp, 0.0, 0.0, 1)};
+  return run(hp->kind, MODE_STEP_PREDICT, a, launch, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -237,7 +237,8 @@ class OptimizerState:
         self._hp = config.hparams()
         self._launch = launch
         self._lib = _lib.load()
-        self._pending_check_step: int | None = None
+        # CUDA-graph mode: launches take their scalars from a CoefTape slot
+        self.tape: "CoefTape | None" = None
 
     # -- state plumbing ---------------------------------------------------------
 
@@ -332,6 +333,15 @@ class OptimizerState:
         """K2: one update in place on flat.data from flat.grad."""
         self._bind(flat.layout)
         self._ensure_state()
+        if self.tape is not None:
+            slot = self.tape.record(self, _lib.PO_COEF_STEP, lr, 0.0)
+            rc = self._lib.po_step_dc(
+                ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1), _ptr(self._s2),
+                flat.layout.numel, slot, _ptr(self._bad), self._launch_ref(), _stream(flat.data.device),
+            )
+            _lib.check(rc, "po_step_dc")
+            self.step_count += 1
+            return
         rc = self._lib.po_step(
             ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1),
             _ptr(self._s2), None, flat.layout.numel, float(lr), self.step_count,
@@ -346,8 +356,16 @@ class OptimizerState:
         if steps_ahead < 0:
             raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
         self._bind(flat.layout)
-        if self.step_count > 0:
+        if self.step_count > 0 or self.tape is not None:
             self._ensure_state()
+        if self.tape is not None:
+            slot = self.tape.record(self, _lib.PO_COEF_PREDICT, 0.0, float(lr) * steps_ahead)
+            rc = self._lib.po_predict_dc(
+                ctypes.byref(self._hp), _ptr(flat.data), _ptr(self._s1), _ptr(self._s2), _ptr(out),
+                flat.layout.numel, slot, self._launch_ref(), _stream(flat.data.device),
+            )
+            _lib.check(rc, "po_predict_dc")
+            return
         rc = self._lib.po_predict(
             ctypes.byref(self._hp), _ptr(flat.data), _ptr(self._s1), _ptr(self._s2), _ptr(out),
             flat.layout.numel, float(lr) * steps_ahead, self.step_count, self._launch_ref(),
@@ -363,6 +381,16 @@ class OptimizerState:
             raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
         self._bind(flat.layout)
         self._ensure_state()
+        if self.tape is not None:
+            slot = self.tape.record(self, _lib.PO_COEF_STEP_PREDICT, lr, float(lr_pred) * steps_ahead)
+            rc = self._lib.po_step_predict_dc(
+                ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1), _ptr(self._s2),
+                _ptr(out), flat.layout.numel, slot, _ptr(self._bad), self._launch_ref(),
+                _stream(flat.data.device),
+            )
+            _lib.check(rc, "po_step_predict_dc")
+            self.step_count += 1
+            return
         rc = self._lib.po_step_predict(
             ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1),
             _ptr(self._s2), _ptr(out), flat.layout.numel, float(lr), float(lr_pred) * steps_ahead,
@@ -431,6 +459,69 @@ class OptimizerState:
         )
         _lib.check(rc, "po_direction")
         return self._out(out, host)
+
+
+class CoefTape:
+    """Device-resident per-launch coefficients for CUDA-graph capture.
+
+    While a graph is being captured, every K1/K2/K3 launch of an attached
+    OptimizerState records (optimizer, kind, step count relative to the
+    capture start, lr, lr*s) and gets a slot in a device po_coef array.
+    Before each replay, `refresh()` recomputes every slot for the optimizer's
+    CURRENT step count (host double arithmetic, `po_coef_fill`) and copies the
+    array to the device on the replay stream, so replaying the graph
+    continues training exactly as re-running the eager code would.
+    """
+
+    def __init__(self, device, capacity: int = 1 << 14):
+        self.device = torch.device(device)
+        self.capacity = capacity
+        self.dev = torch.zeros(capacity * 4, dtype=torch.float32, device=self.device)
+        # double-buffered pinned staging: a refresh never overwrites a buffer
+        # whose H2D copy may still be pending
+        self.host = [torch.zeros(capacity * 4, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.copied = [None, None]
+        self.flip = 0
+        self.entries: list[tuple] = []
+        self.base: dict[int, int] = {}
+        self._lib = _lib.load()
+
+    def begin(self, opts) -> None:
+        """Start recording: remember each optimizer's step count at capture start."""
+        self.entries.clear()
+        self.base = {id(o): o.step_count for o in opts}
+        for o in opts:
+            o.tape = self
+
+    def end(self, opts) -> None:
+        for o in opts:
+            o.tape = None
+
+    def record(self, opt, which: int, lr: float, lr_times_s: float) -> int:
+        i = len(self.entries)
+        if i >= self.capacity:
+            raise RuntimeError("CoefTape capacity exceeded")
+        self.entries.append((opt, which, opt.step_count - self.base[id(opt)], float(lr), float(lr_times_s)))
+        return self.dev.data_ptr() + 16 * i
+
+    def refresh(self, step_counts: dict[int, int], stream=None) -> None:
+        """Fill every slot for the optimizers' step counts at replay start."""
+        k = self.flip
+        self.flip ^= 1
+        if self.copied[k] is not None:
+            self.copied[k].synchronize()
+        host = self.host[k]
+        buf = (_lib.po_coef * self.capacity).from_address(host.data_ptr())
+        for i, (opt, which, rel, lr, c) in enumerate(self.entries):
+            rc = self._lib.po_coef_fill(ctypes.byref(opt._hp), which, lr, c, step_counts[id(opt)] + rel,
+                                        ctypes.addressof(buf[i]))
+            _lib.check(rc, "po_coef_fill")
+        n = 4 * len(self.entries)
+        if n:
+            self.dev[:n].copy_(host[:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self.copied[k] = ev
 
 
 class HostStreamer:

@@ -225,3 +225,43 @@ def test_execute_rejects_bad_inputs():
     with pytest.raises(ValueError):
         execute(build_timeline("spectrain", 4, 4), stages, [type(o)(type(o.config)("adam"), o.names) for o in opts],
                 "spectrain", src, "mse", lambda mb: 0.01)
+
+
+@pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("optimizer_prediction", "sgdm"),
+                                           ("async_raw", "adamw")])
+def test_graph_replays_continue_training_like_eager_runs(strategy, kind):
+    """GraphedExecute: warm-up eager run + 2 replays == 3 eager runs (each a full
+    run of the timeline from the current state); coefficients advance."""
+    import torch
+
+    from paper_2312_00839_b200.bench_pipeline import DeviceBatches
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import GraphedExecute, build_timeline, execute
+    from paper_2312_00839_b200.stages import build_layers, build_stages, torch_init
+
+    dev = torch.device("cuda", 0)
+    dims, acts = [64, 96, 96, 80, 10], ["relu", "relu", "relu", "linear"]
+    data = DeviceBatches(torch, dev, dims=dims)
+    tl = build_timeline(strategy, 4, 9)
+
+    def setup():
+        stages = build_stages(build_layers(dims, acts), 4, torch_init(3, dev), device=dev)
+        return stages, [OptimizerState(OptimizerConfig(kind), s.param_names, device=dev) for s in stages]
+
+    sa, oa = setup()
+    eager_losses = []
+    for _ in range(3):
+        for s in sa:
+            s.version = 1
+        eager_losses.append(execute(tl, sa, oa, strategy, data, "softmax_xent", lambda mb: 1e-3,
+                                    checks="deferred").losses)
+    sb, ob = setup()
+    g = GraphedExecute(tl, sb, ob, strategy, data, "softmax_xent", lambda mb: 1e-3, warmup_runs=1)
+    graph_losses = []
+    for _ in range(2):
+        g.replay()
+        graph_losses.append(g.report().losses)
+    assert [o.step_count for o in ob] == [o.step_count for o in oa] == [27] * 4
+    np.testing.assert_allclose(graph_losses, eager_losses[1:], rtol=1e-5, atol=1e-7)
+    for x, y in zip(sa, sb):
+        assert float((x.flat.data - y.flat.data).abs().max()) <= 1e-5 * float(x.flat.data.abs().max())
