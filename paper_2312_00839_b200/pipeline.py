@@ -29,12 +29,11 @@ from .runtime import (
     PREDICTIVE_STRATEGIES,
     STRATEGY_SCHEDULE,
     VersionRecord,
-    _LivePolicy,
-    _PredictivePolicy,
+    _make_policy,
     _StageRt,
     _to_device,
 )
-from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, update_gaps, validate_timeline
+from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
 from .stages import StageModel, loss_and_grad
 
 
@@ -101,7 +100,7 @@ class PipelineStageRunner:
         self.eager = checks == "eager"
         self.fuse = fuse
         self.predictive = strategy in PREDICTIVE_STRATEGIES
-        self.policy = _PredictivePolicy(update_gaps(tl)) if self.predictive else _LivePolicy()
+        self.policy = _make_policy(strategy, tl)
         self.rt = _StageRt(stage, opt, self.depth)
         self.program = stage_program(tl, self.rank, predictive=self.predictive)
         self.comm = _Exchange(dist, group)

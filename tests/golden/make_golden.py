@@ -172,6 +172,25 @@ def make_runtime():
                          "strategy": strategy, "kind": kind, "lr": lr, "init_seed": 5, "data_seed": 101,
                          "rows": 8, "weight_decay": cfg.weight_decay, **_report(rep, stages)}
                     )
+    # §8(f) next: the paper's comparison policies and the synchronous schedules
+    for strategy, depth, micros in (("weight_stashing", 4, 1), ("two_buffered", 4, 1), ("gpipe", 4, 4),
+                                    ("gpipe", 2, 1), ("naive", 4, 1), ("serial", 1, 1), ("spectrain", 4, 1)):
+        for kind, lr in (("sgdm", 0.05), ("adam", 0.01)):
+            if strategy == "spectrain" and kind != "sgdm":
+                continue
+            n = 14
+            layers = build_layers(SMALL_DIMS, SMALL_ACTS)
+            stages = build_stages(layers, depth, RngStream(5).substream("params"))
+            cfg = OptimizerConfig(kind, weight_decay=0.0) if kind == "sgdm" else OptimizerConfig(kind)
+            opts = [OptimizerState(cfg, s.param_names) for s in stages]
+            tl = build_timeline(strategy, depth, n, micros)
+            rep = execute(tl, stages, opts, strategy, RegressionSource(101, 8, SMALL_DIMS[0], SMALL_DIMS[-1]),
+                          "mse", lambda mb, lr=lr: lr)
+            runs.append(
+                {"name": "small_extra", "dims": SMALL_DIMS, "acts": SMALL_ACTS, "depth": depth, "n": n,
+                 "micros": micros, "strategy": strategy, "kind": kind, "lr": lr, "init_seed": 5, "data_seed": 101,
+                 "rows": 8, "weight_decay": cfg.weight_decay, **_report(rep, stages)}
+            )
     # config 1: the CPU-reference run, prediction on and off
     for depth in (4,):
         for strategy in ("optimizer_prediction", "async_raw"):

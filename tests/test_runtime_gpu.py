@@ -69,7 +69,7 @@ def build(case, strategy=None, device="cuda"):
     kw = {"weight_decay": case.get("weight_decay", 5e-4)} if case["kind"] == "sgdm" else {}
     cfg = OptimizerConfig(case["kind"], **kw)
     opts = [OptimizerState(cfg, s.param_names) for s in stages]
-    tl = build_timeline(strategy or case["strategy"], case["depth"], case["n"])
+    tl = build_timeline(strategy or case["strategy"], case["depth"], case["n"], case.get("micros", 1))
     return tl, stages, opts
 
 
@@ -77,7 +77,7 @@ def run_case(case, checks="eager", fuse=True, strategy=None):
     from paper_2312_00839_b200.runtime import execute
 
     tl, stages, opts = build(case, strategy)
-    if case["name"] == "small":
+    if case["name"].startswith("small"):
         src = Source(case["data_seed"], case["rows"], case["dims"][0], case["dims"][-1])
         loss = "mse"
     else:
@@ -114,6 +114,16 @@ def test_small_runs_match_reference(case):
     for stage, want_stage in zip(stages, case["params"]):
         for p, want in zip(stage.params, want_stage):
             assert optim_ref.inf_norm_rel(p.detach().cpu().double().numpy(), np.array(want)) <= PARAM_TOL
+
+
+EXTRA = [c for c in GOLDEN if c["name"] == "small_extra"]
+
+
+@pytest.mark.parametrize("case", EXTRA, ids=lambda c: f"D{c['depth']}-{c['strategy']}-T{c['micros']}-{c['kind']}")
+def test_other_strategies_match_reference(case):
+    """§8(f) next #1/#2: weight stashing, 2BW, GPipe micro-batch mean
+    accumulation, naive, serial and SpecTrain on the device vs the reference."""
+    test_small_runs_match_reference(case)
 
 
 CONFIG1 = [c for c in GOLDEN if c["name"] == "config1"]
