@@ -228,7 +228,32 @@ def make_rng():
     (HERE / "rng_golden.json").write_text(json.dumps(out) + "\n")
 
 
+def make_files():
+    """The reference's own report.json / losses.csv / versions.csv for a small
+    PipeOptim run (experiments.write_run_outputs, experiments.py:375-392)."""
+    import tempfile
+
+    cfg = config_from_dict({
+        "name": "files", "seed": 0, "depth": 4, "strategy": "optimizer_prediction",
+        "schedule": {"kind": "1f1b"},
+        "model": {"layer_dims": [4, 8, 8, 8, 1], "activations": ["tanh", "tanh", "tanh", "linear"]},
+        "optimizer": {"kind": "adam"},
+        "training": {"n_epochs": 2, "batch_size": 16, "lr": 0.01},
+        "dataset": {"kind": "synthetic-regression", "n_samples": 210, "seed": 5, "input_dim": 4,
+                    "target_dim": 1, "noise": 0.05},
+    })
+    res = X.run_experiment(cfg)
+    out = HERE / "files"
+    out.mkdir(exist_ok=True)
+    with tempfile.TemporaryDirectory() as td:
+        d = X.write_run_outputs(res, Path(td), "csv")
+        for name in ("report.json", "losses.csv", "versions.csv"):
+            (out / name).write_text((d / name).read_text())
+    (out / "config.json").write_text(json.dumps(cfg.model_dump(mode="json"), indent=2, sort_keys=True) + "\n")
+
+
 if __name__ == "__main__":
+    make_files()
     make_optim()
     make_schedule()
     make_rng()
