@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-pipeline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--pipeline-batches", type=int, default=64)
+    ap.add_argument("--pipeline-timeout", type=float, default=420.0)
+    ap.add_argument("--no-configs", action="store_true", help="skip configs 2-4 in the pipeline leg")
     return ap.parse_args()
 
 
@@ -307,14 +309,29 @@ def e2e_leg(args, torch, dist, world, device):
 
 
 def pipeline_leg(args, torch, dist, rank, world, device):
-    """Config 1 through the 1F1B runner: samples/s with prediction on vs off."""
+    """Config 1 through the 1F1B runner (+ configs 2-4 unless --no-configs):
+    samples/s with prediction on vs off."""
+    from paper_2312_00839_b200 import bench_pipeline as bp
+
     if world == 1:
-        from paper_2312_00839_b200.bench_pipeline import single_gpu_pipeline
+        out = bp.single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches)
+    else:
+        out = bp.multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches)
+    if not args.no_configs:
+        from paper_2312_00839_b200.pipeline import bench_module_pipeline
 
-        return single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches)
-    from paper_2312_00839_b200.bench_pipeline import multi_gpu_pipeline
-
-    return multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches)
+        configs = {}
+        for name in bp.MODULE_CONFIGS:
+            try:
+                if world == 1:
+                    configs[name] = bp.single_gpu_module_pipeline(torch, device, name, n_batches=16)
+                else:
+                    configs[name] = bench_module_pipeline(torch, dist, rank, world, device, name, n_batches=16)
+            except Exception as exc:
+                configs[name] = {"error": f"{type(exc).__name__}: {exc}"}
+            torch.cuda.empty_cache()
+        out["configs"] = configs
+    return out
 
 
 def ours(args):
@@ -330,15 +347,41 @@ def ours(args):
         dist.init_process_group("nccl", device_id=device)
     kern = kernel_leg(args, torch, dist, rank, world, device)
     e2e = None if args.no_e2e else e2e_leg(args, torch, dist, world, device)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.kind)
+    line = _line(args, kern, e2e, cpu, world)
     pipe = None
     if not args.no_pipeline:
+        # the pipeline leg runs last under a watchdog: a hung NCCL exchange must
+        # not cost the kernel measurement — rank 0 then prints the line with the
+        # pipeline marked as timed out and every rank exits
+        import threading
+
+        def _expire():
+            if rank == 0:
+                line["pipeline"] = {"error": f"timeout after {args.pipeline_timeout} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        dog = threading.Timer(args.pipeline_timeout, _expire)
+        dog.daemon = True
+        dog.start()
         try:
             pipe = pipeline_leg(args, torch, dist, rank, world, device)
         except Exception as exc:  # reported, never silently dropped
             pipe = {"error": f"{type(exc).__name__}: {exc}"}
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.kind)
+        dog.cancel()
+    line["pipeline"] = pipe
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _line(args, kern, e2e, cpu, world):
     peak, peak_src = measured_peak()
     traffic = ncu_traffic()
     gbs = kern["gbs_per_rank"]
@@ -372,7 +415,7 @@ def ours(args):
             "frac": round(gbs / peak, 4),
             "frac_of_8tbs": round(gbs / 8000.0, 4),
             "peak_source": peak_src,
-            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+            "traffic": (round(traffic["dram_bytes_per_launch"] * kern["n"] / traffic["n"]) if traffic else None),
             "traffic_note": (f"ncu dram__bytes_read+write per launch at n={traffic.get('n')}" if traffic else
                              "no ncu capture committed"),
             "kernel": "po_stream_kernel<ADAM, STEP_PREDICT> (K3)",
@@ -381,16 +424,11 @@ def ours(args):
         "clocks": kern["clocks"],
         "e2e": e2e,
         "gpu_launches": launches,
-        "pipeline": pipe,
+        "pipeline": None,
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
-    if world > 1:
-        dist.barrier()
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    return line
 
 
 def main():

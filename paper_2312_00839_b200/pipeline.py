@@ -277,3 +277,50 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
     out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4),
                launches=n_batches * 2)
     return out
+
+
+def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_batches: int = 16):
+    """Configs 2-4 on `world` GPUs, one stage per GPU (depth = world):
+    prediction on vs off, samples/s device-timed, max over ranks."""
+    from .bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import build_timeline
+
+    cfg = MODULE_CONFIGS[name]
+    torch_mod.backends.cuda.matmul.allow_tf32 = True
+    torch_mod.backends.cudnn.allow_tf32 = True
+    data = ModuleBatches(torch_mod, device, cfg)
+    out = {"config": f"{name}: D={world} (one stage per GPU, NCCL P2P), batch {cfg['batch']}, {cfg['opt']}, "
+                     f"{n_batches} mini-batches, TF32 convs/GEMMs, fp32 master weights"}
+    for strategy in ("async_raw", "optimizer_prediction"):
+        times = []
+        for trial, n in enumerate((2 * world, n_batches)):
+            stages, _ = module_stages_for(torch_mod, name, device, depth=world)
+            stage = stages[rank]
+            for k, st in enumerate(stages):  # only this rank's stage stays on the device
+                if k != rank:
+                    st.module.to("cpu")
+            del stages
+            kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
+            opt = OptimizerState(OptimizerConfig(cfg["opt"], **kw), stage.param_names, device=device)
+            tl = build_timeline(strategy, world, n)
+            runner = PipelineStageRunner(dist, tl, stage, opt, strategy, data, "softmax_xent", lambda mb: cfg["lr"],
+                                         cfg["batch"])
+            torch_mod.cuda.synchronize(device)
+            dist.barrier()
+            e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
+            e0.record()
+            runner.run()
+            e1.record()
+            torch_mod.cuda.synchronize(device)
+            dist.barrier()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        t = torch_mod.tensor([times[-1]], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
+        out[key] = {"samples_per_s": round(n_batches * cfg["batch"] / float(t.item()), 2), "s": round(float(t.item()), 4)}
+    on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
+    out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4))
+    torch_mod.backends.cuda.matmul.allow_tf32 = False
+    torch_mod.backends.cudnn.allow_tf32 = False
+    return out

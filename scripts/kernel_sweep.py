@@ -70,6 +70,9 @@ def call(lib, kernel, kind, b: Buffers, launch, stream, t=10, s=3, lr=1e-3):
     _lib.check(rc, kernel)
 
 
+FLUSH = True
+
+
 def time_kernel(lib, kernel, kind, b, launch=None, reps=20, warmup=5):
     stream = torch.cuda.current_stream()
     # L2 flush by READING 256 MB (2x L2): clean lines, so the timed kernel does
@@ -79,7 +82,8 @@ def time_kernel(lib, kernel, kind, b, launch=None, reps=20, warmup=5):
         call(lib, kernel, kind, b, launch, stream.cuda_stream)
     times = []
     for _ in range(reps):
-        flush.sum()
+        if FLUSH:
+            flush.sum()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -118,12 +122,32 @@ def main():
     ap.add_argument("--tune-all", action="store_true",
                     help="focused launch-shape search for every kernel x kind")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-flush", action="store_true", help="warm L2 (pipeline-like) instead of flushing")
+    ap.add_argument("--tune-small", action="store_true", help="launch-shape search at 2^20..2^24")
     args = ap.parse_args()
+    global FLUSH
+    FLUSH = not args.no_flush
     lib = _lib.load()
     peak = peak_gbs()
     rows = []
     print(f"# device {torch.cuda.get_device_name()}  measured copy peak {peak} GB/s", flush=True)
-    if args.tune_all:
+    if args.tune_small:
+        shapes = [(512, 1, 1), (512, 2, 1), (512, 4, 1), (256, 8, 1), (256, 4, 2), (128, 16, 1), (1024 // 2, 2, 2),
+                  (256, 8, 2), (128, 16, 2), (256, 6, 1)]
+        for lg in (20, 22, 24):
+            n = 1 << lg
+            b = Buffers(n)
+            for kernel in args.kernels.split(","):
+                for kind in args.kinds.split(","):
+                    for block, cps, unroll in shapes:
+                        la = _lib.make_launch(block, cps, 8, 1, unroll)
+                        med, best = time_kernel(lib, kernel, kind, b, la, reps=20, warmup=3)
+                        gbs = BYTES[(kernel, kind)] * n / med / 1e9
+                        row = dict(n=n, kernel=kernel, kind=kind, block=block, cps=cps, unroll=unroll,
+                                   us=round(med * 1e6, 2), gbs=round(gbs, 1), flush=FLUSH)
+                        rows.append(row)
+                        print(json.dumps(row), flush=True)
+    elif args.tune_all:
         n = 1 << args.tune_log2
         b = Buffers(n)
         print(f"# torch copy_ at 2^{args.tune_log2}: {copy_gbs(n):.1f} GB/s", flush=True)
