@@ -80,7 +80,13 @@ class PipelineStageRunner:
     """Runs one stage's 1F1B program on this rank."""
 
     def __init__(self, dist, tl: Timeline, stage: StageModel, opt, strategy: str, data, loss_kind: str,
-                 lr_for_mb, rows: int, *, checks: str = "deferred", fuse: bool = True, group=None):
+                 lr_for_mb, rows: int, *, checks: str = "deferred", fuse: bool = True, group=None,
+                 stage_ranks: list[int] | None = None, dp_group=None, dp_rank: int = 0, dp_size: int = 1):
+        """stage_ranks[k] is the global rank holding stage k of this pipeline
+        replica (default: rank k). With dp_size > 1 (hybrid DP x PP), replica
+        `dp_rank` trains on rows [dp_rank*rows, (dp_rank+1)*rows) of every
+        batch and the stage gradient is averaged over `dp_group` before each
+        update, so the replicas stay identical."""
         if STRATEGY_SCHEDULE.get(strategy) != "1f1b" or tl.kind != "1f1b":
             raise ValueError(f"the distributed runner executes 1f1b strategies, got {strategy!r} on {tl.kind!r}")
         if strategy == "spectrain" and opt.config.kind != "sgdm":
@@ -105,15 +111,17 @@ class PipelineStageRunner:
         self.program = stage_program(tl, self.rank, predictive=self.predictive)
         self.comm = _Exchange(dist, group)
         self.device = stage.flat.device
+        self.stage_ranks = stage_ranks or list(range(self.depth))
+        self.dp_group, self.dp_rank, self.dp_size = dp_group, dp_rank, dp_size
         opt.eager_checks = self.eager
 
     # -- what each op consumes / produces -------------------------------------------------
 
     def _input_spec(self, op):
         if op.kind == FORWARD and self.rank > 0:
-            return (self.rows, *self.stage.in_shape), self.rank - 1
+            return (self.rows, *self.stage.in_shape), self.stage_ranks[self.rank - 1]
         if op.kind == BACKWARD and self.rank < self.depth - 1:
-            return (self.rows, *self.stage.out_shape), self.rank + 1
+            return (self.rows, *self.stage.out_shape), self.stage_ranks[self.rank + 1]
         return None
 
     def run(self) -> StageReport:
@@ -152,7 +160,7 @@ class PipelineStageRunner:
             out_msg = None
             if op.kind == FORWARD:
                 if self.rank == 0:
-                    inp = _to_device(self.data.batch(op.mb)[0], self.device)
+                    inp = self._shard(_to_device(self.data.batch(op.mb)[0], self.device))
                 weights, fv, predicted, target = self.policy.forward_view(self.rt, op.mb, 0, self.lr_for_mb(op.mb))
                 try:
                     out = self.stage.run_forward(weights, (op.mb, 0), inp, fv, check_finite=self.eager,
@@ -163,9 +171,9 @@ class PipelineStageRunner:
                 records[op.mb] = rec
                 order.append(rec)
                 if self.rank < self.depth - 1:
-                    out_msg = (out.contiguous(), self.rank + 1)
+                    out_msg = (out.contiguous(), self.stage_ranks[self.rank + 1])
                 else:
-                    y = _to_device(self.data.batch(op.mb)[1], self.device)
+                    y = self._shard(_to_device(self.data.batch(op.mb)[1], self.device))
                     loss, g = loss_and_grad(out, y, self.loss_kind)
                     if self.eager and not bool(torch.isfinite(loss)):
                         raise NumericError(f"mb {op.mb} stage {self.rank}: non-finite loss under {self.loss_kind}")
@@ -181,7 +189,7 @@ class PipelineStageRunner:
                 rec.backward_version = bv
                 rec.live_backward_version = self.stage.version
                 if self.rank > 0:
-                    out_msg = (g_in.contiguous(), self.rank - 1)
+                    out_msg = (g_in.contiguous(), self.stage_ranks[self.rank - 1])
             snapshot_peak = max(snapshot_peak, self.policy.snapshot_count(self.rt))
             wi += 1
             # one grouped exchange: this op's output + the next work op's input
@@ -207,7 +215,17 @@ class PipelineStageRunner:
         return StageReport(self.rank, order, host_losses, self.stage.version, self.stage.stash.peak,
                            snapshot_peak, time.perf_counter() - t0, executed)
 
+    def _shard(self, t):
+        if self.dp_size == 1:
+            return t
+        return t[self.dp_rank * self.rows : (self.dp_rank + 1) * self.rows]
+
     def _update(self, op):
+        if self.dp_size > 1:
+            # hybrid DP x PP: mean gradient over the data-parallel replicas of
+            # this stage, then the (fused) update on identical replicas
+            self.dist.all_reduce(self.stage.flat.grad, group=self.dp_group)
+            self.stage.flat.grad.mul_(1.0 / self.dp_size)
         lr = self.lr_for_mb(op.mb)
         try:
             if self.fuse and op.fuse_predict:

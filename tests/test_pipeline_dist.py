@@ -147,3 +147,51 @@ def test_gloo_pipeline_matches_oracle(tmp_path, world, strategy, kind):
         params = json.loads((tmp_path / f"params{k}.json").read_text())
         for name, want in zip(ref["names"][k], ref["params"][k]):
             assert optim_ref.inf_norm_rel(np.array(params[name]), want) <= 1e-4
+
+
+def _hybrid_worker(rank, world, port, dp, pp, n, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.pipeline import PipelineStageRunner, gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+        from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+        r, k = divmod(rank, pp)
+        groups = [dist.new_group([q * pp + s for q in range(dp)]) for s in range(pp)]
+        layers = build_layers(DIMS, ACTS)
+        stage = StageModel(k, partition_layers(layers, pp)[k],
+                           lambda sp: rng_ref.layer_init(5, sp.index, sp.in_dim, sp.out_dim), "cpu")
+        opt = StandInOptimizer("adam", stage.param_names)
+        tl = build_timeline("optimizer_prediction", pp, n)
+        runner = PipelineStageRunner(dist, tl, stage, opt, "optimizer_prediction", Src(), "mse", lambda mb: 0.01,
+                                     8 // dp, stage_ranks=[r * pp + s for s in range(pp)], dp_group=groups[k],
+                                     dp_rank=r, dp_size=dp)
+        rep = runner.run()
+        reps = gather_reports(dist, rep, world)
+        if rank == 0:
+            last = [rp for rp in reps if rp.rank == pp - 1]
+            losses = np.mean([rp.losses for rp in last], axis=0).tolist()
+            Path(out_dir, "out.json").write_text(json.dumps({"losses": losses}))
+        params = {n_: p.detach().double().numpy().tolist() for n_, p in zip(stage.param_names, stage.params)}
+        Path(out_dir, f"params{rank}.json").write_text(json.dumps(params))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_hybrid_dp_pp_equals_full_batch_pipeline(tmp_path):
+    """DP=2 x PP=2 on 4 gloo ranks (each replica half of every batch, stage
+    gradients averaged before the fused update) == the 2-stage pipeline on the
+    full batch (oracle), and the two replicas stay identical."""
+    dp, pp, n = 2, 2, 10
+    mp.spawn(_hybrid_worker, args=(dp * pp, free_port(), dp, pp, n, str(tmp_path)), nprocs=dp * pp, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    ref = runtime_ref.run(DIMS, ACTS, pp, n, "optimizer_prediction", optim_ref.Hyper("adam", weight_decay=0.0),
+                          Src().batch, "mse", lambda mb: 0.01, lambda i, a, b: rng_ref.layer_init(5, i, a, b))
+    assert np.allclose(got["losses"], ref["losses"], rtol=1e-4, atol=1e-6)
+    for k in range(pp):
+        p0 = json.loads((tmp_path / f"params{k}.json").read_text())
+        p1 = json.loads((tmp_path / f"params{pp + k}.json").read_text())
+        for name, want in zip(ref["names"][k], ref["params"][k]):
+            assert p0[name] == p1[name]  # replicas identical
+            assert optim_ref.inf_norm_rel(np.array(p0[name]), want) <= 1e-4
