@@ -71,6 +71,65 @@ def _graphed(torch, device, strategy, depth, n_batches, data, replays, seed=0, d
     return rep, e0.elapsed_time(e1) / 1e3 / replays, g.launches
 
 
+def stage_unit_times(torch, device, stages, opts, data, loss_kind, predictive: bool, reps: int = 20):
+    """Per-stage device time of one mini-batch's work — forward (+ loss on the
+    last stage) + backward + update (K3 when predictive and not last, else
+    K2) — each captured in a CUDA graph and replayed `reps` times on
+    THROWAWAY stages (it trains them). SURVEY.md §8d's t_f,k + t_b,k (+ t_u,k)."""
+    from .stages import loss_and_grad
+
+    times = []
+    for k, (st, opt) in enumerate(zip(stages, opts)):
+        last = k == len(stages) - 1
+        x0, y0 = data.batch(1)
+        x = x0 if k == 0 else torch.randn((x0.shape[0], *st.in_shape), device=device)
+        g_last = None if last else torch.randn((x0.shape[0], *st.out_shape), device=device)
+        staging = st.flat.layout.empty(device)
+        opt._ensure_state()
+
+        def unit():
+            out = st.run_forward(st.params, (0, 0), x, 1, check_finite=False)
+            g = loss_and_grad(out, y0, loss_kind)[1] if last else g_last
+            st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0)
+            if predictive and not last:
+                opt.step_predict_(st.flat, 1e-4, 1e-4, len(stages) - k - 1, staging)
+            else:
+                opt.step_(st.flat, 1e-4)
+
+        opt.eager_checks = False
+        for _ in range(2):
+            unit()
+        torch.cuda.synchronize(device)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            unit()
+        graph.replay()
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize(device)
+        times.append(e0.elapsed_time(e1) / 1e3 / reps)
+    return times
+
+
+def pipeline_roofline(stage_times, batch, n, depth, boundary_bytes, link_gbs=770.0):
+    """SURVEY.md §8d pipeline roofline: min(compute, link) samples/s.
+    compute = B / max_k t_k * n / (n + D - 1) (1F1B unit makespan 2n+2D-2);
+    link = B / (max boundary bytes / per-direction NVLink bandwidth) — the
+    activation and the gradient of a boundary move in opposite directions.
+    Single GPU (all stages serialised): B / sum_k t_k."""
+    one_gpu = batch / sum(stage_times)
+    compute = batch / max(stage_times) * n / (n + depth - 1)
+    link = batch / (max(boundary_bytes) / (link_gbs * 1e9)) if boundary_bytes else float("inf")
+    return {"single_gpu_samples_per_s": round(one_gpu, 1), "compute_samples_per_s": round(compute, 1),
+            "link_samples_per_s": round(link, 1) if link != float("inf") else None,
+            "multi_gpu_samples_per_s": round(min(compute, link), 1), "link_gbs": link_gbs,
+            "stage_ms": [round(t * 1e3, 4) for t in stage_times]}
+
+
 def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, replays: int = 5):
     """All `depth` stages on one GPU, events in timeline order (the single-GPU
     1F1B runner). Each measured unit is one full run of the 1F1B timeline
@@ -92,6 +151,17 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
                     "eager_samples_per_s": round(n_batches * BATCH / esec, 1), "final_loss": rep.losses[-1],
                     "optimizer_launches_per_run": n_launch}
         launches += n_launch * replays
+    from .optim import OptimizerConfig, OptimizerState
+    from .stages import build_layers, build_stages, torch_init
+
+    for strategy, key in (("async_raw", "pred_off"), ("optimizer_prediction", "pred_on")):
+        stages = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), depth, torch_init(7, device), device=device)
+        opts = [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in stages]
+        t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction")
+        bounds = [4 * BATCH * s_.out_dim for s_ in stages[:-1]]
+        roof = pipeline_roofline(t, BATCH, n_batches, depth, bounds)
+        out[key]["roofline"] = roof
+        out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] / roof["single_gpu_samples_per_s"], 4)
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out["value"] = on
     out["unit"] = "samples/s"

@@ -195,3 +195,54 @@ def test_hybrid_dp_pp_equals_full_batch_pipeline(tmp_path):
         for name, want in zip(ref["names"][k], ref["params"][k]):
             assert p0[name] == p1[name]  # replicas identical
             assert optim_ref.inf_norm_rel(np.array(p0[name]), want) <= 1e-4
+
+
+def _conv_worker(rank, world, port, n, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch.nn as nn
+
+        from paper_2312_00839_b200.pipeline import PipelineStageRunner, gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+        from paper_2312_00839_b200.stage_models import LiveLinear, build_module_stages
+
+        torch.manual_seed(0)
+        blocks = [nn.Sequential(nn.Conv2d(3, 8, 3, padding=1), nn.ReLU()),
+                  nn.Sequential(nn.Conv2d(8, 8, 3, padding=1), nn.ReLU(), nn.MaxPool2d(2)),
+                  nn.Sequential(nn.Flatten(), LiveLinear(8 * 4 * 4, 5))]
+        stages = build_module_stages(blocks, world, "cpu", (3, 8, 8))
+        stage = stages[rank]
+        opt = StandInOptimizer("sgdm", stage.param_names)
+
+        class ImgSrc:
+            def batch(self, mb):
+                g = torch.Generator().manual_seed(mb)
+                return torch.randn(4, 3, 8, 8, generator=g), torch.nn.functional.one_hot(
+                    torch.randint(0, 5, (4,), generator=g), 5).float()
+
+        tl = build_timeline("optimizer_prediction", world, n)
+        runner = PipelineStageRunner(dist, tl, stage, opt, "optimizer_prediction", ImgSrc(), "softmax_xent",
+                                     lambda mb: 0.05, 4)
+        rep = runner.run()
+        reps = gather_reports(dist, rep, world)
+        if rank == 0:
+            Path(out_dir, "out.json").write_text(json.dumps({
+                "records": sorted([[r.mb, r.stage, r.forward_version, r.predicted, r.prediction_target,
+                                    r.backward_version, r.live_backward_version] for rp in reps for r in rp.records]),
+                "losses": reps[-1].losses}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_module_stages_pipeline(tmp_path):
+    """Conv module stages (4-D activations over P2P) through the distributed runner."""
+    world, n = 3, 8
+    mp.spawn(_conv_worker, args=(world, free_port(), n, str(tmp_path)), nprocs=world, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    ref = runtime_ref.run([3] * (world + 1), ["tanh"] * world, world, n, "optimizer_prediction",
+                          optim_ref.Hyper("sgdm"), lambda mb: (np.ones((2, 3)), np.ones((2, 3))), "mse",
+                          lambda mb: 1e-3, lambda i, a, b: rng_ref.layer_init(0, i, a, b))
+    want = sorted([[r[0], r[2], r[3], r[4], r[5], r[6], r[7]] for r in ref["records"]])
+    assert got["records"] == want
+    assert len(got["losses"]) == n and all(np.isfinite(got["losses"]))
