@@ -153,6 +153,25 @@ int po_step_predict_dc(const po_hparams* hp, float* w, const float* g, float* st
                        float* w_hat, int64_t n, const po_coef* coef_dev, int64_t* nonfinite_index,
                        const po_launch* launch, void* stream);
 
+/* ---- fused per-event stage ops (pipeoptim_stage_ops.cu) ---------------- */
+
+#define PO_LOSS_MSE 0
+#define PO_LOSS_SOFTMAX_XENT 1
+
+/* flags[index] = 0 if any of x[0..n) is NaN or +-Inf (flags pre-set to 1 by
+ * the caller): the deferred form of the forward-output finiteness check
+ * (stages.py:182). One launch, no host sync. */
+int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void* stream);
+
+/* Loss and its gradient w.r.t. pred in one launch (linalg.py:212-241):
+ * softmax_xent (mean row cross-entropy, grad (softmax - target)/rows) or mse
+ * (mean of squares, grad 2 (pred - target)/numel). pred/target/grad are
+ * row-major [rows x cols]; *loss (device) receives the scalar. `scratch` is
+ * a device buffer of rows floats + one uint32 counter that must be zero
+ * before the first launch (the kernel re-arms it). */
+int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t rows, int64_t cols, float* grad,
+                 float* loss, float* scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,11 @@ EXPORTS = (
     "po_step_dc",
     "po_predict_dc",
     "po_step_predict_dc",
+    "po_all_finite",
+    "po_loss_grad",
 )
+
+PO_LOSS_MSE, PO_LOSS_SOFTMAX_XENT = 0, 1
 
 PO_COEF_STEP, PO_COEF_PREDICT, PO_COEF_STEP_PREDICT = 0, 1, 2
 
@@ -91,6 +95,8 @@ _SIGNATURES = {
     "po_step_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _I64, _P, _P, _LA, _P]),
     "po_predict_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _I64, _P, _LA, _P]),
     "po_step_predict_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _P, _I64, _P, _P, _LA, _P]),
+    "po_all_finite": (ctypes.c_int, [_P, _I64, _P, _I64, _P]),
+    "po_loss_grad": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, _I64, _P, _P, _P, _P]),
 }
 
 _lock = threading.Lock()

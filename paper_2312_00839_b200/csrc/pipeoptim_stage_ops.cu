@@ -1,0 +1,161 @@
+// pipeoptim_stage_ops.cu — fused per-event stage ops for the 1F1B runners.
+//
+// The runners' small per-event ops were each several torch launches
+// (profiles/r1_pipeline_breakdown.md): a finiteness check of a forward output
+// (isfinite -> abs/compare/and -> all-reduce -> index copy: 5 launches) and
+// the last stage's loss + gradient (~10 launches). Here each is ONE launch:
+//
+//   po_all_finite   flags[index] = 0 if any x is NaN/Inf (flags pre-set to 1).
+//                   Replaces stages.py:182's require_finite in deferred mode.
+//   po_loss_grad    softmax cross-entropy or MSE loss AND its gradient
+//                   (linalg.py:212-241), the loss reduced in a fixed order by
+//                   the last CTA to finish (deterministic, no float atomics).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "pipeoptim.h"
+
+namespace {
+
+__global__ void all_finite_kernel(const float* __restrict__ x, int64_t n, uint8_t* flags, int64_t index) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n4 = (reinterpret_cast<uintptr_t>(x) % 16 == 0) ? n / 4 : 0;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int64_t j = i; j < n4; j += stride) {
+    float4 v = x4[j];
+    bad |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+  }
+  for (int64_t j = n4 * 4 + i; j < n; j += stride) bad |= !isfinite(x[j]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags[index] = 0;
+}
+
+constexpr int kLossThreads = 256;
+
+__device__ __forceinline__ float block_reduce_max(float v, float* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  v = (threadIdx.x < blockDim.x / 32) ? sh[threadIdx.x] : -INFINITY;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (threadIdx.x == 0) sh[32] = v;
+  __syncthreads();
+  return sh[32];
+}
+
+__device__ __forceinline__ float block_reduce_sum(float v, float* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  v = (threadIdx.x < blockDim.x / 32) ? sh[threadIdx.x] : 0.f;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (threadIdx.x == 0) sh[32] = v;
+  __syncthreads();
+  return sh[32];
+}
+
+// One CTA per row. softmax_xent: z = x - max; e = exp(z); sm = e / sum(e);
+// row loss = -log(sum(sm * y)); grad = (sm - y) / rows. mse: row partial
+// sum of (x - y)^2; grad = 2 (x - y) / numel. The last CTA reduces the row
+// partials in row order into *loss.
+__global__ void loss_grad_kernel(const float* __restrict__ pred, const float* __restrict__ target, int64_t rows,
+                                 int64_t cols, int kind, float* __restrict__ grad, float* __restrict__ row_part,
+                                 unsigned int* counter, float* loss) {
+  __shared__ float sh[33];
+  __shared__ bool last;
+  const int64_t r = blockIdx.x;
+  const float* x = pred + r * cols;
+  const float* y = target + r * cols;
+  float* g = grad + r * cols;
+  float part;
+  if (kind == 1) {  // softmax cross-entropy (linalg.py:228-235)
+    float m = -INFINITY;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) m = fmaxf(m, x[c]);
+    m = block_reduce_max(m, sh);
+    float s = 0.f;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) s += expf(x[c] - m);
+    s = block_reduce_sum(s, sh);
+    float picked = 0.f;
+    const float inv_rows = 1.0f / (float)rows;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float sm = expf(x[c] - m) / s;
+      picked += sm * y[c];
+      g[c] = (sm - y[c]) * inv_rows;
+    }
+    picked = block_reduce_sum(picked, sh);
+    part = -logf(picked);
+  } else {  // mse (linalg.py:223-227)
+    const float scale = 2.0f / (float)(rows * cols);
+    float acc = 0.f;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float d = x[c] - y[c];
+      acc += d * d;
+      g[c] = d * scale;
+    }
+    part = block_reduce_sum(acc, sh);
+  }
+  if (threadIdx.x == 0) {
+    row_part[r] = part;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == (unsigned int)(rows - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    // fixed-order reduction of the row partials by the last CTA
+    float acc = 0.f;
+    for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) acc += ((volatile float*)row_part)[i];
+    acc = block_reduce_sum(acc, sh);
+    if (threadIdx.x == 0) {
+      *loss = (kind == 1) ? acc / (float)rows : acc / (float)(rows * cols);
+      *counter = 0u;  // re-armed for the next launch (graph replays)
+    }
+  }
+}
+
+int sm_count_ops() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+}  // namespace
+
+extern "C" {
+
+int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void* stream) {
+  if (n < 0 || flags == nullptr || index < 0 || (n > 0 && x == nullptr)) return PO_EINVAL;
+  if (n == 0) return 0;
+  static int sms = 0;
+  if (sms == 0) sms = sm_count_ops();
+  const int block = 256;
+  int64_t want = (n / 4 + block - 1) / block;
+  int64_t grid = want < 1 ? 1 : (want > 4 * sms ? 4 * sms : want);
+  all_finite_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(x, n, flags, index);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t rows, int64_t cols, float* grad,
+                 float* loss, float* scratch, void* stream) {
+  if ((kind != PO_LOSS_MSE && kind != PO_LOSS_SOFTMAX_XENT) || rows < 1 || cols < 1) return PO_EINVAL;
+  if (pred == nullptr || target == nullptr || grad == nullptr || loss == nullptr || scratch == nullptr)
+    return PO_EINVAL;
+  if (rows > 0x7fffffff) return PO_EINVAL;
+  // scratch layout: [rows] float row partials, then one uint32 counter (caller zeroes it once)
+  unsigned int* counter = reinterpret_cast<unsigned int*>(scratch + rows);
+  loss_grad_kernel<<<(unsigned)rows, kLossThreads, 0, (cudaStream_t)stream>>>(pred, target, rows, cols, kind, grad,
+                                                                             scratch, counter, loss);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+}  // extern "C"

@@ -29,7 +29,7 @@ import torch.nn.functional as F
 
 from .errors import NumericError
 from .optim import FlatParams
-from .stages import ActivationStash, StashEntry
+from .stages import ActivationStash, StashEntry, record_finite
 
 
 class _LiveLinearFn(torch.autograd.Function):
@@ -233,7 +233,7 @@ class ModuleStage:
             if not bool(torch.isfinite(out).all()):
                 raise NumericError(f"non-finite value in stage {self.rank} forward output")
         elif finite_flags is not None:
-            finite_flags[flag_index] = torch.isfinite(out).all()
+            record_finite(out, finite_flags, flag_index)
         self.stash.put(key, StashEntry(version, [x_in], [out]))
         return out.detach()
 

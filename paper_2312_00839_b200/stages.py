@@ -205,7 +205,7 @@ def _activation_grad_mul(g: torch.Tensor, pre: torch.Tensor, kind: str) -> torch
         t = torch.tanh(pre)
         return g * (1.0 - t * t)
     if kind == "relu":
-        return g * (pre > 0.0).to(g.dtype)
+        return g * (pre > 0.0)  # one multiply with the mask promoted in-kernel
     return g
 
 
@@ -236,9 +236,23 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
                 f"non-finite value in stage {stage.rank} forward output at entry ({bad[0]}, {bad[1]})"
             )
     elif finite_flags is not None:
-        finite_flags[flag_index] = torch.isfinite(h).all()
+        record_finite(h, finite_flags, flag_index)
     stage.stash.put(key, StashEntry(version, inputs, pres))
     return h
+
+
+def record_finite(t: torch.Tensor, flags: torch.Tensor, index: int) -> None:
+    """flags[index] = all(isfinite(t)) without a host sync: one po_all_finite
+    launch on CUDA (flags must be pre-set to True)."""
+    if t.is_cuda:
+        from . import _lib
+
+        tc = t if t.is_contiguous() else t.contiguous()
+        rc = _lib.load().po_all_finite(tc.data_ptr(), tc.numel(), flags.data_ptr(), index,
+                                       torch.cuda.current_stream(t.device).cuda_stream)
+        _lib.check(rc, "po_all_finite")
+    else:
+        flags[index] = torch.isfinite(t).all()
 
 
 def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
@@ -292,15 +306,40 @@ def params_by_layer(stages: list[StageModel]) -> dict[int, tuple[torch.Tensor, t
 LOSS_KINDS = ("mse", "softmax_xent")
 
 
+_LOSS_SCRATCH: dict = {}
+
+
 def loss_and_grad(pred: torch.Tensor, target: torch.Tensor, kind: str):
     """(loss as a 0-d device tensor, grad wrt pred).
 
     mse: mean over all entries of (pred - target)^2, grad 2*(pred - target)/numel.
     softmax_xent: logits vs one-hot target, row-max-shifted softmax, mean row
     cross-entropy, grad (softmax - target)/rows.
+    On CUDA this is ONE fused launch (po_loss_grad); on CPU (the gloo tests
+    of the distributed runner) plain torch ops.
     """
     if pred.shape != target.shape:
         raise DimensionError(f"loss_and_grad: shapes differ: {tuple(pred.shape)} vs {tuple(target.shape)}")
+    if kind not in LOSS_KINDS:
+        raise ValueError(f"unknown loss kind: {kind!r}")
+    if pred.is_cuda and pred.dim() == 2:
+        from . import _lib
+
+        rows, cols = pred.shape
+        p = pred if pred.is_contiguous() else pred.contiguous()
+        t = target.to(torch.float32)
+        t = t if t.is_contiguous() else t.contiguous()
+        key = (pred.device, rows)
+        if key not in _LOSS_SCRATCH:
+            _LOSS_SCRATCH[key] = torch.zeros(rows + 1, dtype=torch.float32, device=pred.device)
+        grad = torch.empty_like(p)
+        loss = torch.empty((), dtype=torch.float32, device=pred.device)
+        code = _lib.PO_LOSS_MSE if kind == "mse" else _lib.PO_LOSS_SOFTMAX_XENT
+        rc = _lib.load().po_loss_grad(code, p.data_ptr(), t.data_ptr(), rows, cols, grad.data_ptr(),
+                                      loss.data_ptr(), _LOSS_SCRATCH[key].data_ptr(),
+                                      torch.cuda.current_stream(pred.device).cuda_stream)
+        _lib.check(rc, "po_loss_grad")
+        return loss, grad
     if kind == "mse":
         diff = pred - target
         n = diff.numel()

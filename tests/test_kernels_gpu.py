@@ -297,3 +297,42 @@ def test_direction_and_axpy(lib):
                                        None, stream()) == 0
             (pw,) = R.predict_weights([w.astype(np.float64)], 1e-3, 3, [host(out)])
             assert R.inf_norm_rel(host(wh), pw) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 5, 4096, 1_000_003])
+@pytest.mark.parametrize("offset", [0, 1])
+def test_all_finite(lib, n, offset):
+    import torch
+
+    x = dev(np.random.default_rng(n).normal(size=n).astype(np.float32), offset)
+    flags = torch.ones(4, dtype=torch.bool, device="cuda")
+    assert lib.po_all_finite(x.data_ptr(), n, flags.data_ptr(), 1, stream()) == 0
+    assert flags.tolist() == [True] * 4
+    for bad in (np.inf, -np.inf, np.nan):
+        y = x.clone()
+        y[n // 2] = float(bad)
+        flags.fill_(True)
+        assert lib.po_all_finite(y.data_ptr(), n, flags.data_ptr(), 2, stream()) == 0
+        assert flags.tolist() == [True, True, False, True]
+
+
+@pytest.mark.parametrize("kind,rows,cols", [("softmax_xent", 128, 10), ("softmax_xent", 64, 32000),
+                                            ("softmax_xent", 3, 1), ("mse", 8, 3), ("mse", 128, 1000)])
+def test_fused_loss_grad_matches_reference_formulas(kind, rows, cols):
+    """po_loss_grad vs linalg.py:212-241 in float64 on the same fp32 inputs."""
+    import torch
+
+    from oracle import runtime_ref
+    from paper_2312_00839_b200.stages import loss_and_grad
+
+    rng = np.random.default_rng(rows * cols)
+    pred = (rng.normal(size=(rows, cols)) * 20).astype(np.float32)
+    if kind == "mse":
+        tgt = rng.normal(size=(rows, cols)).astype(np.float32)
+    else:
+        tgt = np.eye(cols, dtype=np.float32)[rng.integers(0, cols, rows)]
+    for _ in range(2):  # the second launch exercises the re-armed counter
+        loss, grad = loss_and_grad(torch.from_numpy(pred).cuda(), torch.from_numpy(tgt).cuda(), kind)
+        want_loss, want_grad = runtime_ref.loss_and_grad(pred.astype(np.float64), tgt.astype(np.float64), kind)
+        assert abs(float(loss) - want_loss) <= 1e-5 * abs(want_loss) + 1e-7
+        assert R.inf_norm_rel(host(grad), want_grad) <= 2e-6
