@@ -85,6 +85,7 @@ def stage_unit_times(torch, device, stages, opts, data, loss_kind, predictive: b
         x = x0 if k == 0 else torch.randn((x0.shape[0], *st.in_shape), device=device)
         g_last = None if last else torch.randn((x0.shape[0], *st.out_shape), device=device)
         staging = st.flat.layout.empty(device)
+        opt._bind(st.flat.layout)
         opt._ensure_state()
 
         def unit():
