@@ -49,24 +49,51 @@ class StageReport:
     executed: list
 
 
-class _Exchange:
-    """Grouped neighbour P2P for one rank."""
+class _StagedRecv:
+    """Completion handle of a host-staged receive: wait(), then copy to device."""
 
-    def __init__(self, dist, group=None):
+    def __init__(self, reqs, host, dev):
+        self.reqs, self.host, self.dev = reqs, host, dev
+
+    def wait(self):
+        for r in self.reqs:
+            r.wait()
+        self.dev.copy_(self.host)
+
+    def is_completed(self):
+        return all(r.is_completed() for r in self.reqs)
+
+
+class _Exchange:
+    """Grouped neighbour P2P for one rank.
+
+    host_staging=True moves device tensors through host memory (for a
+    backend without device transport, e.g. gloo with several ranks on one
+    GPU in the tests); with NCCL the device buffers go over NVLink directly.
+    """
+
+    def __init__(self, dist, group=None, host_staging: bool = False):
         self.dist = dist
         self.group = group
+        self.host_staging = host_staging
         self.inflight: list = []  # (request, tensor) kept alive until complete
 
     def post(self, sends, recvs):
         """sends: [(tensor, peer)], recvs: [(buffer, peer)] -> requests for recvs."""
         d = self.dist
         self.inflight = [(rq, ts) for rq, ts in self.inflight if not all(r.is_completed() for r in rq)]
+        if self.host_staging:
+            sends = [(t.cpu(), peer) for t, peer in sends]
+            staged = [(torch.empty(b.shape, dtype=b.dtype), b, peer) for b, peer in recvs]
+            recvs = [(h, peer) for h, _, peer in staged]
         ops = [d.P2POp(d.isend, t, peer, self.group) for t, peer in sends]
         ops += [d.P2POp(d.irecv, b, peer, self.group) for b, peer in recvs]
         if not ops:
             return []
         reqs = d.batch_isend_irecv(ops)
         self.inflight.append((reqs, [t for t, _ in sends]))
+        if self.host_staging and staged:
+            return [_StagedRecv(reqs, staged[0][0], staged[0][1])]
         return reqs
 
     def drain(self):
@@ -81,7 +108,8 @@ class PipelineStageRunner:
 
     def __init__(self, dist, tl: Timeline, stage: StageModel, opt, strategy: str, data, loss_kind: str,
                  lr_for_mb, rows: int, *, checks: str = "deferred", fuse: bool = True, group=None,
-                 stage_ranks: list[int] | None = None, dp_group=None, dp_rank: int = 0, dp_size: int = 1):
+                 stage_ranks: list[int] | None = None, dp_group=None, dp_rank: int = 0, dp_size: int = 1,
+                 host_staging: bool = False):
         """stage_ranks[k] is the global rank holding stage k of this pipeline
         replica (default: rank k). With dp_size > 1 (hybrid DP x PP), replica
         `dp_rank` trains on rows [dp_rank*rows, (dp_rank+1)*rows) of every
@@ -109,7 +137,7 @@ class PipelineStageRunner:
         self.policy = _make_policy(strategy, tl)
         self.rt = _StageRt(stage, opt, self.depth)
         self.program = stage_program(tl, self.rank, predictive=self.predictive)
-        self.comm = _Exchange(dist, group)
+        self.comm = _Exchange(dist, group, host_staging=host_staging)
         self.device = stage.flat.device
         self.stage_ranks = stage_ranks or list(range(self.depth))
         self.dp_group, self.dp_rank, self.dp_size = dp_group, dp_rank, dp_size
