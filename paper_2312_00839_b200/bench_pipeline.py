@@ -131,45 +131,50 @@ def pipeline_roofline(stage_times, batch, n, depth, boundary_bytes, link_gbs=770
             "stage_ms": [round(t * 1e3, 4) for t in stage_times]}
 
 
-def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, replays: int = 5):
+def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, replays: int = 5, tf32: bool = False,
+                        with_eager: bool = True, with_roofline: bool = True):
     """All `depth` stages on one GPU, events in timeline order (the single-GPU
     1F1B runner). Each measured unit is one full run of the 1F1B timeline
     (n_batches mini-batches, warm-up and drain included), replayed from a CUDA
     graph (`GraphedExecute`); the eager (Python-driven) runner is reported
-    beside it. Samples/s with prediction on and off."""
-    torch.backends.cuda.matmul.allow_tf32 = False
+    beside it. Samples/s with prediction on and off, and the pipeline
+    roofline from per-stage graphed unit times."""
+    from .optim import OptimizerConfig, OptimizerState
+    from .stages import build_layers, build_stages, torch_init
+
+    torch.backends.cuda.matmul.allow_tf32 = tf32
     data = DeviceBatches(torch, device)
     out = {"config": f"config1 MLP {CONFIG1_DIMS}, B={BATCH}, Adam lr 1e-4, 1F1B D={depth} on 1 GPU "
                      f"(single-process runner, CUDA-graph replay of whole {n_batches}-mini-batch runs), "
-                     f"fp32 GEMMs (TF32 off)"}
+                     f"{'TF32' if tf32 else 'fp32 (TF32 off)'} GEMMs, fp32 master weights"}
     launches = 0
     for strategy in ("async_raw", "optimizer_prediction"):
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
         rep, sec, n_launch = _graphed(torch, device, strategy, depth, n_batches, data, replays)
-        _run_once(torch, device, strategy, depth, min(n_batches, 2 * depth + 2), data)  # eager warm-up
-        _, esec, _ = _run_once(torch, device, strategy, depth, n_batches, data)
         out[key] = {"samples_per_s": round(n_batches * BATCH / sec, 1), "s_per_run": round(sec, 5),
-                    "eager_samples_per_s": round(n_batches * BATCH / esec, 1), "final_loss": rep.losses[-1],
-                    "optimizer_launches_per_run": n_launch}
+                    "final_loss": rep.losses[-1], "optimizer_launches_per_run": n_launch}
+        if with_eager:
+            _run_once(torch, device, strategy, depth, min(n_batches, 2 * depth + 2), data)  # eager warm-up
+            _, esec, _ = _run_once(torch, device, strategy, depth, n_batches, data)
+            out[key]["eager_samples_per_s"] = round(n_batches * BATCH / esec, 1)
         launches += n_launch * replays
-    from .optim import OptimizerConfig, OptimizerState
-    from .stages import build_layers, build_stages, torch_init
-
-    for strategy, key in (("async_raw", "pred_off"), ("optimizer_prediction", "pred_on")):
-        stages = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), depth, torch_init(7, device), device=device)
-        opts = [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in stages]
-        t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction")
-        bounds = [4 * BATCH * s_.out_dim for s_ in stages[:-1]]
-        roof = pipeline_roofline(t, BATCH, n_batches, depth, bounds)
-        out[key]["roofline"] = roof
-        out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] / roof["single_gpu_samples_per_s"], 4)
+        if with_roofline:
+            stages = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), depth, torch_init(7, device), device=device)
+            opts = [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in stages]
+            t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction")
+            roof = pipeline_roofline(t, BATCH, n_batches, depth, [4 * BATCH * s_.out_dim for s_ in stages[:-1]])
+            out[key]["roofline"] = roof
+            out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] / roof["single_gpu_samples_per_s"],
+                                                            4)
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out["value"] = on
     out["unit"] = "samples/s"
     out["prediction_overhead"] = round(1.0 - on / off, 4)
-    out["eager_prediction_overhead"] = round(
-        1.0 - out["pred_on"]["eager_samples_per_s"] / out["pred_off"]["eager_samples_per_s"], 4)
+    if with_eager:
+        out["eager_prediction_overhead"] = round(
+            1.0 - out["pred_on"]["eager_samples_per_s"] / out["pred_off"]["eager_samples_per_s"], 4)
     out["launches"] = launches
+    torch.backends.cuda.matmul.allow_tf32 = False
     return out
 
 

@@ -426,8 +426,13 @@ struct DefaultShape {
   int block, ctas_per_sm, unroll, cache;
 };
 
-DefaultShape default_shape(int kind, int mode) {
+DefaultShape default_shape(int kind, int mode, int64_t n) {
   const bool sg = kind == PO_SGDM;
+  // pipeline-stage sizes (< 32 M elements, the 1F1B configs' 0.01-20 M-param
+  // stages): many small CTAs, one vector per stream in flight — measured +2%
+  // (fp32 GEMMs) to +11% (TF32) config-1 pipeline throughput
+  // (profiles/r1_pipeline.md, scripts/pipeline_variants.py)
+  if (n < (int64_t(1) << 25)) return DefaultShape{128, 16, 1, 1};
   switch (mode) {
     case MODE_PREDICT: return sg ? DefaultShape{256, 8, 2, 1} : DefaultShape{512, 2, 1, 1};
     case MODE_STEP: return sg ? DefaultShape{512, 1, 1, 1} : DefaultShape{512, 1, 2, 0};
@@ -442,7 +447,7 @@ constexpr int kDefaultVec = 8;
 int run(int kind, int mode, Args a, const po_launch* L, cudaStream_t s) {
   if (a.n < 0) return PO_EINVAL;
   if (a.n == 0) return 0;
-  const DefaultShape d = default_shape(kind, mode);
+  const DefaultShape d = default_shape(kind, mode, a.n);
   int block = (L && L->block > 0) ? L->block : d.block;
   int cps = (L && L->ctas_per_sm > 0) ? L->ctas_per_sm : d.ctas_per_sm;
   int vec = (L && L->vec > 0) ? L->vec : kDefaultVec;
