@@ -318,6 +318,7 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         t = bp.single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches, tf32=True, with_eager=False,
                                    with_roofline=False)
         out["tf32"] = {k: t[k] for k in ("pred_on", "pred_off", "prediction_overhead", "config")}
+        out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
     else:
         out = bp.multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches)
     if not args.no_configs:

@@ -204,6 +204,33 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
     return out
 
 
+def projected_multi_gpu(torch, device, depth: int = 8, n_batches: int = 64, tf32: bool = False):
+    """The north-star setting (one stage per GPU, D = 8) projected from
+    per-stage graphed unit times measured on this GPU: config 1 widened to
+    8 layers (one more 1024-wide ReLU layer per extra stage, as bench.py
+    --gpus 8 runs it). Pipeline throughput = the slowest stage's unit time
+    with the 1F1B fill/drain factor n/(n+D-1); the NVLink term (0.5 MB
+    activation per boundary at 770 GB/s) is ~1000x faster and not binding."""
+    from .optim import OptimizerConfig, OptimizerState
+    from .stages import build_layers, build_stages, torch_init
+
+    torch.backends.cuda.matmul.allow_tf32 = tf32
+    dims = [3072] + [1024] * (depth - 1) + [10]
+    acts = ["relu"] * (depth - 1) + ["linear"]
+    data = DeviceBatches(torch, device, dims=dims)
+    out = {"config": f"MLP {dims}, B={BATCH}, Adam, D={depth} (one stage per GPU), "
+                     f"{'TF32' if tf32 else 'fp32'} GEMMs; projected from per-stage graphed unit times"}
+    for strategy, key in (("async_raw", "pred_off"), ("optimizer_prediction", "pred_on")):
+        stages = build_stages(build_layers(dims, acts), depth, torch_init(11, device), device=device)
+        opts = [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in stages]
+        t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction")
+        out[key] = pipeline_roofline(t, BATCH, n_batches, depth, [4 * BATCH * s_.out_dim for s_ in stages[:-1]])
+    out["prediction_overhead"] = round(
+        1.0 - out["pred_on"]["multi_gpu_samples_per_s"] / out["pred_off"]["multi_gpu_samples_per_s"], 4)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return out
+
+
 MODULE_CONFIGS = {
     # BASELINE configs[1..3] (SURVEY.md §8d pipeline synthetic inputs)
     "config2_vgg16": dict(blocks="vgg16", in_shape=(3, 32, 32), classes=100, batch=128, depth=4, opt="sgdm", lr=0.01),
