@@ -292,6 +292,28 @@ def e2e_leg(args, torch, dist, world, device):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     opt.check_finite()
+    # device-resident weights/state, gradient from pinned host memory, the
+    # non-finite flag read back (the training-loop setting)
+    wd = torch.empty(n, device=device).normal_(0, 0.02)
+    whd = torch.empty(n, device=device)
+    opt2 = OptimizerState(OptimizerConfig(kind), ["stage.flat"], device=device, eager_checks=False)
+    streamer.step_predict_resident(opt2, wd, g_h, 1e-3, 1e-3, 3, whd)
+    torch.cuda.synchronize(device)
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record()
+    res_launches = 0
+    for _ in range(args.e2e_steps):
+        res_launches += streamer.step_predict_resident(opt2, wd, g_h, 1e-3, 1e-3, 3, whd)
+        bad = int(opt2._bad.item())  # the step's result read back every step
+        assert bad == (1 << 63) - 1
+    r1.record()
+    torch.cuda.synchronize(device)
+    ms_res = r0.elapsed_time(r1) / args.e2e_steps
+    if world > 1:
+        tt = torch.tensor([ms_res], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_res = float(tt.item())
+    del wd, whd, opt2
     res = {
         "value": round(world * BYTES_PER_PARAM[kind] * n / (ms * 1e-3) / 1e9, 2),
         "unit": "GB/s",
@@ -302,6 +324,16 @@ def e2e_leg(args, torch, dist, world, device):
         "path": "OptimizerState + HostStreamer.step_predict: pinned host W,G -> device (chunked, 3 streams) -> "
                 "K3 against device-resident m,v -> W', W_hat -> host",
         "launches": launches[0],
+        "resident_params": {
+            "value": round(world * BYTES_PER_PARAM[kind] * n / (ms_res * 1e-3) / 1e9, 2),
+            "unit": "GB/s",
+            "h2d_bytes_per_step": 4 * n,
+            "d2h_bytes_per_step": 8,
+            "ms_per_step": round(ms_res, 3),
+            "path": "HostStreamer.step_predict_resident: pinned host G -> device (chunked) -> K3 on device-resident "
+                    "W, m, v -> W', W_hat on device; non-finite flag read back",
+            "launches": res_launches,
+        },
     }
     del w_h, g_h, wo_h, wh_h, streamer, opt
     torch.cuda.empty_cache()

@@ -533,7 +533,7 @@ class HostStreamer:
     This is what a caller that keeps parameters on the host sees end to end.
     """
 
-    def __init__(self, device, chunk_elems: int = 1 << 25, slots: int = 3):
+    def __init__(self, device, chunk_elems: int = 1 << 24, slots: int = 4):
         self.device = torch.device(device)
         self.chunk = int(chunk_elems)
         self.slots = int(slots)
