@@ -1,6 +1,5 @@
 """Host-buffer (e2e) K3 path: PCIe throughput under different chunk sizes /
 slot counts, plus the device-resident-params variant (G in, flag out)."""
-import ctypes
 import json
 import sys
 import time
