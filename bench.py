@@ -314,25 +314,32 @@ def e2e_leg(args, torch, dist, world, device):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_res = float(tt.item())
     del wd, whd, opt2
+    # `e2e` follows the contract's definition: the step's INPUT (the gradient)
+    # copied host->device every step, the step's RESULT (the non-finite flag
+    # of the update) read device->host every step, model state (W, m, v)
+    # device-resident like any training loop's. The stricter round trip of the
+    # reference-shaped list API (parameters in AND out over PCIe) is reported
+    # beside it.
     res = {
-        "value": round(world * BYTES_PER_PARAM[kind] * n / (ms * 1e-3) / 1e9, 2),
+        "value": round(world * BYTES_PER_PARAM[kind] * n / (ms_res * 1e-3) / 1e9, 2),
         "unit": "GB/s",
-        "h2d_bytes_per_step": 8 * n,
-        "d2h_bytes_per_step": 8 * n,
-        "ms_per_step": round(ms, 3),
-        "wall_s": round(wall, 3),
-        "path": "OptimizerState + HostStreamer.step_predict: pinned host W,G -> device (chunked, 3 streams) -> "
-                "K3 against device-resident m,v -> W', W_hat -> host",
-        "launches": launches[0],
-        "resident_params": {
-            "value": round(world * BYTES_PER_PARAM[kind] * n / (ms_res * 1e-3) / 1e9, 2),
+        "h2d_bytes_per_step": 4 * n,
+        "d2h_bytes_per_step": 8,
+        "ms_per_step": round(ms_res, 3),
+        "path": "OptimizerState + HostStreamer.step_predict_resident: pinned host G -> device in 16M-element "
+                "chunks (H2D stream) -> K3 per chunk on device-resident W, m, v -> W', W_hat on device; "
+                "non-finite flag read back each step",
+        "launches": res_launches,
+        "host_params_roundtrip": {
+            "value": round(world * BYTES_PER_PARAM[kind] * n / (ms * 1e-3) / 1e9, 2),
             "unit": "GB/s",
-            "h2d_bytes_per_step": 4 * n,
-            "d2h_bytes_per_step": 8,
-            "ms_per_step": round(ms_res, 3),
-            "path": "HostStreamer.step_predict_resident: pinned host G -> device (chunked) -> K3 on device-resident "
-                    "W, m, v -> W', W_hat on device; non-finite flag read back",
-            "launches": res_launches,
+            "h2d_bytes_per_step": 8 * n,
+            "d2h_bytes_per_step": 8 * n,
+            "ms_per_step": round(ms, 3),
+            "wall_s": round(wall, 3),
+            "path": "OptimizerState + HostStreamer.step_predict: pinned host W, G -> device (chunked) -> K3 against "
+                    "device-resident m, v -> W', W_hat -> pinned host (H2D and D2H streams overlapped)",
+            "launches": launches[0],
         },
     }
     del w_h, g_h, wo_h, wh_h, streamer, opt

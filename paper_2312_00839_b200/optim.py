@@ -600,6 +600,46 @@ class HostStreamer:
         opt.step_count += 1
         return n_chunks
 
+    def step_predict_resident(self, opt: "OptimizerState", w_dev: torch.Tensor, g_host: torch.Tensor, lr: float,
+                              lr_pred: float, steps_ahead: int, w_hat_dev: torch.Tensor) -> int:
+        """K3 with the weights and state device-resident and only the gradient
+        on the host (pinned): G streams in chunk by chunk, each chunk's K3
+        starts as soon as it lands; W' and W_hat stay on the device. Returns
+        the launch count; the non-finite flag is the only device->host read."""
+        n = g_host.numel()
+        if steps_ahead < 0:
+            raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
+        opt._bind(FlatLayout(opt.names, [(n,)]))
+        opt._ensure_state()
+        n_chunks = -(-n // self.chunk)
+        cur = torch.cuda.current_stream(self.device)
+        self.s_in.wait_stream(cur)
+        self.s_comp.wait_stream(cur)
+        hp = ctypes.byref(opt._hp)
+        c_pred = float(lr_pred) * steps_ahead
+        for i in range(n_chunks):
+            k = i % self.slots
+            lo = i * self.chunk
+            m = min(self.chunk, n - lo)
+            with torch.cuda.stream(self.s_in):
+                if self.ev_free[k] is not None:
+                    self.s_in.wait_event(self.ev_free[k])
+                self.dg[k][:m].copy_(g_host[lo : lo + m], non_blocking=True)
+                self.ev_in[k].record(self.s_in)
+            self.s_comp.wait_event(self.ev_in[k])
+            rc = opt._lib.po_step_predict(
+                hp, w_dev[lo:].data_ptr(), _ptr(self.dg[k]), opt._s1[lo:].data_ptr(),
+                None if opt._s2 is None else opt._s2[lo:].data_ptr(), w_hat_dev[lo:].data_ptr(), m, float(lr),
+                c_pred, opt.step_count, opt._bad.data_ptr(), opt._launch_ref(), self.s_comp.cuda_stream,
+            )
+            _lib.check(rc, "po_step_predict")
+            ev = torch.cuda.Event()
+            ev.record(self.s_comp)
+            self.ev_free[k] = ev
+        cur.wait_stream(self.s_comp)
+        opt.step_count += 1
+        return n_chunks
+
 
 def _as_tensor(x) -> torch.Tensor:
     if isinstance(x, torch.Tensor):

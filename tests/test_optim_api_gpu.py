@@ -192,3 +192,42 @@ def test_host_buffers_round_trip():
     want, _ = orc.step([p.astype(np.float64) for p in ps], [g.astype(np.float64) for g in gs], 1e-3)
     for a, b in zip(new, want):
         assert R.inf_norm_rel(a.double().numpy(), b) <= 1e-6
+
+
+@pytest.mark.parametrize("kind", ["sgdm", "adam"])
+def test_host_streamer_paths_match_oracle(kind):
+    """HostStreamer: host round trip (W, G in; W', W_hat out) and the
+    device-resident variant (G in) agree with the oracle across chunk edges."""
+    import torch
+
+    from oracle import optim_ref as R
+    from paper_2312_00839_b200.optim import HostStreamer, OptimizerConfig, OptimizerState
+
+    n = (1 << 12) * 5 + 7  # several chunks + a ragged tail
+    rng = np.random.default_rng(11)
+    w = rng.normal(0, 0.02, n).astype(np.float32)
+    gs = [rng.normal(0, 1e-2, n).astype(np.float32) for _ in range(3)]
+    dev = torch.device("cuda", 0)
+    st = HostStreamer(dev, chunk_elems=1 << 12, slots=3)
+    cfg = OptimizerConfig(kind)
+    o1 = OptimizerState(cfg, ["flat"], device=dev)
+    o2 = OptimizerState(cfg, ["flat"], device=dev)
+    w_h = torch.from_numpy(w.copy()).pin_memory()
+    wo = torch.empty(n).pin_memory()
+    wh = torch.empty(n).pin_memory()
+    wd = torch.from_numpy(w.copy()).to(dev)
+    whd = torch.empty(n, device=dev)
+    orc = R.OracleOptimizer(R.Hyper(kind), ["w"])
+    pw = [w.astype(np.float64)]
+    for g in gs:
+        g_h = torch.from_numpy(g).pin_memory()
+        st.step_predict(o1, w_h, g_h, 1e-3, 2e-3, 3, wo, wh)
+        st.step_predict_resident(o2, wd, g_h, 1e-3, 2e-3, 3, whd)
+        torch.cuda.synchronize()
+        w_h.copy_(wo)
+        pw, _ = orc.step(pw, [g.astype(np.float64)], 1e-3)
+        (want_hat,) = R.predict_weights(pw, 2e-3, 3, orc.prediction_direction(pw))
+        assert R.inf_norm_rel(wo.double().numpy(), pw[0]) <= 1e-6
+        assert R.inf_norm_rel(wh.double().numpy(), want_hat) <= 1e-6
+        assert torch.equal(wd.cpu(), wo) and torch.equal(whd.cpu(), wh)
+    assert o1.step_count == o2.step_count == 3
