@@ -153,6 +153,26 @@ int po_step_predict_dc(const po_hparams* hp, float* w, const float* g, float* st
                        float* w_hat, int64_t n, const po_coef* coef_dev, int64_t* nonfinite_index,
                        const po_launch* launch, void* stream);
 
+/* ---- hybrid DP x PP: gradient mean over peer memory fused into K3 -------- */
+
+/* Release-store `epoch` into slot `my rank` of every replica's flag array
+ * (peer_flag_slots: DEVICE array of dp pointers, one per replica, each
+ * pointing at that replica's flags[my_rank]); enqueue after the backward that
+ * produced this replica's gradient. */
+int po_dp_signal(long long* const* peer_flag_slots, int32_t dp, int64_t epoch, void* stream);
+
+/* K3 on this replica's stage with g = (sum over replicas r, in rank order, of
+ * grads[r]) / dp read directly from the replicas' (peer-mapped) gradient
+ * buffers; every CTA first acquire-waits until flags[r] >= epoch for all r
+ * (flags: this replica's local [dp] array that the peers signal into). If a
+ * replica has not signalled after timeout_ms the kernel writes *status = 1
+ * (device int) and updates nothing. grads_host: HOST array of dp device
+ * pointers. dp <= 8. */
+int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp, float* state1,
+                       float* state2, float* w_hat, int64_t n, double lr, double lr_pred_times_s,
+                       int64_t step_count, int64_t* nonfinite_index, const int64_t* flags, int64_t epoch,
+                       int64_t timeout_ms, int32_t* status, void* stream);
+
 /* ---- fused per-event stage ops (pipeoptim_stage_ops.cu) ---------------- */
 
 #define PO_LOSS_MSE 0

@@ -510,6 +510,128 @@ Coef coef(const po_hparams* hp, double lr, double c_pred, int64_t t) {
   return c;
 }
 
+// ---- hybrid DP x PP: gradient reduction over peer memory fused into K3 -------
+//
+// Each data-parallel replica of a stage owns a flat gradient buffer; the
+// replicas map each other's buffers (CUDA IPC over NVLink / NVSwitch). The
+// fused kernel reads the dp gradients of every element straight from peer
+// memory, sums them in RANK ORDER (so every replica computes the identical
+// mean and the replicas stay bit-identical), and applies K3 in the same pass:
+// no reduced gradient is written to HBM and read back, no separate collective
+// launch. A replica signals "my gradient of epoch e is complete" with one
+// release store per peer into the peer's flag array (po_dp_signal, enqueued
+// after its backward); the fused kernel's CTAs acquire-spin on their local
+// flags before touching any peer gradient. Gradients are double-buffered by
+// epoch parity, which makes a second "consumed" handshake unnecessary: a
+// replica overwrites parity p again only in epoch e+2, after it observed every
+// peer's epoch-(e+1) signal, which each peer issued after its epoch-e update
+// (stream order) had finished reading.
+
+constexpr int kMaxDp = 8;
+
+struct DpArgs {
+  Args a;                             // w, s1, s2, out (w_hat), n, bad, coefficients
+  const float* grads[kMaxDp];         // every replica's gradient (this epoch's parity), rank order
+  int dp;
+  float inv_dp;
+  const long long* flags;             // local [dp]: last epoch each replica signalled
+  long long epoch;
+  long long timeout_cycles;
+  int* status;                        // set to 1 if a peer never signalled (kernel then skips)
+};
+
+__device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int KIND, int VEC>
+__global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    int good = 1;
+    const long long t0 = clock64();
+    for (int r = 0; r < d.dp && good; ++r) {
+      while (ld_acquire_sys(d.flags + r) < d.epoch) {
+        if (clock64() - t0 > d.timeout_cycles) {
+          atomicExch(d.status, 1);
+          good = 0;
+          break;
+        }
+        __nanosleep(256);
+      }
+    }
+    ok = good;
+  }
+  __syncthreads();
+  if (!ok) return;
+  const Args& a = d.a;
+  const Coef c = load_coef(a);
+  const int64_t nv = a.n / VEC;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t bad = INT64_MAX;
+  for (int64_t i = tid; i < nv; i += stride) {
+    const int64_t base = i * VEC;
+    Vec<VEC> g = vload<VEC, 1, true>(d.grads[0] + base);
+    Vec<VEC> w = vload<VEC, 1, false>(a.w + base);
+    Vec<VEC> s1 = vload<VEC, 1, false>(a.s1 + base);
+    Vec<VEC> s2{};
+    if constexpr (KIND != PO_SGDM) s2 = vload<VEC, 1, false>(a.s2 + base);
+#pragma unroll 1
+    for (int r = 1; r < d.dp; ++r) {
+      const Vec<VEC> gr = vload<VEC, 1, true>(d.grads[r] + base);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) g.v[j] = __fadd_rn(g.v[j], gr.v[j]);
+    }
+    Vec<VEC> out;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      bool e = false;
+      elem<KIND, MODE_STEP_PREDICT>(c, w.v[j], __fmul_rn(g.v[j], d.inv_dp), s1.v[j], s2.v[j], out.v[j], e);
+      if (e && bad == INT64_MAX) bad = base + j;
+    }
+    vstore<VEC, 1>(a.w + base, w);
+    vstore<VEC, 1>(a.s1 + base, s1);
+    if constexpr (KIND != PO_SGDM) vstore<VEC, 1>(a.s2 + base, s2);
+    vstore<VEC, 1>(a.out + base, out);
+  }
+  const int64_t t = nv * VEC + tid;  // scalar tail
+  if (t < a.n) {
+    float g = d.grads[0][t];
+    for (int r = 1; r < d.dp; ++r) g = __fadd_rn(g, d.grads[r][t]);
+    float w = a.w[t], s1 = a.s1[t], s2 = (KIND != PO_SGDM) ? a.s2[t] : 0.f, out = 0.f;
+    bool e = false;
+    elem<KIND, MODE_STEP_PREDICT>(c, w, __fmul_rn(g, d.inv_dp), s1, s2, out, e);
+    if (e && bad == INT64_MAX) bad = t;
+    a.w[t] = w;
+    a.s1[t] = s1;
+    if constexpr (KIND != PO_SGDM) a.s2[t] = s2;
+    a.out[t] = out;
+  }
+  if (a.bad != nullptr && bad != INT64_MAX) atomicMin(a.bad, (unsigned long long)bad);
+}
+
+__global__ void po_dp_signal_kernel(long long* const* slots, int dp, long long epoch) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < dp; ++r)
+      asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(slots[r]), "l"(epoch) : "memory");
+  }
+}
+
+template <int KIND>
+cudaError_t launch_dp(const DpArgs& d, int vec, dim3 grid, dim3 block, cudaStream_t s) {
+  if (vec == 8)
+    po_dp_kernel<KIND, 8><<<grid, block, 0, s>>>(d);
+  else if (vec == 4)
+    po_dp_kernel<KIND, 4><<<grid, block, 0, s>>>(d);
+  else
+    po_dp_kernel<KIND, 1><<<grid, block, 0, s>>>(d);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" {
@@ -641,6 +763,63 @@ int po_step_predict_dc(const po_hparams* hp, float* w, const float* g, float* st
   Args a{w, g, state1, hp->kind == PO_SGDM ? nullptr : state2, w_hat, n,
          reinterpret_cast<unsigned long long*>(nonfinite_index), coef_dev, coef(hp, 0.0, 0.0, 1)};
   return run(hp->kind, MODE_STEP_PREDICT, a, launch, (cudaStream_t)stream);
+}
+
+int po_dp_signal(long long* const* peer_flag_slots, int32_t dp, int64_t epoch, void* stream) {
+  if (peer_flag_slots == nullptr || dp < 1 || dp > kMaxDp) return PO_EINVAL;
+  po_dp_signal_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(peer_flag_slots, dp, (long long)epoch);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp, float* state1,
+                       float* state2, float* w_hat, int64_t n, double lr, double lr_pred_times_s,
+                       int64_t step_count, int64_t* nonfinite_index, const int64_t* flags, int64_t epoch,
+                       int64_t timeout_ms, int32_t* status, void* stream) {
+  if (!valid_hp(hp) || step_count < 0 || dp < 1 || dp > kMaxDp || grads_host == nullptr || flags == nullptr ||
+      status == nullptr || n < 0)
+    return PO_EINVAL;
+  if (n > 0 && (w == nullptr || state1 == nullptr || w_hat == nullptr || (hp->kind != PO_SGDM && state2 == nullptr)))
+    return PO_EINVAL;
+  DpArgs d;
+  memset(&d, 0, sizeof(d));
+  d.a = Args{w, nullptr, state1, hp->kind == PO_SGDM ? nullptr : state2, w_hat, n,
+             reinterpret_cast<unsigned long long*>(nonfinite_index), nullptr,
+             coef(hp, lr, lr_pred_times_s, step_count + 1)};
+  for (int r = 0; r < dp; ++r) {
+    if (n > 0 && grads_host[r] == nullptr) return PO_EINVAL;
+    d.grads[r] = grads_host[r];
+  }
+  d.dp = dp;
+  d.inv_dp = (float)(1.0 / (double)dp);
+  d.flags = reinterpret_cast<const long long*>(flags);
+  d.epoch = (long long)epoch;
+  d.timeout_cycles = (long long)(timeout_ms > 0 ? timeout_ms : 60000) * 2000000LL;  // ~2 GHz SM clock
+  d.status = status;
+  if (n == 0) return 0;
+  int vec = 8;
+  const void* ptrs[4] = {w, state1, hp->kind == PO_SGDM ? nullptr : state2, w_hat};
+  auto all_aligned = [&](int bytes) {
+    for (const void* p : ptrs)
+      if (!aligned(p, bytes)) return false;
+    for (int r = 0; r < dp; ++r)
+      if (!aligned(grads_host[r], bytes)) return false;
+    return true;
+  };
+  while (vec > 1 && !all_aligned(vec * 4)) vec = vec == 8 ? 4 : 1;
+  const int block = 256;
+  const int64_t nv = n / vec;
+  int64_t want = (nv + block - 1) / block;
+  if (want < 1) want = 1;
+  int64_t cap = (int64_t)sm_count() * 8;
+  const int64_t grid = want < cap ? want : cap;
+  cudaError_t e;
+  switch (hp->kind) {
+    case PO_SGDM: e = launch_dp<PO_SGDM>(d, vec, dim3((unsigned)grid), dim3(block), (cudaStream_t)stream); break;
+    case PO_ADAM: e = launch_dp<PO_ADAM>(d, vec, dim3((unsigned)grid), dim3(block), (cudaStream_t)stream); break;
+    default: e = launch_dp<PO_ADAMW>(d, vec, dim3((unsigned)grid), dim3(block), (cudaStream_t)stream); break;
+  }
+  return e == cudaSuccess ? 0 : (int)e;
 }
 
 }  // extern "C"

@@ -109,7 +109,7 @@ class PipelineStageRunner:
     def __init__(self, dist, tl: Timeline, stage: StageModel, opt, strategy: str, data, loss_kind: str,
                  lr_for_mb, rows: int, *, checks: str = "deferred", fuse: bool = True, group=None,
                  stage_ranks: list[int] | None = None, dp_group=None, dp_rank: int = 0, dp_size: int = 1,
-                 host_staging: bool = False):
+                 host_staging: bool = False, fused_dp=None):
         """stage_ranks[k] is the global rank holding stage k of this pipeline
         replica (default: rank k). With dp_size > 1 (hybrid DP x PP), replica
         `dp_rank` trains on rows [dp_rank*rows, (dp_rank+1)*rows) of every
@@ -141,6 +141,12 @@ class PipelineStageRunner:
         self.device = stage.flat.device
         self.stage_ranks = stage_ranks or list(range(self.depth))
         self.dp_group, self.dp_rank, self.dp_size = dp_group, dp_rank, dp_size
+        # fused_dp: a dp_fused.FusedDPGroup — the DP mean is read from the
+        # replicas' peer-mapped gradients inside the K3 pass (no all-reduce)
+        self.fused_dp = fused_dp
+        if fused_dp is not None:
+            stage.set_grad_buffer(fused_dp.grad)
+            self._scratch = None
         opt.eager_checks = self.eager
 
     # -- what each op consumes / produces -------------------------------------------------
@@ -227,6 +233,8 @@ class PipelineStageRunner:
                 nxt_buf, recv = None, []
             nxt_req = self.comm.post([out_msg] if out_msg else [], recv)
         self.comm.drain()
+        if self.fused_dp is not None:
+            self.fused_dp.check()
         if not self.eager:
             if not bool(flags.all()):
                 bad = int((~flags).nonzero()[0].item())
@@ -249,6 +257,24 @@ class PipelineStageRunner:
         return t[self.dp_rank * self.rows : (self.dp_rank + 1) * self.rows]
 
     def _update(self, op):
+        if self.fused_dp is not None:
+            lr = self.lr_for_mb(op.mb)
+            if self.fuse and op.fuse_predict:
+                out, lr_p, gap = self.rt.staging_buffer(), self.lr_for_mb(op.next_mb), op.next_gap
+                self.rt.prepared = (op.next_mb, op.next_gap)
+            else:  # plain step: the prediction output goes to scratch
+                if self._scratch is None:
+                    self._scratch = self.stage.flat.layout.empty(self.device)
+                out, lr_p, gap = self._scratch, 0.0, 0
+            self.fused_dp.step_predict(self.opt, self.stage.flat, lr, lr_p, gap, out)
+            if self.eager:
+                self.opt.check_finite()
+                self.fused_dp.check()
+            self.stage.set_grad_buffer(self.fused_dp.grad)
+            self.stage.version += 1
+            self.rt.pending_count = 0
+            self.policy.after_update(self.rt)
+            return
         if self.dp_size > 1:
             # hybrid DP x PP: mean gradient over the data-parallel replicas of
             # this stage, then the (fused) update on identical replicas

@@ -214,6 +214,11 @@ class ModuleStage:
     def numel(self) -> int:
         return self.flat.layout.numel
 
+    def set_grad_buffer(self, buf: torch.Tensor) -> None:
+        self.flat.grad = buf
+        for p, gv in zip(self._params, self.flat.grads):
+            p.grad = gv
+
     def _point(self, views) -> None:
         for p, v in zip(self._params, views):
             if p.data_ptr() != v.data_ptr():

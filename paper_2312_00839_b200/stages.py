@@ -180,6 +180,11 @@ class StageModel:
     def out_shape(self) -> tuple:
         return (self.out_dim,)
 
+    def set_grad_buffer(self, buf: torch.Tensor) -> None:
+        """Point the stage's flat gradient at `buf` (same layout), e.g. the
+        current parity of a fused-DP double buffer."""
+        self.flat.grad = buf
+
     def run_forward(self, weights, key, x, version, check_finite=True, finite_flags=None, flag_index=0):
         return stage_forward(self, weights, key, x, version, check_finite, finite_flags, flag_index)
 

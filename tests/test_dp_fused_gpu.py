@@ -1,0 +1,140 @@
+"""Hybrid DP x PP with the gradient mean fused into K3 over peer-mapped
+memory (po_step_predict_dp). On the one-GPU box the replicas are processes
+sharing the B200 (CUDA IPC on one device, gloo + host staging for the
+pipeline P2P) — the same kernel and handshake that run over NVLink."""
+
+import json
+import os
+import socket
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import optim_ref, rng_ref, runtime_ref
+
+pytestmark = pytest.mark.gpu
+
+DIMS = [16, 24, 24, 24, 10]
+ACTS = ["tanh", "tanh", "tanh", "linear"]
+
+
+class Src:
+    def batch(self, mb):
+        s = rng_ref.Stream(9, f"batch-{mb}")
+        return s.normal(8, DIMS[0]), s.normal(8, DIMS[-1])
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _single(rank, port, out_dir):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        from paper_2312_00839_b200 import _lib
+        from paper_2312_00839_b200.dp_fused import FusedDPGroup
+        from paper_2312_00839_b200.optim import FlatLayout, FlatParams, OptimizerConfig, OptimizerState
+
+        dev = torch.device("cuda", 0)
+        n = 100_003
+        lay = FlatLayout(["w"], [(n,)])
+        grp = FusedDPGroup(dist, None, 0, 1, lay.numel, dev)
+        gen = torch.Generator(device=dev).manual_seed(1)
+        w0 = torch.randn(lay.numel, device=dev, generator=gen) * 0.02
+        g = torch.randn(lay.numel, device=dev, generator=gen) * 0.01
+        results = []
+        for fused in (True, False):
+            flat = FlatParams(lay, dev, w0.clone())
+            opt = OptimizerState(OptimizerConfig("adamw"), ["w"], device=dev)
+            out = torch.empty(lay.numel, device=dev)
+            for _ in range(3):
+                if fused:
+                    grp.grad.copy_(g)
+                    grp.step_predict(opt, flat, 1e-3, 2e-3, 3, out)
+                else:
+                    flat.grad.copy_(g)
+                    opt.step_predict_(flat, 1e-3, 2e-3, 3, out)
+            torch.cuda.synchronize()
+            results.append((flat.data.clone(), out.clone()))
+        grp.check()
+        same = torch.equal(results[0][0], results[1][0]) and torch.equal(results[0][1], results[1][1])
+        Path(out_dir, "single.json").write_text(json.dumps({"same": bool(same)}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_dp_with_one_replica_equals_k3(tmp_path):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_single, args=(_port(), str(tmp_path)), nprocs=1, join=True)
+    assert json.loads((tmp_path / "single.json").read_text())["same"]
+
+
+def _hybrid(rank, world, port, dp, pp, n, kind, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.dp_fused import FusedDPGroup
+        from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+        from paper_2312_00839_b200.pipeline import PipelineStageRunner, gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+        from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+        torch.backends.cuda.matmul.allow_tf32 = False
+        dev = torch.device("cuda", 0)
+        r, k = divmod(rank, pp)
+        groups = [dist.new_group([q * pp + s for q in range(dp)]) for s in range(pp)]
+        stage = StageModel(k, partition_layers(build_layers(DIMS, ACTS), pp)[k],
+                           lambda sp: rng_ref.layer_init(4, sp.index, sp.in_dim, sp.out_dim), dev)
+        kw = {"weight_decay": 0.0} if kind == "sgdm" else {}
+        opt = OptimizerState(OptimizerConfig(kind, **kw), stage.param_names, device=dev)
+        fused = FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, dev, timeout_ms=120_000)
+        tl = build_timeline("optimizer_prediction", pp, n)
+        runner = PipelineStageRunner(dist, tl, stage, opt, "optimizer_prediction", Src(), "mse", lambda mb: 0.01,
+                                     8 // dp, stage_ranks=[r * pp + s for s in range(pp)], dp_group=groups[k],
+                                     dp_rank=r, dp_size=dp, host_staging=True, fused_dp=fused)
+        rep = runner.run()
+        reps = gather_reports(dist, rep, world)
+        if rank == 0:
+            last = [rp for rp in reps if rp.rank == pp - 1]
+            Path(out_dir, "out.json").write_text(json.dumps({
+                "losses": np.mean([rp.losses for rp in last], axis=0).tolist(),
+                "records": sorted([[x.mb, x.stage, x.forward_version, x.predicted, x.prediction_target,
+                                    x.backward_version, x.live_backward_version] for x in reps[0].records])}))
+        Path(out_dir, f"params{rank}.json").write_text(json.dumps(
+            {n_: p.detach().double().cpu().numpy().tolist() for n_, p in zip(stage.param_names, stage.params)}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgdm"])
+def test_fused_dp_x_pp_equals_full_batch_pipeline(tmp_path, kind):
+    """DP 2 x PP 2 (4 processes on one GPU): the fused peer-memory mean + K3
+    keeps the replicas bit-identical and equals the 2-stage pipeline on the
+    full batch (oracle)."""
+    import torch.multiprocessing as mp
+
+    dp, pp, n = 2, 2, 8
+    mp.spawn(_hybrid, args=(dp * pp, _port(), dp, pp, n, kind, str(tmp_path)), nprocs=dp * pp, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    ref = runtime_ref.run(DIMS, ACTS, pp, n, "optimizer_prediction", optim_ref.Hyper(kind, weight_decay=0.0),
+                          Src().batch, "mse", lambda mb: 0.01, lambda i, a, b: rng_ref.layer_init(4, i, a, b))
+    assert np.allclose(got["losses"], ref["losses"], rtol=1e-4, atol=1e-6)
+    for k in range(pp):
+        p0 = json.loads((tmp_path / f"params{k}.json").read_text())
+        p1 = json.loads((tmp_path / f"params{pp + k}.json").read_text())
+        for name, want in zip(ref["names"][k], ref["params"][k]):
+            assert p0[name] == p1[name]  # replicas bit-identical
+            assert optim_ref.inf_norm_rel(np.array(p0[name]), want) <= 1e-4
