@@ -360,6 +360,13 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
     else:
         out = bp.multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches)
+        if world >= 2 and world % 2 == 0:
+            from paper_2312_00839_b200.pipeline import bench_hybrid_dp_pp
+
+            try:
+                out["hybrid_dp_pp"] = bench_hybrid_dp_pp(torch, dist, rank, world, device)
+            except Exception as exc:
+                out["hybrid_dp_pp"] = {"error": f"{type(exc).__name__}: {exc}"}
     if not args.no_configs:
         from paper_2312_00839_b200.pipeline import bench_module_pipeline
 
@@ -416,12 +423,14 @@ def ours(args):
             pipe = {"error": f"{type(exc).__name__}: {exc}"}
         dog.cancel()
     line["pipeline"] = pipe
-    if world > 1:
-        dist.barrier()
-    if rank == 0:
+    if rank == 0:  # printed before any teardown that could fail
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        try:
+            dist.barrier()
+            dist.destroy_process_group()
+        except Exception:
+            os._exit(0)
 
 
 def _line(args, kern, e2e, cpu, world):

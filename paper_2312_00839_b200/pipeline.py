@@ -396,3 +396,53 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
     torch_mod.backends.cuda.matmul.allow_tf32 = False
     torch_mod.backends.cudnn.allow_tf32 = False
     return out
+
+
+def bench_hybrid_dp_pp(torch_mod, dist, rank, world, device, n_batches: int = 32):
+    """DP 2 x PP world/2 on config-1-shaped stages (each replica half of every
+    B = 128 batch): the stage-gradient mean by NCCL all-reduce + K3 vs the
+    fused peer-memory mean inside K3 (dp_fused). Samples/s, max over ranks."""
+    from .bench_pipeline import BATCH, CONFIG1_ACTS, CONFIG1_DIMS, DeviceBatches
+    from .dp_fused import FusedDPGroup
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import build_timeline
+    from .stages import build_layers, partition_layers, torch_init
+
+    dp, pp = 2, world // 2
+    if world % 2 or pp < 1:
+        return {"error": f"hybrid leg needs an even world size, got {world}"}
+    torch_mod.backends.cuda.matmul.allow_tf32 = False
+    r, k = divmod(rank, pp)
+    groups = [dist.new_group([q * pp + s for q in range(dp)]) for s in range(pp)]
+    if pp <= 4:
+        dims, acts = CONFIG1_DIMS, CONFIG1_ACTS
+    else:
+        dims, acts = [3072] + [1024] * (pp - 1) + [10], ["relu"] * (pp - 1) + ["linear"]
+    layers = build_layers(dims, acts)
+    data = DeviceBatches(torch_mod, device, dims=dims)
+    out = {"config": f"DP {dp} x PP {pp}, MLP {dims}, B={BATCH} ({BATCH // dp} rows per replica), Adam, "
+                     f"optimizer_prediction, {n_batches} mini-batches"}
+    for arm in ("nccl_allreduce", "fused_peer_mean"):
+        times = []
+        for trial, n in enumerate((2 * pp + 2, n_batches)):
+            stage = StageModel(k, partition_layers(layers, pp)[k], torch_init(0, device), device)
+            opt = OptimizerState(OptimizerConfig("adam"), stage.param_names, device=device)
+            fused = (FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, device)
+                     if arm == "fused_peer_mean" else None)
+            runner = PipelineStageRunner(dist, build_timeline("optimizer_prediction", pp, n), stage, opt,
+                                         "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-4, BATCH // dp,
+                                         stage_ranks=[r * pp + s for s in range(pp)], dp_group=groups[k],
+                                         dp_rank=r, dp_size=dp, fused_dp=fused)
+            torch_mod.cuda.synchronize(device)
+            dist.barrier()
+            e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
+            e0.record()
+            runner.run()
+            e1.record()
+            torch_mod.cuda.synchronize(device)
+            dist.barrier()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        t = torch_mod.tensor([times[-1]], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[arm] = {"samples_per_s": round(n_batches * BATCH / float(t.item()), 1), "s": round(float(t.item()), 4)}
+    return out
