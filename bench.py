@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--pipeline-batches", type=int, default=64)
     ap.add_argument("--pipeline-timeout", type=float, default=420.0)
     ap.add_argument("--no-configs", action="store_true", help="skip configs 2-4 in the pipeline leg")
+    # test-only: exercise the multi-rank bench on ONE GPU (ranks share the
+    # device, gloo transport with host staging); never used for numbers
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--share-gpu", action="store_true")
     return ap.parse_args()
 
 
@@ -359,12 +363,14 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         out["tf32"] = {k: t[k] for k in ("pred_on", "pred_off", "prediction_overhead", "config")}
         out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
     else:
-        out = bp.multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches)
+        staged = args.dist_backend != "nccl"
+        out = bp.multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches,
+                                    host_staging=staged)
         if world >= 2 and world % 2 == 0:
             from paper_2312_00839_b200.pipeline import bench_hybrid_dp_pp
 
             try:
-                out["hybrid_dp_pp"] = bench_hybrid_dp_pp(torch, dist, rank, world, device)
+                out["hybrid_dp_pp"] = bench_hybrid_dp_pp(torch, dist, rank, world, device, host_staging=staged)
             except Exception as exc:
                 out["hybrid_dp_pp"] = {"error": f"{type(exc).__name__}: {exc}"}
     if not args.no_configs:
@@ -376,7 +382,8 @@ def pipeline_leg(args, torch, dist, rank, world, device):
                 if world == 1:
                     configs[name] = bp.single_gpu_module_pipeline(torch, device, name, n_batches=16)
                 else:
-                    configs[name] = bench_module_pipeline(torch, dist, rank, world, device, name, n_batches=16)
+                    configs[name] = bench_module_pipeline(torch, dist, rank, world, device, name, n_batches=16,
+                                                          host_staging=args.dist_backend != "nccl")
             except Exception as exc:
                 configs[name] = {"error": f"{type(exc).__name__}: {exc}"}
             torch.cuda.empty_cache()
@@ -391,10 +398,13 @@ def ours(args):
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (there is no CPU fallback for the PipeOptim kernels)")
-    device = torch.device("cuda", local)
+    device = torch.device("cuda", 0 if args.share_gpu else local)
     torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group("gloo")
     kern = kernel_leg(args, torch, dist, rank, world, device)
     e2e = None if args.no_e2e else e2e_leg(args, torch, dist, world, device)
     cpu = None

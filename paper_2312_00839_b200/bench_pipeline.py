@@ -321,8 +321,8 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
     return out
 
 
-def multi_gpu_pipeline(torch, dist, rank, world, device, n_batches: int = 64):
+def multi_gpu_pipeline(torch, dist, rank, world, device, n_batches: int = 64, host_staging: bool = False):
     """One stage per GPU over NCCL (pipeline.py); depth = world."""
     from .pipeline import bench_config1_pipeline
 
-    return bench_config1_pipeline(torch, dist, rank, world, device, n_batches=n_batches)
+    return bench_config1_pipeline(torch, dist, rank, world, device, n_batches=n_batches, host_staging=host_staging)

@@ -305,7 +305,7 @@ def gather_reports(dist, report: StageReport, world: int):
 # ---- bench support ---------------------------------------------------------------------------
 
 
-def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int = 64):
+def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int = 64, host_staging: bool = False):
     """Config-1-shaped pipeline on `world` GPUs: prediction on vs off, samples/s
     (device-timed per rank, max over ranks)."""
     from .bench_pipeline import BATCH, CONFIG1_ACTS, CONFIG1_DIMS, DeviceBatches
@@ -331,7 +331,7 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
             opt = OptimizerState(OptimizerConfig("adam"), stage.param_names, device=device)
             tl = build_timeline(strategy, world, n_batches if trial else 2 * world + 2)
             runner = PipelineStageRunner(dist, tl, stage, opt, strategy, data, "softmax_xent", lambda mb: 1e-4,
-                                         BATCH)
+                                         BATCH, host_staging=host_staging)
             torch_mod.cuda.synchronize(device)
             dist.barrier()
             e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
@@ -351,7 +351,8 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
     return out
 
 
-def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_batches: int = 16):
+def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_batches: int = 16,
+                          host_staging: bool = False):
     """Configs 2-4 on `world` GPUs, one stage per GPU (depth = world):
     prediction on vs off, samples/s device-timed, max over ranks."""
     from .bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
@@ -377,7 +378,7 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
             opt = OptimizerState(OptimizerConfig(cfg["opt"], **kw), stage.param_names, device=device)
             tl = build_timeline(strategy, world, n)
             runner = PipelineStageRunner(dist, tl, stage, opt, strategy, data, "softmax_xent", lambda mb: cfg["lr"],
-                                         cfg["batch"])
+                                         cfg["batch"], host_staging=host_staging)
             torch_mod.cuda.synchronize(device)
             dist.barrier()
             e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
@@ -398,7 +399,7 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
     return out
 
 
-def bench_hybrid_dp_pp(torch_mod, dist, rank, world, device, n_batches: int = 32):
+def bench_hybrid_dp_pp(torch_mod, dist, rank, world, device, n_batches: int = 32, host_staging: bool = False):
     """DP 2 x PP world/2 on config-1-shaped stages (each replica half of every
     B = 128 batch): the stage-gradient mean by NCCL all-reduce + K3 vs the
     fused peer-memory mean inside K3 (dp_fused). Samples/s, max over ranks."""
@@ -432,7 +433,7 @@ def bench_hybrid_dp_pp(torch_mod, dist, rank, world, device, n_batches: int = 32
             runner = PipelineStageRunner(dist, build_timeline("optimizer_prediction", pp, n), stage, opt,
                                          "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-4, BATCH // dp,
                                          stage_ranks=[r * pp + s for s in range(pp)], dp_group=groups[k],
-                                         dp_rank=r, dp_size=dp, fused_dp=fused)
+                                         dp_rank=r, dp_size=dp, fused_dp=fused, host_staging=host_staging)
             torch_mod.cuda.synchronize(device)
             dist.barrier()
             e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
