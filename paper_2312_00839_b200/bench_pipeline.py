@@ -267,16 +267,27 @@ class ModuleBatches:
 _COSTS: dict = {}
 
 
-def module_stages_for(torch, name, device, depth=None):
-    from .stage_models import build_module_stages, profile_block_costs
+def module_block_costs(torch, name, device):
+    """Profiled per-block costs (cached). Multi-rank callers must use ONE
+    rank's costs everywhere: timing noise would otherwise give the ranks
+    different partitions and mismatched activation shapes."""
+    from .stage_models import profile_block_costs
 
     cfg = MODULE_CONFIGS[name]
-    depth = depth or cfg["depth"]
     in_dtype = torch.long if cfg.get("tokens") else torch.float32
     if name not in _COSTS:
         _COSTS[name] = profile_block_costs(make_blocks(cfg["blocks"], cfg["classes"]), cfg["in_shape"], cfg["batch"],
                                            device, in_dtype=in_dtype)
-    costs = _COSTS[name]
+    return _COSTS[name]
+
+
+def module_stages_for(torch, name, device, depth=None, costs=None):
+    from .stage_models import build_module_stages
+
+    cfg = MODULE_CONFIGS[name]
+    depth = depth or cfg["depth"]
+    in_dtype = torch.long if cfg.get("tokens") else torch.float32
+    costs = costs if costs is not None else module_block_costs(torch, name, device)
     torch.manual_seed(0)
     blocks = make_blocks(cfg["blocks"], cfg["classes"])
     return build_module_stages(blocks, depth, device, cfg["in_shape"], costs=costs, in_dtype=in_dtype), costs

@@ -355,11 +355,15 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
                           host_staging: bool = False):
     """Configs 2-4 on `world` GPUs, one stage per GPU (depth = world):
     prediction on vs off, samples/s device-timed, max over ranks."""
-    from .bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
+    from .bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_block_costs, module_stages_for
     from .optim import OptimizerConfig, OptimizerState
     from .runtime import build_timeline
 
     cfg = MODULE_CONFIGS[name]
+    # one partition for every rank: rank 0's profiled costs, broadcast
+    box = [module_block_costs(torch_mod, name, device) if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    costs = box[0]
     torch_mod.backends.cuda.matmul.allow_tf32 = True
     torch_mod.backends.cudnn.allow_tf32 = True
     data = ModuleBatches(torch_mod, device, cfg)
@@ -368,7 +372,7 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
     for strategy in ("async_raw", "optimizer_prediction"):
         times = []
         for trial, n in enumerate((2 * world, n_batches)):
-            stages, _ = module_stages_for(torch_mod, name, device, depth=world)
+            stages, _ = module_stages_for(torch_mod, name, device, depth=world, costs=costs)
             stage = stages[rank]
             for k, st in enumerate(stages):  # only this rank's stage stays on the device
                 if k != rank:
