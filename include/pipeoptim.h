@@ -163,10 +163,10 @@ int po_dp_signal(long long* const* peer_flag_slots, int32_t dp, int64_t epoch, v
 
 /* K3 on this replica's stage with g = (sum over replicas r, in rank order, of
  * grads[r]) / dp read directly from the replicas' (peer-mapped) gradient
- * buffers; every CTA first acquire-waits until flags[r] >= epoch for all r
- * (flags: this replica's local [dp] array that the peers signal into). If a
- * replica has not signalled after timeout_ms the kernel writes *status = 1
- * (device int) and updates nothing. grads_host: HOST array of dp device
+ * buffers, after a one-CTA kernel has acquire-waited until flags[r] >= epoch
+ * for all r (flags: this replica's local [dp] array that the peers signal
+ * into). If a replica has not signalled after timeout_ms, *status = 1 (device
+ * int) and nothing is updated. grads_host: HOST array of dp device
  * pointers. dp <= 8. */
 int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp, float* state1,
                        float* state2, float* w_hat, int64_t n, double lr, double lr_pred_times_s,

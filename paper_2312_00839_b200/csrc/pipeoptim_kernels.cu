@@ -520,8 +520,8 @@ Coef coef(const po_hparams* hp, double lr, double c_pred, int64_t t) {
 // no reduced gradient is written to HBM and read back, no separate collective
 // launch. A replica signals "my gradient of epoch e is complete" with one
 // release store per peer into the peer's flag array (po_dp_signal, enqueued
-// after its backward); the fused kernel's CTAs acquire-spin on their local
-// flags before touching any peer gradient. Gradients are double-buffered by
+// after its backward); a one-CTA kernel acquire-waits on the local flags
+// before the streaming kernel touches any peer gradient. Gradients are double-buffered by
 // epoch parity, which makes a second "consumed" handshake unnecessary: a
 // replica overwrites parity p again only in epoch e+2, after it observed every
 // peer's epoch-(e+1) signal, which each peer issued after its epoch-e update
@@ -546,26 +546,29 @@ __device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
   return v;
 }
 
+// One 32-thread CTA acquire-waits for every replica's signal. It runs BEFORE
+// the streaming kernel (stream order) so the wait occupies one CTA, never the
+// whole GPU: NCCL kernels of the pipeline exchanges keep running beside it
+// (a full-grid spin could starve them and close a dependency cycle across
+// replicas).
+__global__ void po_dp_wait_kernel(const long long* flags, int dp, long long epoch, long long timeout_cycles,
+                                  int* status) {
+  if (threadIdx.x != 0) return;
+  const long long t0 = clock64();
+  for (int r = 0; r < dp; ++r) {
+    while (ld_acquire_sys(flags + r) < epoch) {
+      if (clock64() - t0 > timeout_cycles) {
+        atomicExch(status, 1);
+        return;
+      }
+      __nanosleep(512);
+    }
+  }
+}
+
 template <int KIND, int VEC>
 __global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
-  __shared__ int ok;
-  if (threadIdx.x == 0) {
-    int good = 1;
-    const long long t0 = clock64();
-    for (int r = 0; r < d.dp && good; ++r) {
-      while (ld_acquire_sys(d.flags + r) < d.epoch) {
-        if (clock64() - t0 > d.timeout_cycles) {
-          atomicExch(d.status, 1);
-          good = 0;
-          break;
-        }
-        __nanosleep(256);
-      }
-    }
-    ok = good;
-  }
-  __syncthreads();
-  if (!ok) return;
+  if (*(volatile int*)d.status != 0) return;  // a replica never signalled: update nothing
   const Args& a = d.a;
   const Coef c = load_coef(a);
   const int64_t nv = a.n / VEC;
@@ -813,7 +816,9 @@ int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads
   if (want < 1) want = 1;
   int64_t cap = (int64_t)sm_count() * 8;
   const int64_t grid = want < cap ? want : cap;
-  cudaError_t e;
+  po_dp_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d.flags, dp, d.epoch, d.timeout_cycles, status);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
   switch (hp->kind) {
     case PO_SGDM: e = launch_dp<PO_SGDM>(d, vec, dim3((unsigned)grid), dim3(block), (cudaStream_t)stream); break;
     case PO_ADAM: e = launch_dp<PO_ADAM>(d, vec, dim3((unsigned)grid), dim3(block), (cudaStream_t)stream); break;
