@@ -79,7 +79,8 @@ typedef struct po_launch {
   int32_t ctas_per_sm;  /* persistent grid = SMs * ctas_per_sm, 0 = default */
   int32_t vec;          /* floats per access: 4 (128-bit) or 8 (256-bit), 0 = default */
   int32_t cache;        /* 0 = tuned default, 1 = streaming .cs, 2 = L1::no_allocate
-                           loads, 3 = plain ld/st */
+                           loads, 3 = plain ld/st, 4 = mixed (W / W_hat plain,
+                           gradient and state streaming) */
   int32_t unroll;       /* vectors per stream in flight per thread: 1, 2, 4; 0 = default */
 } po_launch;
 

@@ -184,6 +184,15 @@ __device__ __forceinline__ void vstore(float* p, const Vec<VEC>& r) {
   }
 }
 
+// CACHE 4 = "mixed": the weights and the predicted weights keep normal L2
+// priority (the stage's next GEMMs read them right away — pipeline-sized
+// stages fit in L2), the gradient and the optimizer state stream (.cs: not
+// needed again until the next update). Per-stream policy for each CACHE:
+enum Stream_ : int { S_W = 0, S_G = 1, S_STATE = 2, S_OUT = 3 };
+__host__ __device__ constexpr int pol(int cache, int stream) {
+  return cache == 4 ? ((stream == S_W || stream == S_OUT) ? 0 : 1) : cache;
+}
+
 // ---- the per-element rules --------------------------------------------------
 
 // Adam/AdamW moment-ratio direction (m/bc1) / (sqrt(v/bc2) + eps),
@@ -246,22 +255,22 @@ template <int KIND, int MODE, int VEC, int CACHE>
 __device__ __forceinline__ void do_vec(const Args& a, const Coef& c, int64_t vi, int64_t& bad) {
   const int64_t base = vi * VEC;
   Vec<VEC> w{}, g{}, s1{}, s2{}, out{};
-  if constexpr (uses_w(MODE)) w = vload<VEC, CACHE, !writes_w(MODE)>(a.w + base);
-  if constexpr (uses_g(MODE)) g = vload<VEC, CACHE, true>(a.g + base);
-  if constexpr (uses_s1(MODE)) s1 = vload<VEC, CACHE, !writes_state(MODE)>(a.s1 + base);
-  if constexpr (uses_s2(KIND, MODE)) s2 = vload<VEC, CACHE, !writes_state(MODE)>(a.s2 + base);
+  if constexpr (uses_w(MODE)) w = vload<VEC, pol(CACHE, S_W), !writes_w(MODE)>(a.w + base);
+  if constexpr (uses_g(MODE)) g = vload<VEC, pol(CACHE, S_G), true>(a.g + base);
+  if constexpr (uses_s1(MODE)) s1 = vload<VEC, pol(CACHE, S_STATE), !writes_state(MODE)>(a.s1 + base);
+  if constexpr (uses_s2(KIND, MODE)) s2 = vload<VEC, pol(CACHE, S_STATE), !writes_state(MODE)>(a.s2 + base);
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
     bool e = false;
     elem<KIND, MODE>(c, w.v[j], g.v[j], s1.v[j], s2.v[j], out.v[j], e);
     if (e && bad == INT64_MAX) bad = base + j;
   }
-  if constexpr (writes_w(MODE)) vstore<VEC, CACHE>(a.w + base, w);
+  if constexpr (writes_w(MODE)) vstore<VEC, pol(CACHE, S_W)>(a.w + base, w);
   if constexpr (writes_state(MODE)) {
-    vstore<VEC, CACHE>(a.s1 + base, s1);
-    if constexpr (KIND != PO_SGDM) vstore<VEC, CACHE>(a.s2 + base, s2);
+    vstore<VEC, pol(CACHE, S_STATE)>(a.s1 + base, s1);
+    if constexpr (KIND != PO_SGDM) vstore<VEC, pol(CACHE, S_STATE)>(a.s2 + base, s2);
   }
-  if constexpr (writes_out(MODE)) vstore<VEC, CACHE>(a.out + base, out);
+  if constexpr (writes_out(MODE)) vstore<VEC, pol(CACHE, S_OUT)>(a.out + base, out);
 }
 
 // Persistent grid-stride stream. Each thread issues UNROLL independent vector
@@ -281,10 +290,10 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const int64_t base = (i + u * stride) * VEC;
-      if constexpr (uses_w(MODE)) w[u] = vload<VEC, CACHE, !writes_w(MODE)>(a.w + base);
-      if constexpr (uses_g(MODE)) g[u] = vload<VEC, CACHE, true>(a.g + base);
-      if constexpr (uses_s1(MODE)) s1[u] = vload<VEC, CACHE, !writes_state(MODE)>(a.s1 + base);
-      if constexpr (uses_s2(KIND, MODE)) s2[u] = vload<VEC, CACHE, !writes_state(MODE)>(a.s2 + base);
+      if constexpr (uses_w(MODE)) w[u] = vload<VEC, pol(CACHE, S_W), !writes_w(MODE)>(a.w + base);
+      if constexpr (uses_g(MODE)) g[u] = vload<VEC, pol(CACHE, S_G), true>(a.g + base);
+      if constexpr (uses_s1(MODE)) s1[u] = vload<VEC, pol(CACHE, S_STATE), !writes_state(MODE)>(a.s1 + base);
+      if constexpr (uses_s2(KIND, MODE)) s2[u] = vload<VEC, pol(CACHE, S_STATE), !writes_state(MODE)>(a.s2 + base);
     }
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
@@ -378,6 +387,7 @@ cudaError_t launch_cache(const Args& a, const Shape& sh, dim3 grid, dim3 block, 
     switch (sh.cache) {
       case 0: return launch_unroll<KIND, MODE, VEC, 0>(a, sh, grid, block, s);
       case 2: return launch_unroll<KIND, MODE, VEC, 2>(a, sh, grid, block, s);
+      case 4: return launch_unroll<KIND, MODE, VEC, 4>(a, sh, grid, block, s);
       default: return launch_unroll<KIND, MODE, VEC, 1>(a, sh, grid, block, s);
     }
   } else {
@@ -451,7 +461,7 @@ int run(int kind, int mode, Args a, const po_launch* L, cudaStream_t s) {
   int block = (L && L->block > 0) ? L->block : d.block;
   int cps = (L && L->ctas_per_sm > 0) ? L->ctas_per_sm : d.ctas_per_sm;
   int vec = (L && L->vec > 0) ? L->vec : kDefaultVec;
-  int cache = (L && L->cache > 0 && L->cache <= 2) ? L->cache : d.cache;
+  int cache = (L && L->cache > 0 && L->cache <= 4) ? L->cache : d.cache;
   if (L && L->cache == 3) cache = 0;  // explicit plain ld/st request
   int unroll = (L && L->unroll > 0) ? L->unroll : d.unroll;
   if (block % 32 != 0 || block > 512) return PO_EINVAL;

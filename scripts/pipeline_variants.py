@@ -18,10 +18,11 @@ dev = torch.device("cuda", 0)
 data = DeviceBatches(torch, dev)
 n = 64
 variants = {"default": None}
-for block, cps, unroll in ((128, 16, 1), (512, 1, 1), (256, 8, 1)):
-    for cache in (1, 3):
+for block, cps, unroll in ((128, 16, 1), (256, 8, 1)):
+    for cache in (1, 4):
         variants[f"{block}x{cps}u{unroll}c{cache}"] = (block, cps, 8, cache, unroll)
 for tf32 in (False, True):
+    torch.cuda.empty_cache()
     torch.backends.cuda.matmul.allow_tf32 = tf32
     for name, la in variants.items():
         res = {}

@@ -202,7 +202,7 @@ def test_fused_equals_unfused_bitwise(lib, kind):
 
 
 @pytest.mark.parametrize("vec", [1, 4, 8])
-@pytest.mark.parametrize("cache", [1, 2, 3])
+@pytest.mark.parametrize("cache", [1, 2, 3, 4])
 @pytest.mark.parametrize("unroll", [1, 2, 4])
 def test_launch_shapes_bit_identical(lib, vec, cache, unroll):
     """Every launch shape computes the same bits (the arithmetic is shape-free)."""
