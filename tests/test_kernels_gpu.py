@@ -338,3 +338,47 @@ def test_fused_loss_grad_matches_reference_formulas(kind, rows, cols):
         want_loss, want_grad = runtime_ref.loss_and_grad(pred.astype(np.float64), tgt.astype(np.float64), kind)
         assert abs(float(loss) - want_loss) <= 1e-5 * abs(want_loss) + 1e-7
         assert R.inf_norm_rel(host(grad), want_grad) <= 2e-6
+
+
+def test_more_than_2_31_elements(lib):
+    """64-bit indexing: a 2^31 + 13 element stage (8 GB per buffer); K3 checked
+    bit-exact against the fp32 emulation on the first and last 2^20 elements."""
+    import torch
+
+    n = (1 << 31) + 13
+    free, _ = torch.cuda.mem_get_info()
+    if free < 6 * 4 * n:
+        pytest.skip("not enough device memory")
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    w = torch.randn(n, device="cuda", generator=gen) * 0.02
+    g = torch.randn(n, device="cuda", generator=gen) * 0.01
+    m = torch.randn(n, device="cuda", generator=gen) * 1e-3
+    v = (torch.randn(n, device="cuda", generator=gen) * 1e-2).square_()
+    out = torch.empty(n, device="cuda")
+    k = 1 << 20
+    heads = [x[:k].cpu().numpy() for x in (w, g, m, v)]
+    tails = [x[-k:].cpu().numpy() for x in (w, g, m, v)]
+    assert lib.po_step_predict(ctypes.byref(hp("adam")), w.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(),
+                               out.data_ptr(), n, 1e-3, 3e-3, 7, None, None, stream()) == 0
+    for sl, src in ((slice(0, k), heads), (slice(n - k, n), tails)):
+        ew, _, _, ewh = F.step("adam", *src, 1e-3, 7, c_pred=3e-3)
+        assert np.array_equal(w[sl].cpu().numpy(), ew)
+        assert np.array_equal(out[sl].cpu().numpy(), ewh)
+    del w, g, m, v, out
+    torch.cuda.empty_cache()
+
+
+def test_empty_and_tiny_buffers(lib):
+    import torch
+
+    H = ctypes.byref(hp("sgdm"))
+    assert lib.po_step_predict(H, None, None, None, None, None, 0, 1e-3, 1e-3, 0, None, None, stream()) == 0
+    assert lib.po_predict(H, None, None, None, None, 0, 1e-3, 3, None, stream()) == 0
+    for n in (1, 2, 3, 8, 9, 31):  # shorter than one vector / one warp
+        w, g, s1, s2 = make_inputs("sgdm", n, 2, seed=n)
+        dw, dg, d1 = dev(w), dev(g), dev(s1)
+        out = torch.empty(n, device="cuda")
+        assert lib.po_step_predict(H, dw.data_ptr(), dg.data_ptr(), d1.data_ptr(), None, out.data_ptr(), n, 1e-3,
+                                   2e-3, 2, None, None, stream()) == 0
+        ew, _, _, ewh = F.step("sgdm", w, g, s1, s2, 1e-3, 2, c_pred=2e-3)
+        assert np.array_equal(f32(dw), ew) and np.array_equal(f32(out), ewh)
