@@ -340,7 +340,7 @@ class OptimizerState:
         self._bind(flat.layout)
         self._ensure_state()
         if self.tape is not None:
-            slot = self.tape.record(self, _lib.PO_COEF_STEP, lr, 0.0)
+            slot = self.tape.record(self, _lib.PO_COEF_STEP, lr, 0.0, 0)
             rc = self._lib.po_step_dc(
                 ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1), _ptr(self._s2),
                 flat.layout.numel, slot, _ptr(self._bad), self._launch_ref(), _stream(flat.data.device),
@@ -365,7 +365,7 @@ class OptimizerState:
         if self.step_count > 0 or self.tape is not None:
             self._ensure_state()
         if self.tape is not None:
-            slot = self.tape.record(self, _lib.PO_COEF_PREDICT, 0.0, float(lr) * steps_ahead)
+            slot = self.tape.record(self, _lib.PO_COEF_PREDICT, 0.0, lr, steps_ahead)
             rc = self._lib.po_predict_dc(
                 ctypes.byref(self._hp), _ptr(flat.data), _ptr(self._s1), _ptr(self._s2), _ptr(out),
                 flat.layout.numel, slot, self._launch_ref(), _stream(flat.data.device),
@@ -388,7 +388,7 @@ class OptimizerState:
         self._bind(flat.layout)
         self._ensure_state()
         if self.tape is not None:
-            slot = self.tape.record(self, _lib.PO_COEF_STEP_PREDICT, lr, float(lr_pred) * steps_ahead)
+            slot = self.tape.record(self, _lib.PO_COEF_STEP_PREDICT, lr, lr_pred, steps_ahead)
             rc = self._lib.po_step_predict_dc(
                 ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1), _ptr(self._s2),
                 _ptr(out), flat.layout.numel, slot, _ptr(self._bad), self._launch_ref(),
@@ -503,23 +503,37 @@ class CoefTape:
         for o in opts:
             o.tape = None
 
-    def record(self, opt, which: int, lr: float, lr_times_s: float) -> int:
+    def record(self, opt, which: int, lr, lr_pred, steps_ahead: int) -> int:
+        """One launch's slot. `lr` / `lr_pred` may be `MbLr` values (a float
+        that remembers the mini-batch it was computed for), in which case
+        refresh() re-evaluates the learning-rate schedule for every replay."""
         i = len(self.entries)
         if i >= self.capacity:
             raise RuntimeError("CoefTape capacity exceeded")
-        self.entries.append((opt, which, opt.step_count - self.base[id(opt)], float(lr), float(lr_times_s)))
+        self.entries.append((opt, which, opt.step_count - self.base[id(opt)], lr, lr_pred, int(steps_ahead)))
         return self.dev.data_ptr() + 16 * i
 
-    def refresh(self, step_counts: dict[int, int], stream=None) -> None:
-        """Fill every slot for the optimizers' step counts at replay start."""
+    @staticmethod
+    def _lr(value, lr_fn, mb_offset):
+        mb = getattr(value, "mb", None)
+        if lr_fn is None or mb is None:
+            return float(value)
+        return float(lr_fn(mb_offset + mb))
+
+    def refresh(self, step_counts: dict[int, int], lr_fn=None, mb_offset: int = 0) -> None:
+        """Fill every slot for the optimizers' step counts at replay start (and,
+        with `lr_fn`, the schedule's learning rate at global mini-batch
+        mb_offset + mb), in double on the host exactly as the eager calls."""
         k = self.flip
         self.flip ^= 1
         if self.copied[k] is not None:
             self.copied[k].synchronize()
         host = self.host[k]
         buf = (_lib.po_coef * self.capacity).from_address(host.data_ptr())
-        for i, (opt, which, rel, lr, c) in enumerate(self.entries):
-            rc = self._lib.po_coef_fill(ctypes.byref(opt._hp), which, lr, c, step_counts[id(opt)] + rel,
+        for i, (opt, which, rel, lr, lr_pred, s) in enumerate(self.entries):
+            a = self._lr(lr, lr_fn, mb_offset)
+            c = self._lr(lr_pred, lr_fn, mb_offset) * s
+            rc = self._lib.po_coef_fill(ctypes.byref(opt._hp), which, a, c, step_counts[id(opt)] + rel,
                                         ctypes.addressof(buf[i]))
             _lib.check(rc, "po_coef_fill")
         n = 4 * len(self.entries)
@@ -528,6 +542,16 @@ class CoefTape:
             ev = torch.cuda.Event()
             ev.record()
             self.copied[k] = ev
+
+
+class MbLr(float):
+    """A learning rate that remembers the (run-local) mini-batch it is for, so a
+    CUDA-graph replay can re-evaluate the schedule (CoefTape.refresh)."""
+
+    def __new__(cls, value, mb):
+        obj = super().__new__(cls, value)
+        obj.mb = mb
+        return obj
 
 
 class HostStreamer:

@@ -241,7 +241,8 @@ def test_execute_rejects_bad_inputs():
                                            ("async_raw", "adamw")])
 def test_graph_replays_continue_training_like_eager_runs(strategy, kind):
     """GraphedExecute: warm-up eager run + 2 replays == 3 eager runs (each a full
-    run of the timeline from the current state); coefficients advance."""
+    run of the timeline from the current state); bias corrections and a
+    run-spanning learning-rate schedule advance between replays."""
     import torch
 
     from paper_2312_00839_b200.bench_pipeline import DeviceBatches
@@ -258,15 +259,18 @@ def test_graph_replays_continue_training_like_eager_runs(strategy, kind):
         stages = build_stages(build_layers(dims, acts), 4, torch_init(3, dev), device=dev)
         return stages, [OptimizerState(OptimizerConfig(kind), s.param_names, device=dev) for s in stages]
 
+    def sched(mb):  # a step-decay schedule spanning the runs
+        return 1e-3 * 0.8 ** ((mb - 1) // 4)
+
     sa, oa = setup()
     eager_losses = []
-    for _ in range(3):
+    for run in range(3):
         for s in sa:
             s.version = 1
-        eager_losses.append(execute(tl, sa, oa, strategy, data, "softmax_xent", lambda mb: 1e-3,
-                                    checks="deferred").losses)
+        eager_losses.append(execute(tl, sa, oa, strategy, data, "softmax_xent",
+                                    lambda mb, r=run: sched(r * tl.n_batches + mb), checks="deferred").losses)
     sb, ob = setup()
-    g = GraphedExecute(tl, sb, ob, strategy, data, "softmax_xent", lambda mb: 1e-3, warmup_runs=1)
+    g = GraphedExecute(tl, sb, ob, strategy, data, "softmax_xent", sched, warmup_runs=1, schedule_spans_runs=True)
     graph_losses = []
     for _ in range(2):
         g.replay()
