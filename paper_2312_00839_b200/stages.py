@@ -334,15 +334,17 @@ def loss_and_grad(pred: torch.Tensor, target: torch.Tensor, kind: str):
         p = pred if pred.is_contiguous() else pred.contiguous()
         t = target.to(torch.float32)
         t = t if t.is_contiguous() else t.contiguous()
-        key = (pred.device, rows)
+        stream = torch.cuda.current_stream(pred.device).cuda_stream
+        # scratch (row partials + the last-CTA counter) per device, row count
+        # and stream: launches on different streams must not share a counter
+        key = (pred.device, rows, stream)
         if key not in _LOSS_SCRATCH:
             _LOSS_SCRATCH[key] = torch.zeros(rows + 1, dtype=torch.float32, device=pred.device)
         grad = torch.empty_like(p)
         loss = torch.empty((), dtype=torch.float32, device=pred.device)
         code = _lib.PO_LOSS_MSE if kind == "mse" else _lib.PO_LOSS_SOFTMAX_XENT
         rc = _lib.load().po_loss_grad(code, p.data_ptr(), t.data_ptr(), rows, cols, grad.data_ptr(),
-                                      loss.data_ptr(), _LOSS_SCRATCH[key].data_ptr(),
-                                      torch.cuda.current_stream(pred.device).cuda_stream)
+                                      loss.data_ptr(), _LOSS_SCRATCH[key].data_ptr(), stream)
         _lib.check(rc, "po_loss_grad")
         return loss, grad
     if kind == "mse":
