@@ -103,13 +103,194 @@ class _Exchange:
         self.inflight.clear()
 
 
+class _SlotTape:
+    """A one-slot coefficient tape: graph-captured optimizer launches read
+    their scalars from one device po_coef that is refilled (host double
+    arithmetic, po_coef_fill) before each replay. The pinned staging is a ring
+    so the host never overwrites a slot whose H2D copy may still be pending."""
+
+    RING = 8
+
+    def __init__(self, device):
+        from . import _lib
+
+        self._lib = _lib
+        self.dev = torch.zeros(4, dtype=torch.float32, device=device)
+        self.host = torch.zeros(self.RING * 4, dtype=torch.float32).pin_memory()
+        self.done = [None] * self.RING
+        self.k = 0
+
+    def record(self, opt, which, lr, lr_pred, steps_ahead):
+        return self.dev.data_ptr()
+
+    def fill(self, opt, which, lr, lr_times_s):
+        import ctypes
+
+        k = self.k
+        self.k = (k + 1) % self.RING
+        if self.done[k] is not None:
+            self.done[k].synchronize()
+        host = self.host[4 * k : 4 * k + 4]
+        rc = self._lib.load().po_coef_fill(ctypes.byref(opt._hp), which, float(lr), float(lr_times_s),
+                                           opt.step_count, host.data_ptr())
+        self._lib.check(rc, "po_coef_fill")
+        self.dev.copy_(host, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.done[k] = ev
+
+
+class _OpGraphs:
+    """Per-(op kind, stash slot) CUDA graphs of one rank's stage work.
+
+    The first occurrence of an op in a slot runs eagerly (it also warms
+    cuBLAS on the stream), the second is captured and replayed, later ones
+    replay. Every cross-op tensor lives at a static address: receive buffers
+    per slot, the forward's stash / output / loss per slot (graph pool), the
+    live and staging weights, the flat gradient. Slots are mb mod D (at most
+    D - k mini-batches are in flight on stage k). Optimizer updates replay a
+    K2 or K3 graph whose scalars come from a _SlotTape refilled on the host
+    before each replay.
+    """
+
+    def __init__(self, runner: "PipelineStageRunner"):
+        self.r = runner
+        self.slots = runner.depth
+        self.count: dict = {}
+        self.graphs: dict = {}
+        self.recv: dict = {}
+        self.xbuf: dict = {}
+        self.ybuf: dict = {}
+        self.sends: dict = {}
+        self.tape = _SlotTape(runner.device)
+
+    def _slot(self, mb):
+        return mb % self.slots
+
+    def recv_buffer(self, op, shape):
+        key = (op.kind, self._slot(op.mb))
+        buf = self.recv.get(key)
+        if buf is None or tuple(buf.shape) != tuple(shape):
+            buf = self.recv[key] = torch.empty(shape, dtype=torch.float32, device=self.r.device)
+        return buf
+
+    def _static(self, table, slot, t):
+        buf = table.get(slot)
+        if buf is None or buf.shape != t.shape:
+            buf = table[slot] = torch.empty_like(t)
+        buf.copy_(t)
+        return buf
+
+    def _run(self, key, fn):
+        """Eager on the first occurrence, capture + replay on the second,
+        replay afterwards. Returns fn's outputs (graph-owned when captured)."""
+        n = self.count.get(key, 0)
+        self.count[key] = n + 1
+        if n == 0:
+            return fn()
+        if n == 1:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                outs = fn()
+            self.graphs[key] = (graph, outs)
+        graph, outs = self.graphs[key]
+        graph.replay()
+        return outs
+
+    def _wait_send(self, key):
+        for w in self.sends.pop(key, []):
+            w.wait()
+
+    def sent(self, op, reqs):
+        self.sends[(op.kind, self._slot(op.mb))] = list(reqs)
+
+    def forward(self, op, weights, x, y, fv, flags, flag_base):
+        r, slot = self.r, self._slot(op.mb)
+        st = r.stage
+        self._wait_send((op.kind, slot))  # the slot's previous output must have left
+        if r.rank == 0:
+            x = self._static(self.xbuf, slot, x)
+        if y is not None:
+            y = self._static(self.ybuf, slot, y)
+        last = r.rank == r.depth - 1
+
+        def fn():
+            out = st.run_forward(weights, ("slot", slot), x, fv, check_finite=False, finite_flags=flags,
+                                 flag_index=flag_base + slot)
+            if last:
+                loss, grad = loss_and_grad(out, y, r.loss_kind)
+                return out, loss, grad
+            return out, None, None
+
+        return self._run(("F", slot, weights[0].data_ptr()), fn)
+
+    def backward(self, op, weights, g_out):
+        r, slot = self.r, self._slot(op.mb)
+        self._wait_send((op.kind, slot))
+
+        def fn():
+            g_in, _ = r.stage.run_backward(weights, ("slot", slot), g_out, accumulate=False,
+                                           need_input_grad=r.rank > 0)
+            return g_in
+
+        return self._run(("B", slot), fn)
+
+    def update(self, op):
+        from . import _lib
+
+        r = self.r
+        lr = r.lr_for_mb(op.mb)
+        fused = r.fuse and op.fuse_predict
+        key = ("U", fused)
+        first = self.count.get(key, 0) == 0
+        if fused:
+            lr_p, gap = r.lr_for_mb(op.next_mb), op.next_gap
+            r.rt.staging_buffer()
+
+            def fn():
+                r.opt.step_predict_(r.stage.flat, lr, lr_p, gap, r.rt.staging)
+
+            which, c = _lib.PO_COEF_STEP_PREDICT, float(lr_p) * gap
+        else:
+
+            def fn():
+                r.opt.step_(r.stage.flat, lr)
+
+            which, c = _lib.PO_COEF_STEP, 0.0
+        if first:
+            fn()  # eager (advances step_count itself)
+            self.count[key] = 1
+        else:
+            if self.count[key] == 1:  # capture with the slot tape; nothing runs during capture
+                r.opt._ensure_state()
+                sc = r.opt.step_count
+                r.opt.tape = self.tape
+                graph = torch.cuda.CUDAGraph()
+                try:
+                    with torch.cuda.graph(graph):
+                        fn()
+                finally:
+                    r.opt.tape = None
+                    r.opt.step_count = sc
+                self.graphs[key] = (graph, None)
+                self.count[key] = 2
+            self.tape.fill(r.opt, which, lr, c)
+            self.graphs[key][0].replay()
+            r.opt.step_count += 1
+        if fused:
+            r.rt.prepared = (op.next_mb, op.next_gap)
+        r.stage.version += 1
+        r.rt.pending_count = 0
+        r.policy.after_update(r.rt)
+
+
 class PipelineStageRunner:
     """Runs one stage's 1F1B program on this rank."""
 
     def __init__(self, dist, tl: Timeline, stage: StageModel, opt, strategy: str, data, loss_kind: str,
                  lr_for_mb, rows: int, *, checks: str = "deferred", fuse: bool = True, group=None,
                  stage_ranks: list[int] | None = None, dp_group=None, dp_rank: int = 0, dp_size: int = 1,
-                 host_staging: bool = False, fused_dp=None):
+                 host_staging: bool = False, fused_dp=None, graphed: bool = False):
         """stage_ranks[k] is the global rank holding stage k of this pipeline
         replica (default: rank k). With dp_size > 1 (hybrid DP x PP), replica
         `dp_rank` trains on rows [dp_rank*rows, (dp_rank+1)*rows) of every
@@ -148,6 +329,13 @@ class PipelineStageRunner:
             stage.set_grad_buffer(fused_dp.grad)
             self._scratch = None
         opt.eager_checks = self.eager
+        # graphed=True: every op's device work is captured once per (kind,
+        # stash slot) into a CUDA graph and replayed (the eager per-op Python
+        # cost dominates small stages); needs deferred checks, an MLP stage
+        # and no data parallelism (those paths run eagerly)
+        use_graphs = (graphed and not self.eager and dp_size == 1 and isinstance(stage, StageModel)
+                      and self.device.type == "cuda")
+        self._graphs = _OpGraphs(self) if use_graphs else None
 
     # -- what each op consumes / produces -------------------------------------------------
 
@@ -166,14 +354,18 @@ class PipelineStageRunner:
         grads_local: dict[int, torch.Tensor] = {}
         snapshot_peak = 1
         executed = []
-        flags = torch.ones(len(work), dtype=torch.bool, device=self.device)
+        g = self._graphs
+        # finiteness flags: one per eager forward (by work index), one per
+        # graphed slot (po_all_finite only ever clears a flag)
+        flags = torch.ones(len(work) + (g.slots if g else 0), dtype=torch.bool, device=self.device)
+        in_flight = peak_in_flight = 0
         t0 = time.perf_counter()
 
         def post_recv(op):
             spec = self._input_spec(op)
             if spec is None:
                 return None, []
-            buf = torch.empty(spec[0], dtype=torch.float32, device=self.device)
+            buf = g.recv_buffer(op, spec[0]) if g else torch.empty(spec[0], dtype=torch.float32, device=self.device)
             return buf, [(buf, spec[1])]
 
         nxt_buf, recv = post_recv(work[0]) if work else (None, [])
@@ -185,7 +377,10 @@ class PipelineStageRunner:
             i += 1
             executed.append((op.kind, op.mb))
             if op.kind == UPDATE:
-                self._update(op)
+                if g is not None:
+                    g.update(op)
+                else:
+                    self._update(op)
                 snapshot_peak = max(snapshot_peak, self.policy.snapshot_count(self.rt))
                 continue
             inp, req = nxt_buf, nxt_req
@@ -193,37 +388,52 @@ class PipelineStageRunner:
                 r.wait()
             out_msg = None
             if op.kind == FORWARD:
+                x = inp
+                y = None
+                last = self.rank == self.depth - 1
                 if self.rank == 0:
-                    inp = self._shard(_to_device(self.data.batch(op.mb)[0], self.device))
+                    x = self._shard(_to_device(self.data.batch(op.mb)[0], self.device))
+                if last:
+                    y = self._shard(_to_device(self.data.batch(op.mb)[1], self.device))
                 weights, fv, predicted, target = self.policy.forward_view(self.rt, op.mb, 0, self.lr_for_mb(op.mb))
                 try:
-                    out = self.stage.run_forward(weights, (op.mb, 0), inp, fv, check_finite=self.eager,
-                                                 finite_flags=flags, flag_index=wi)
+                    if g is not None:
+                        out, loss, grad = g.forward(op, weights, x, y, fv, flags, len(work))
+                    else:
+                        out = self.stage.run_forward(weights, (op.mb, 0), x, fv, check_finite=self.eager,
+                                                     finite_flags=flags, flag_index=wi)
+                        loss = grad = None
+                        if last:
+                            loss, grad = loss_and_grad(out, y, self.loss_kind)
                 except NumericError as err:
                     raise NumericError(f"mb {op.mb} stage {self.rank}: {err}") from err
+                in_flight += 1
+                peak_in_flight = max(peak_in_flight, in_flight)
                 rec = VersionRecord(op.mb, 0, self.rank, fv, predicted, target)
                 records[op.mb] = rec
                 order.append(rec)
-                if self.rank < self.depth - 1:
-                    out_msg = (out.contiguous(), self.stage_ranks[self.rank + 1])
+                if not last:
+                    out_msg = (out if out.is_contiguous() else out.contiguous(), self.stage_ranks[self.rank + 1])
                 else:
-                    y = self._shard(_to_device(self.data.batch(op.mb)[1], self.device))
-                    loss, g = loss_and_grad(out, y, self.loss_kind)
                     if self.eager and not bool(torch.isfinite(loss)):
                         raise NumericError(f"mb {op.mb} stage {self.rank}: non-finite loss under {self.loss_kind}")
-                    losses[op.mb] = loss.detach()
-                    grads_local[op.mb] = g
+                    losses[op.mb] = loss.detach().clone() if g is not None else loss.detach()
+                    grads_local[op.mb] = grad
             else:
                 g_out = grads_local.pop(op.mb) if self.rank == self.depth - 1 else inp
                 rec = records[op.mb]
                 weights, bv = self.policy.backward_view(self.rt, op.mb, 0, rec.forward_version)
-                g_in, _ = self.stage.run_backward(weights, (op.mb, 0), g_out, accumulate=False,
-                                                  need_input_grad=self.rank > 0)
+                if g is not None:
+                    g_in = g.backward(op, weights, g_out)
+                else:
+                    g_in, _ = self.stage.run_backward(weights, (op.mb, 0), g_out, accumulate=False,
+                                                      need_input_grad=self.rank > 0)
+                in_flight -= 1
                 self.rt.pending_count = 1
                 rec.backward_version = bv
                 rec.live_backward_version = self.stage.version
                 if self.rank > 0:
-                    out_msg = (g_in.contiguous(), self.stage_ranks[self.rank - 1])
+                    out_msg = (g_in if g_in.is_contiguous() else g_in.contiguous(), self.stage_ranks[self.rank - 1])
             snapshot_peak = max(snapshot_peak, self.policy.snapshot_count(self.rt))
             wi += 1
             # one grouped exchange: this op's output + the next work op's input
@@ -232,13 +442,16 @@ class PipelineStageRunner:
             else:
                 nxt_buf, recv = None, []
             nxt_req = self.comm.post([out_msg] if out_msg else [], recv)
+            if g is not None and out_msg is not None:
+                g.sent(op, nxt_req)
         self.comm.drain()
         if self.fused_dp is not None:
             self.fused_dp.check()
         if not self.eager:
             if not bool(flags.all()):
                 bad = int((~flags).nonzero()[0].item())
-                raise NumericError(f"mb {work[bad].mb} stage {self.rank}: non-finite value in stage forward output")
+                where = f"mb {work[bad].mb}" if bad < len(work) else f"mb slot {bad - len(work)} (graphed)"
+                raise NumericError(f"{where} stage {self.rank}: non-finite value in stage forward output")
             self.opt.check_finite()
         host_losses = None
         if losses is not None:
@@ -248,7 +461,8 @@ class PipelineStageRunner:
                 raise NumericError(f"stage {self.rank}: non-finite loss under {self.loss_kind}")
         if self.stage.version != self.tl.n_batches + 1 or len(self.stage.stash):
             raise RuntimeError(f"stage {self.rank} did not drain: version {self.stage.version}")
-        return StageReport(self.rank, order, host_losses, self.stage.version, self.stage.stash.peak,
+        stash_peak = max(self.stage.stash.peak, peak_in_flight)
+        return StageReport(self.rank, order, host_losses, self.stage.version, stash_peak,
                            snapshot_peak, time.perf_counter() - t0, executed)
 
     def _shard(self, t):
@@ -323,31 +537,34 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
     data = DeviceBatches(torch_mod, device, dims=dims)
     out = {"config": f"MLP {dims}, B={BATCH}, Adam lr 1e-4, 1F1B D={world} (one stage per GPU, NCCL P2P), "
                      f"{n_batches} mini-batches, fp32 GEMMs"}
-    for strategy in ("async_raw", "optimizer_prediction"):
-        times = []
-        for trial in range(2):  # trial 0 warms NCCL / cuBLAS
-            group = partition_layers(layers, world)[rank]
-            stage = StageModel(rank, group, torch_init(0, device), device)
-            opt = OptimizerState(OptimizerConfig("adam"), stage.param_names, device=device)
-            tl = build_timeline(strategy, world, n_batches if trial else 2 * world + 2)
-            runner = PipelineStageRunner(dist, tl, stage, opt, strategy, data, "softmax_xent", lambda mb: 1e-4,
-                                         BATCH, host_staging=host_staging)
-            torch_mod.cuda.synchronize(device)
-            dist.barrier()
-            e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
-            e0.record()
-            runner.run()
-            e1.record()
-            torch_mod.cuda.synchronize(device)
-            dist.barrier()
-            times.append(e0.elapsed_time(e1) / 1e3)
-        t = torch_mod.tensor([times[-1]], device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
-        out[key] = {"samples_per_s": round(n_batches * BATCH / float(t.item()), 1), "s": round(float(t.item()), 4)}
+    for graphed in (False, True):
+        for strategy in ("async_raw", "optimizer_prediction"):
+            times = []
+            for trial in range(2):  # trial 0 warms NCCL / cuBLAS
+                group = partition_layers(layers, world)[rank]
+                stage = StageModel(rank, group, torch_init(0, device), device)
+                opt = OptimizerState(OptimizerConfig("adam"), stage.param_names, device=device)
+                tl = build_timeline(strategy, world, n_batches if trial else 2 * world + 2)
+                runner = PipelineStageRunner(dist, tl, stage, opt, strategy, data, "softmax_xent", lambda mb: 1e-4,
+                                             BATCH, host_staging=host_staging, graphed=graphed)
+                torch_mod.cuda.synchronize(device)
+                dist.barrier()
+                e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
+                e0.record()
+                runner.run()
+                e1.record()
+                torch_mod.cuda.synchronize(device)
+                dist.barrier()
+                times.append(e0.elapsed_time(e1) / 1e3)
+            t = torch_mod.tensor([times[-1]], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            key = ("graphed_" if graphed else "") + ("pred_on" if strategy == "optimizer_prediction" else "pred_off")
+            out[key] = {"samples_per_s": round(n_batches * BATCH / float(t.item()), 1),
+                        "s": round(float(t.item()), 4)}
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
-    out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4),
-               launches=n_batches * 2)
+    gon, goff = out["graphed_pred_on"]["samples_per_s"], out["graphed_pred_off"]["samples_per_s"]
+    out.update(value=max(on, gon), unit="samples/s", prediction_overhead=round(1.0 - on / off, 4),
+               graphed_prediction_overhead=round(1.0 - gon / goff, 4), launches=n_batches * 2)
     return out
 
 

@@ -26,7 +26,7 @@ class Src:
         return s.normal(8, DIMS[0]), s.normal(8, DIMS[-1])
 
 
-def _worker(rank, world, port, strategy, kind, n, out_dir):
+def _worker(rank, world, port, strategy, kind, n, out_dir, graphed=False):
     import torch
     import torch.distributed as dist
 
@@ -46,7 +46,8 @@ def _worker(rank, world, port, strategy, kind, n, out_dir):
         opt = OptimizerState(OptimizerConfig(kind, **kw), stage.param_names, device=dev)
         tl = build_timeline(strategy, world, n)
         runner = PipelineStageRunner(dist, tl, stage, opt, strategy, Src(), "mse", lambda mb: 0.01, 8,
-                                     host_staging=True)
+                                     host_staging=True, checks="deferred", graphed=graphed)
+        assert (runner._graphs is not None) == graphed
         rep = runner.run()
         reps = gather_reports(dist, rep, world)
         if rank == 0:
@@ -69,11 +70,14 @@ def _port():
 
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("async_raw", "sgdm")])
-def test_multiprocess_runner_with_device_kernels(tmp_path, world, strategy, kind):
+@pytest.mark.parametrize("graphed", [False, True])
+def test_multiprocess_runner_with_device_kernels(tmp_path, world, strategy, kind, graphed):
+    """graphed=True: every op's device work replayed from per-(kind, slot)
+    CUDA graphs, optimizer scalars from the slot tape — same numbers."""
     import torch.multiprocessing as mp
 
-    n = 2 * world + 5
-    mp.spawn(_worker, args=(world, _port(), strategy, kind, n, str(tmp_path)), nprocs=world, join=True)
+    n = 3 * world + 5  # enough mini-batches that every slot is captured and replayed
+    mp.spawn(_worker, args=(world, _port(), strategy, kind, n, str(tmp_path), graphed), nprocs=world, join=True)
     got = json.loads((tmp_path / "out.json").read_text())
     ref = runtime_ref.run(DIMS, ACTS, world, n, strategy, optim_ref.Hyper(kind, weight_decay=0.0), Src().batch,
                           "mse", lambda mb: 0.01, lambda i, a, b: rng_ref.layer_init(3, i, a, b))
