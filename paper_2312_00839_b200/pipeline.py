@@ -54,11 +54,15 @@ class _StagedRecv:
 
     def __init__(self, reqs, host, dev):
         self.reqs, self.host, self.dev = reqs, host, dev
+        self.done = False
 
     def wait(self):
+        if self.done:  # idempotent: a second wait must not re-copy stale data
+            return
         for r in self.reqs:
             r.wait()
         self.dev.copy_(self.host)
+        self.done = True
 
     def is_completed(self):
         return all(r.is_completed() for r in self.reqs)
