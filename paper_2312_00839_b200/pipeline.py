@@ -49,6 +49,26 @@ class StageReport:
     executed: list
 
 
+class _Req:
+    """A communication request whose wait() may be called more than once: a
+    gloo send's wait consumes its completion, so a second wait (the run loop
+    waits every posted request before the next op; the graphed runner waits a
+    slot's previous send again before overwriting its buffer) would block."""
+
+    __slots__ = ("work", "done")
+
+    def __init__(self, work):
+        self.work, self.done = work, False
+
+    def wait(self):
+        if not self.done:
+            self.work.wait()
+            self.done = True
+
+    def is_completed(self):
+        return self.done or self.work.is_completed()
+
+
 class _StagedRecv:
     """Completion handle of a host-staged receive: wait(), then copy to device."""
 
@@ -94,7 +114,7 @@ class _Exchange:
         ops += [d.P2POp(d.irecv, b, peer, self.group) for b, peer in recvs]
         if not ops:
             return []
-        reqs = d.batch_isend_irecv(ops)
+        reqs = [_Req(w) for w in d.batch_isend_irecv(ops)]
         self.inflight.append((reqs, [t for t, _ in sends]))
         if self.host_staging and staged:
             return [_StagedRecv(reqs, staged[0][0], staged[0][1])]
