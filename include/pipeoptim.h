@@ -193,6 +193,26 @@ int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void
 int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t rows, int64_t cols, float* grad,
                  float* loss, float* scratch, void* stream);
 
+/* ---- live-weight LSTM cell (pipeoptim_lstm.cu) --------------------------
+ * One time step of an LSTM layer whose GEMMs run in cuBLAS (PyTorch gate
+ * order i, f, g, o; hidden % 4 == 0; all pointers 16-byte aligned). Used by
+ * the GNMT stages so the backward can multiply by the LIVE weights
+ * (stages.py:200-208 semantics, S9) — cuDNN keeps the forward weights. */
+
+/* gates [batch x 4*hidden]: pre-activations in, activations out (in place).
+ * c_prev (NULL = zeros), c_out, h_out: [batch x hidden]. y_out (nullable):
+ * a second copy of h_t with row stride y_ld (the batch-first layer output). */
+int po_lstm_cell_fwd(float* gates, const float* c_prev, float* c_out, float* h_out, float* y_out, int64_t y_ld,
+                     int64_t batch, int64_t hidden, void* stream);
+
+/* act: the forward's activations [batch x 4*hidden]; c_prev (NULL = zeros),
+ * c: [batch x hidden]; dy (nullable, row stride dy_ld): the output gradient
+ * at this step; dh_rec (nullable): dgates_{t+1} W_hh (the recurrent
+ * gradient); dc: in = dc_t from step t+1 (zeros at t = T-1), out = dc_{t-1}.
+ * dgates [batch x 4*hidden] receives the pre-activation gradients. */
+int po_lstm_cell_bwd(const float* act, const float* c_prev, const float* c, const float* dy, int64_t dy_ld,
+                     const float* dh_rec, float* dc, float* dgates, int64_t batch, int64_t hidden, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

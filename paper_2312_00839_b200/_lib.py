@@ -35,6 +35,8 @@ EXPORTS = (
     "po_loss_grad",
     "po_dp_signal",
     "po_step_predict_dp",
+    "po_lstm_cell_fwd",
+    "po_lstm_cell_bwd",
 )
 
 PO_LOSS_MSE, PO_LOSS_SOFTMAX_XENT = 0, 1
@@ -102,6 +104,8 @@ _SIGNATURES = {
     "po_dp_signal": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _P]),
     "po_step_predict_dp": (ctypes.c_int, [_HP, _P, _P, ctypes.c_int32, _P, _P, _P, _I64, _D, _D, _I64, _P, _P, _I64,
                                           _I64, _P, _P]),
+    "po_lstm_cell_fwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
+    "po_lstm_cell_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _I64, _I64, _P]),
 }
 
 _lock = threading.Lock()

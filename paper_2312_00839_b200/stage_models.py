@@ -23,10 +23,13 @@ deviation the reference cannot pin, it has no LSTM.)
 
 from __future__ import annotations
 
+import math
+
 import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
+from . import _lib
 from .errors import NumericError
 from .optim import FlatParams
 from .stages import ActivationStash, StashEntry, record_finite
@@ -97,10 +100,109 @@ def resnet101_blocks(num_classes: int = 200) -> list[nn.Module]:
     return blocks
 
 
+class _LiveLSTMFn(torch.autograd.Function):
+    """One batch-first LSTM layer (PyTorch gate order i, f, g, o) with the
+    reference's stage semantics (stages.py:187-209, S9): the forward runs on
+    the weights it is given (W_hat for a predicted stage) and stashes its
+    activations; the backward forms dW from those activations and propagates
+    dx / dh through the LIVE weights (the module's parameters at backward
+    time), exactly as the MLP stage's `g = dpre W_live^T`.
+
+    Layout: time-major inside (x^T (T, B, Din), gates (T, B, 4H), h (T+1, B, H),
+    c (T, B, H)), batch-first at the boundary. Forward: one GEMM for all
+    input projections, then per step one cuBLAS GEMM (gates_t += h_{t-1}
+    W_hh^T) and one po_lstm_cell_fwd. Backward: per step one po_lstm_cell_bwd
+    and one GEMM (dh_{t-1} = dgates_t W_hh_live), then three GEMMs over all
+    steps (dx, dW_ih, dW_hh) and a column sum (db)."""
+
+    @staticmethod
+    def forward(ctx, x, w_ih, w_hh, b_ih, b_hh, module):
+        if not x.is_cuda:
+            raise RuntimeError("LiveLSTM runs on the B200 kernels (po_lstm_cell_*): no CPU path")
+        lib = _lib.load()
+        stream = torch.cuda.current_stream(x.device).cuda_stream
+        bsz, steps, d_in = x.shape
+        hid = w_hh.shape[1]
+        xt = x.detach().transpose(0, 1).contiguous()
+        gates = torch.addmm(b_ih + b_hh, xt.view(steps * bsz, d_in), w_ih.t()).view(steps, bsz, 4 * hid)
+        hs = torch.empty((steps + 1, bsz, hid), device=x.device, dtype=x.dtype)
+        cs = torch.empty((steps, bsz, hid), device=x.device, dtype=x.dtype)
+        y = torch.empty((bsz, steps, hid), device=x.device, dtype=x.dtype)
+        w_hh_t = w_hh.t()
+        for t in range(steps):
+            if t > 0:
+                gates[t].addmm_(hs[t], w_hh_t)
+            rc = lib.po_lstm_cell_fwd(gates[t].data_ptr(), cs[t - 1].data_ptr() if t else None, cs[t].data_ptr(),
+                                      hs[t + 1].data_ptr(), y[:, t].data_ptr(), steps * hid, bsz, hid, stream)
+            _lib.check(rc, "po_lstm_cell_fwd")
+        ctx.save_for_backward(xt, gates, hs, cs)
+        ctx.module = module
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        xt, gates, hs, cs = ctx.saved_tensors
+        m = ctx.module
+        w_ih, w_hh = m.weight_ih_l0, m.weight_hh_l0  # point at the live buffer again by now
+        lib = _lib.load()
+        stream = torch.cuda.current_stream(dy.device).cuda_stream
+        steps, bsz, hid4 = gates.shape
+        hid = hid4 // 4
+        d_in = xt.shape[2]
+        dy = dy.contiguous()
+        dg = torch.empty_like(gates)
+        dc = torch.zeros((bsz, hid), device=dy.device, dtype=dy.dtype)
+        ping = torch.empty((2, bsz, hid), device=dy.device, dtype=dy.dtype)
+        rec = None
+        for t in range(steps - 1, -1, -1):
+            rc = lib.po_lstm_cell_bwd(gates[t].data_ptr(), cs[t - 1].data_ptr() if t else None, cs[t].data_ptr(),
+                                      dy[:, t].data_ptr(), steps * hid, rec, dc.data_ptr(), dg[t].data_ptr(), bsz,
+                                      hid, stream)
+            _lib.check(rc, "po_lstm_cell_bwd")
+            if t > 0:
+                buf = ping[t % 2]
+                torch.mm(dg[t], w_hh, out=buf)
+                rec = buf.data_ptr()
+        dg2 = dg.view(steps * bsz, hid4)
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = torch.mm(dg2, w_ih).view(steps, bsz, d_in).transpose(0, 1)
+        gw_ih = dg2.t().mm(xt.view(steps * bsz, d_in))
+        if steps > 1:  # h_{-1} = 0 contributes nothing
+            gw_hh = dg[1:].reshape((steps - 1) * bsz, hid4).t().mm(hs[1:steps].reshape((steps - 1) * bsz, hid))
+        else:
+            gw_hh = torch.zeros_like(w_hh)
+        gb = dg2.sum(0)
+        return dx, gw_ih, gw_hh, gb, gb, None
+
+
+class LiveLSTM(nn.Module):
+    """Single-layer batch-first LSTM with nn.LSTM's parameters, names and
+    initialisation (weight_ih_l0, weight_hh_l0, bias_ih_l0, bias_hh_l0, each
+    U(-1/sqrt(H), 1/sqrt(H)) in that order) whose backward uses the live
+    weights (see _LiveLSTMFn). forward(x) -> (y, None)."""
+
+    def __init__(self, input_size: int, hidden_size: int):
+        super().__init__()
+        self.input_size, self.hidden_size = input_size, hidden_size
+        h4 = 4 * hidden_size
+        self.weight_ih_l0 = nn.Parameter(torch.empty(h4, input_size))
+        self.weight_hh_l0 = nn.Parameter(torch.empty(h4, hidden_size))
+        self.bias_ih_l0 = nn.Parameter(torch.empty(h4))
+        self.bias_hh_l0 = nn.Parameter(torch.empty(h4))
+        stdv = 1.0 / math.sqrt(hidden_size)
+        for w in (self.weight_ih_l0, self.weight_hh_l0, self.bias_ih_l0, self.bias_hh_l0):
+            nn.init.uniform_(w, -stdv, stdv)
+
+    def forward(self, x):
+        return _LiveLSTMFn.apply(x, self.weight_ih_l0, self.weight_hh_l0, self.bias_ih_l0, self.bias_hh_l0,
+                                 self), None
+
+
 class _LSTMBlock(nn.Module):
     def __init__(self, d_in, d, residual):
         super().__init__()
-        self.lstm = nn.LSTM(d_in, d, batch_first=True)
+        self.lstm = LiveLSTM(d_in, d)
         self.residual = residual
 
     def forward(self, x):
