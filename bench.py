@@ -389,7 +389,7 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         out = bp.single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches)
         t = bp.single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches, tf32=True, with_eager=False,
                                    with_roofline=False)
-        out["tf32"] = {k: t[k] for k in ("pred_on", "pred_off", "prediction_overhead", "config")}
+        out["tf32"] = {k: t[k] for k in ("pred_on", "pred_off", "prediction_overhead", "serial_streams", "config")}
         out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
     else:
         staged = args.dist_backend != "nccl"

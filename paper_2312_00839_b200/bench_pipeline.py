@@ -49,7 +49,8 @@ def _run_once(torch, device, strategy, depth, n_batches, data, seed=0, dims=CONF
     return rep, e0.elapsed_time(e1) / 1e3, wall
 
 
-def _graph_for(torch, device, strategy, depth, n_batches, data, seed=0, dims=CONFIG1_DIMS, acts=CONFIG1_ACTS):
+def _graph_for(torch, device, strategy, depth, n_batches, data, seed=0, dims=CONFIG1_DIMS, acts=CONFIG1_ACTS,
+               streams="serial"):
     from .optim import OptimizerConfig, OptimizerState
     from .runtime import GraphedExecute, build_timeline
     from .stages import build_layers, build_stages, torch_init
@@ -57,7 +58,8 @@ def _graph_for(torch, device, strategy, depth, n_batches, data, seed=0, dims=CON
     stages = build_stages(build_layers(dims, acts), depth, torch_init(seed, device), device=device)
     opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=device) for s in stages]
     tl = build_timeline(strategy, depth, n_batches)
-    g = GraphedExecute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: 1e-4, warmup_runs=1)
+    g = GraphedExecute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: 1e-4, warmup_runs=1,
+                       streams=streams)
     g.replay()  # first replay: graph upload
     torch.cuda.synchronize(device)
     return g
@@ -73,17 +75,18 @@ def _time_replays(torch, device, g, replays):
     return e0.elapsed_time(e1) / 1e3 / replays
 
 
-def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=5):
-    """Prediction off/on graphs timed in alternation (median of `trials`), so
-    clock and thermal drift hit both arms alike."""
+def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=5, streams=("stage", "serial")):
+    """Prediction off/on graphs (per stream mode) timed in alternation (median
+    of `trials`), so clock and thermal drift hit every arm alike."""
     import statistics
 
-    graphs = {s: _graph_for(torch, device, s, depth, n_batches, data) for s in ("async_raw", "optimizer_prediction")}
-    times = {s: [] for s in graphs}
+    graphs = {(s, m): _graph_for(torch, device, s, depth, n_batches, data, streams=m)
+              for m in streams for s in ("async_raw", "optimizer_prediction")}
+    times = {k: [] for k in graphs}
     for _ in range(trials):
-        for s, g in graphs.items():
-            times[s].append(_time_replays(torch, device, g, replays))
-    return {s: (graphs[s].report(), statistics.median(times[s]), graphs[s].launches, times[s]) for s in graphs}
+        for k, g in graphs.items():
+            times[k].append(_time_replays(torch, device, g, replays))
+    return {k: (graphs[k].report(), statistics.median(times[k]), graphs[k].launches, times[k]) for k in graphs}
 
 
 def stage_unit_times(torch, device, stages, opts, data, loss_kind, predictive: bool, reps: int = 20):
@@ -148,45 +151,62 @@ def pipeline_roofline(stage_times, batch, n, depth, boundary_bytes, link_gbs=770
 
 def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, replays: int = 5, tf32: bool = False,
                         with_eager: bool = True, with_roofline: bool = True):
-    """All `depth` stages on one GPU, events in timeline order (the single-GPU
-    1F1B runner). Each measured unit is one full run of the 1F1B timeline
-    (n_batches mini-batches, warm-up and drain included), replayed from a CUDA
-    graph (`GraphedExecute`); the eager (Python-driven) runner is reported
-    beside it. Samples/s with prediction on and off, and the pipeline
-    roofline from per-stage graphed unit times."""
+    """All `depth` stages on one GPU (the single-GPU 1F1B runner). Each
+    measured unit is one full run of the 1F1B timeline (n_batches
+    mini-batches, warm-up and drain included), replayed from a CUDA graph
+    (`GraphedExecute`). Headline: the stage-concurrent runner (one CUDA stream
+    per stage, `streams="stage"`); the serialised runner (every event on one
+    stream, timeline order) and the eager (Python-driven) runner beside it.
+    Samples/s with prediction on and off, and the pipeline roofline from
+    per-stage graphed unit times."""
     from .optim import OptimizerConfig, OptimizerState
     from .stages import build_layers, build_stages, torch_init
 
     torch.backends.cuda.matmul.allow_tf32 = tf32
     data = DeviceBatches(torch, device)
     out = {"config": f"config1 MLP {CONFIG1_DIMS}, B={BATCH}, Adam lr 1e-4, 1F1B D={depth} on 1 GPU "
-                     f"(single-process runner, CUDA-graph replay of whole {n_batches}-mini-batch runs), "
-                     f"{'TF32' if tf32 else 'fp32 (TF32 off)'} GEMMs, fp32 master weights"}
+                     f"(single-process runner, one CUDA stream per stage, CUDA-graph replay of whole "
+                     f"{n_batches}-mini-batch runs), {'TF32' if tf32 else 'fp32 (TF32 off)'} GEMMs, "
+                     f"fp32 master weights"}
     launches = 0
     pair = _graphed_pair(torch, device, depth, n_batches, data, replays)
+    out["serial_streams"] = {}
     for strategy in ("async_raw", "optimizer_prediction"):
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
-        rep, sec, n_launch, trials = pair[strategy]
-        out[key] = {"samples_per_s": round(n_batches * BATCH / sec, 1), "s_per_run": round(sec, 5),
-                    "s_per_run_trials": [round(t, 5) for t in trials],
-                    "final_loss": rep.losses[-1], "optimizer_launches_per_run": n_launch}
+        for mode in ("stage", "serial"):
+            rep, sec, n_launch, trials = pair[(strategy, mode)]
+            row = {"samples_per_s": round(n_batches * BATCH / sec, 1), "s_per_run": round(sec, 5),
+                   "s_per_run_trials": [round(t, 5) for t in trials],
+                   "final_loss": rep.losses[-1], "optimizer_launches_per_run": n_launch}
+            if mode == "stage":
+                out[key] = row
+            else:
+                out["serial_streams"][key] = row
+            launches += n_launch * replays
         if with_eager:
             _run_once(torch, device, strategy, depth, min(n_batches, 2 * depth + 2), data)  # eager warm-up
             _, esec, _ = _run_once(torch, device, strategy, depth, n_batches, data)
             out[key]["eager_samples_per_s"] = round(n_batches * BATCH / esec, 1)
-        launches += n_launch * replays
         if with_roofline:
             stages = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), depth, torch_init(7, device), device=device)
             opts = [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in stages]
             t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction")
             roof = pipeline_roofline(t, BATCH, n_batches, depth, [4 * BATCH * s_.out_dim for s_ in stages[:-1]])
             out[key]["roofline"] = roof
-            out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] / roof["single_gpu_samples_per_s"],
-                                                            4)
+            # serialised stages are bounded by B / sum_k t_k; concurrent stages on
+            # one GPU by neither (they share the SMs) — both fractions reported
+            out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] /
+                                                            roof["single_gpu_samples_per_s"], 4)
+            out[key]["frac_of_multi_gpu_roofline"] = round(out[key]["samples_per_s"] /
+                                                           roof["multi_gpu_samples_per_s"], 4)
+            ser = out["serial_streams"][key]
+            ser["frac_of_single_gpu_roofline"] = round(ser["samples_per_s"] / roof["single_gpu_samples_per_s"], 4)
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out["value"] = on
     out["unit"] = "samples/s"
     out["prediction_overhead"] = round(1.0 - on / off, 4)
+    ser = out["serial_streams"]
+    ser["prediction_overhead"] = round(1.0 - ser["pred_on"]["samples_per_s"] / ser["pred_off"]["samples_per_s"], 4)
     if with_roofline:
         # one stage per GPU (the north star's setting): the pipeline runs at the
         # slowest stage's unit time, so the prediction overhead there is the
@@ -194,8 +214,8 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
         r_on, r_off = out["pred_on"]["roofline"], out["pred_off"]["roofline"]
         out["multi_gpu_roofline_prediction_overhead"] = round(
             1.0 - r_on["compute_samples_per_s"] / r_off["compute_samples_per_s"], 4)
-        out["single_gpu_note"] = ("all stages share one GPU's 126 MB L2 here; the predicted-weights staging "
-                                  "buffers add ~21 MB to a ~105 MB per-mini-batch working set")
+        out["single_gpu_note"] = ("all stages share one GPU's SMs and 126 MB L2 here; the predicted-weights "
+                                  "staging buffers add ~21 MB to a ~105 MB per-mini-batch working set")
     if with_eager:
         out["eager_prediction_overhead"] = round(
             1.0 - out["pred_on"]["eager_samples_per_s"] / out["pred_off"]["eager_samples_per_s"], 4)

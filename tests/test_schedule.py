@@ -181,3 +181,13 @@ def test_stage_program_fusion_marks(depth):
         assert len(fused) == n - (depth - k)
     live = stage_program(tl, 0, predictive=False)
     assert not any(o.fuse_predict for o in live)
+
+
+def test_execute_rejects_unknown_stream_mode():
+    import pytest
+
+    from paper_2312_00839_b200.runtime import build_timeline, execute
+
+    tl = build_timeline("async_raw", 2, 4)
+    with pytest.raises(ValueError, match="streams"):
+        execute(tl, [None, None], [None, None], "async_raw", None, "mse", lambda mb: 0.1, streams="bogus")

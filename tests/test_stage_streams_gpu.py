@@ -1,0 +1,98 @@
+"""Stage-concurrent single-GPU runner: `execute(..., streams="stage")` puts
+each stage's events on its own CUDA stream (the D-GPU pipeline's concurrency
+on one device). Each stage's arithmetic and its order are unchanged, so every
+run must be BIT-identical to the serial runner — and through it to the
+reference goldens (records exact, losses in tolerance)."""
+
+import pytest
+
+from test_runtime_gpu import CONFIG1, EXTRA, SMALL, build, check_losses, rec_tuples, run_case  # noqa: F401
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(case, streams, checks="eager", fuse=True):
+    from oracle import data_ref
+    from paper_2312_00839_b200.runtime import execute
+    from test_runtime_gpu import ArraySource, Source
+
+    tl, stages, opts = build(case)
+    if case["name"].startswith("small"):
+        src, loss = Source(case["data_seed"], case["rows"], case["dims"][0], case["dims"][-1]), "mse"
+    else:
+        batches, loss = data_ref.config1(seed=case["data_seed"])
+        src = ArraySource(batches)
+    rep = execute(tl, stages, opts, case["strategy"], src, loss, lambda mb, lr=case["lr"]: lr,
+                  checks=checks, fuse=fuse, streams=streams)
+    return rep, stages
+
+
+def _same(a, sa, b, sb):
+    import torch
+
+    assert a.losses == b.losses
+    assert rec_tuples(a) == rec_tuples(b)
+    assert a.snapshot_peaks == b.snapshot_peaks and a.stash_peaks == b.stash_peaks
+    for x, y in zip(sa, sb):
+        assert torch.equal(x.flat.data, y.flat.data)
+
+
+@pytest.mark.parametrize("case", SMALL + EXTRA,
+                         ids=lambda c: f"D{c['depth']}-{c['strategy']}-T{c.get('micros', 1)}-{c['kind']}")
+def test_stage_streams_bit_identical_to_serial(case):
+    a, sa = _run(case, "serial")
+    b, sb = _run(case, "stage")
+    _same(a, sa, b, sb)
+    assert rec_tuples(b) == case["records"]
+    check_losses(b.losses, case["losses"])
+
+
+@pytest.mark.parametrize("case", CONFIG1, ids=lambda c: c["strategy"])
+def test_config1_stage_streams_host_batches(case):
+    """Host (numpy) batches: x and y are staged to the device on stage 0's
+    stream and consumed by the last stage's."""
+    a, sa = _run(case, "serial", checks="deferred")
+    b, sb = _run(case, "stage", checks="deferred")
+    _same(a, sa, b, sb)
+
+
+def test_stage_streams_unfused_and_eager_checks():
+    case = next(c for c in SMALL if c["depth"] == 4 and c["strategy"] == "optimizer_prediction"
+                and c["kind"] == "adam")
+    a, sa = _run(case, "serial", fuse=False)
+    b, sb = _run(case, "stage", fuse=False)
+    _same(a, sa, b, sb)
+    c, sc = _run(case, "stage", checks="deferred")
+    assert c.losses == b.losses
+
+
+@pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("async_raw", "adamw"),
+                                           ("weight_stashing", "sgdm")])
+def test_graphed_stage_streams_equal_graphed_serial(strategy, kind):
+    """The multi-stream capture (fork/join inside the graph) replays to the
+    same bits as the single-stream capture."""
+    import torch
+
+    from paper_2312_00839_b200.bench_pipeline import DeviceBatches
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import GraphedExecute, build_timeline
+    from paper_2312_00839_b200.stages import build_layers, build_stages, torch_init
+
+    dev = torch.device("cuda", 0)
+    dims, acts = [256, 512, 384, 256, 10], ["relu", "relu", "relu", "linear"]
+    data = DeviceBatches(torch, dev, dims=dims)
+    tl = build_timeline(strategy, 4, 11)
+    out = {}
+    for streams in ("serial", "stage"):
+        stages = build_stages(build_layers(dims, acts), 4, torch_init(5, dev), device=dev)
+        opts = [OptimizerState(OptimizerConfig(kind), s.param_names, device=dev) for s in stages]
+        g = GraphedExecute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: 1e-3, streams=streams)
+        losses = []
+        for _ in range(3):
+            g.replay()
+            losses.append(g.report().losses)
+        torch.cuda.synchronize()
+        out[streams] = (losses, [s.flat.data.clone() for s in stages])
+    assert out["serial"][0] == out["stage"][0]
+    for x, y in zip(out["serial"][1], out["stage"][1]):
+        assert torch.equal(x, y)
