@@ -174,6 +174,36 @@ def cpu_baseline(kind: str, budget_s: float = 12.0, n: int = 1 << 26):
     }
 
 
+def cpu_pipeline_baseline(n_batches: int = 24, strategy: str = "optimizer_prediction", depth: int = 4):
+    """The reference's executor on config 1 (oracle/runtime_ref.py: the numpy
+    float64 restatement of pipesim's 1F1B executor and dense stages, BLAS on
+    every host core) over a bounded sample of n_batches synthetic mini-batches:
+    samples/s, the first clause of BASELINE.json's metric, on the host."""
+    import numpy as np
+
+    from oracle import optim_ref, runtime_ref
+
+    dims, acts, batch = [3072, 1024, 1024, 1024, 10], ["relu", "relu", "relu", "linear"], 128
+    rng = np.random.default_rng(0)
+    xs = [rng.normal(0, 1, (batch, dims[0])) for _ in range(4)]
+    ys = [np.eye(dims[-1])[rng.integers(0, dims[-1], batch)] for _ in range(4)]
+
+    def init(i, din, dout):
+        r = np.random.default_rng(100 + i)
+        return r.normal(0, (2.0 / din) ** 0.5, (din, dout)), np.zeros((1, dout))
+
+    t0 = time.perf_counter()
+    runtime_ref.run(dims, acts, depth, n_batches, strategy, optim_ref.Hyper("adam"),
+                    lambda mb: (xs[(mb - 1) % 4], ys[(mb - 1) % 4]), "softmax_xent", lambda mb: 1e-4, init)
+    sec = time.perf_counter() - t0
+    return {"value": round(n_batches * batch / sec, 1), "unit": "samples/s", "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": (f"oracle/runtime_ref.py (numpy float64 restatement of pipesim's executor) config 1 "
+                       f"MLP {dims}, B={batch}, Adam, 1F1B D={depth}, {strategy}, {n_batches} mini-batches "
+                       f"(warm-up and drain included) in {sec:.2f} s; numpy BLAS threads = all host cores, "
+                       f"optimizer elementwise single-threaded as in the reference")}
+
+
 def reference_arm(args):
     """--impl reference: the reference's algorithm for this path on the host
     cores (the oracle's C port, float64 like the reference, OpenMP on every
@@ -226,6 +256,15 @@ def reference_arm(args):
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "vs_baseline": None,
     }
+    try:
+        line["pipeline"] = {
+            "pred_on": cpu_pipeline_baseline(strategy="optimizer_prediction"),
+            "pred_off": cpu_pipeline_baseline(strategy="async_raw"),
+        }
+        line["pipeline"]["value"] = line["pipeline"]["pred_on"]["value"]
+        line["pipeline"]["unit"] = "samples/s"
+    except Exception as exc:  # the kernel line above must still print
+        line["pipeline"] = {"error": f"{type(exc).__name__}: {exc}"}
     print(json.dumps(line), flush=True)
 
 
@@ -391,6 +430,11 @@ def pipeline_leg(args, torch, dist, rank, world, device):
                                    with_roofline=False)
         out["tf32"] = {k: t[k] for k in ("pred_on", "pred_off", "prediction_overhead", "serial_streams", "config")}
         out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
+        if not args.no_cpu:
+            try:
+                out["cpu_baseline"] = cpu_pipeline_baseline()
+            except Exception as exc:
+                out["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
     else:
         staged = args.dist_backend != "nccl"
         out = bp.multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches,

@@ -6,6 +6,7 @@ CIFAR-10-shaped batches resident in HBM, 1F1B with prediction on
 
 from __future__ import annotations
 
+import math
 import time
 
 CONFIG1_DIMS = [3072, 1024, 1024, 1024, 10]
@@ -313,40 +314,93 @@ def module_stages_for(torch, name, device, depth=None, costs=None):
     return build_module_stages(blocks, depth, device, cfg["in_shape"], costs=costs, in_dtype=in_dtype), costs
 
 
-def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf32: bool = True):
-    """Configs 2-4 through the single-GPU 1F1B runner (all stages on one GPU)."""
+def _module_setup(torch, device, name, strategy, n_batches):
     from .optim import OptimizerConfig, OptimizerState
-    from .runtime import build_timeline, execute
+    from .runtime import build_timeline
+
+    cfg = MODULE_CONFIGS[name]
+    stages, _ = module_stages_for(torch, name, device)
+    kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
+    opts = [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in stages]
+    return stages, opts, build_timeline(strategy, cfg["depth"], n_batches)
+
+
+def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf32: bool = True, trials: int = 3,
+                               with_eager: bool = True, with_roofline: bool = True):
+    """Configs 2-4 through the single-GPU 1F1B runner (all D stages on one
+    GPU). Headline: whole n_batches-mini-batch runs captured into CUDA graphs
+    with one stream per stage (`GraphedExecute(streams="stage")`), prediction
+    off/on replayed in alternation (median of `trials`); the eager serial
+    runner beside it; the pipeline roofline from per-stage graphed unit times
+    (SURVEY.md §8d)."""
+    import statistics
+
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import GraphedExecute, execute
 
     cfg = MODULE_CONFIGS[name]
     torch.backends.cuda.matmul.allow_tf32 = tf32
     torch.backends.cudnn.allow_tf32 = tf32
     data = ModuleBatches(torch, device, cfg)
-    out = {"config": f"{name}: D={cfg['depth']} stages on 1 GPU (single-process runner), batch {cfg['batch']}, "
-                     f"{cfg['opt']} lr {cfg['lr']}, {n_batches} mini-batches, "
-                     f"{'TF32' if tf32 else 'fp32'} convs/GEMMs, fp32 master weights"}
+    lr = cfg["lr"]
+    out = {"config": f"{name}: D={cfg['depth']} stages on 1 GPU (single-process runner, one CUDA stream per stage, "
+                     f"CUDA-graph replay of whole {n_batches}-mini-batch runs), batch {cfg['batch']}, "
+                     f"{cfg['opt']} lr {lr}, {'TF32' if tf32 else 'fp32'} convs/GEMMs, fp32 master weights"}
+    try:
+        graphs = {}
+        for strategy in ("async_raw", "optimizer_prediction"):
+            stages, opts, tl = _module_setup(torch, device, name, strategy, n_batches)
+            graphs[strategy] = (GraphedExecute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: lr,
+                                               warmup_runs=1, streams="stage"), stages)
+            graphs[strategy][0].replay()
+            torch.cuda.synchronize(device)
+        times = {s: [] for s in graphs}
+        for _ in range(trials):
+            for s, (g, _) in graphs.items():
+                times[s].append(_time_replays(torch, device, g, 1))
+        for s, (g, stages) in graphs.items():
+            key = "pred_on" if s == "optimizer_prediction" else "pred_off"
+            sec = statistics.median(times[s])
+            out[key] = {"samples_per_s": round(n_batches * cfg["batch"] / sec, 2), "s_per_run": round(sec, 4),
+                        "s_per_run_trials": [round(t, 4) for t in times[s]],
+                        "final_loss": g.report().losses[-1], "optimizer_launches_per_run": g.launches}
+        out["stage_params"] = [s.numel for s in graphs["async_raw"][1]]
+        out["boundary_bytes"] = [4 * cfg["batch"] * math.prod(s.out_shape) for s in graphs["async_raw"][1][:-1]]
+    finally:
+        graphs = g = stages = opts = None  # noqa: F841 (drop the graphs' memory pools)
+        torch.cuda.empty_cache()
     for strategy in ("async_raw", "optimizer_prediction"):
-        secs = []
-        for trial, n in enumerate((2 * cfg["depth"], n_batches)):
-            stages, costs = module_stages_for(torch, name, device)
-            kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
-            opts = [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in stages]
-            tl = build_timeline(strategy, cfg["depth"], n)
+        key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
+        if with_eager:
+            stages, opts, tl = _module_setup(torch, device, name, strategy, n_batches)
             torch.cuda.synchronize(device)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            rep = execute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: cfg["lr"], checks="deferred")
+            execute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: lr, checks="deferred")
             e1.record()
             torch.cuda.synchronize(device)
-            secs.append(e0.elapsed_time(e1) / 1e3)
-            stage_params = [s.numel for s in stages]
+            out[key]["eager_serial_samples_per_s"] = round(n_batches * cfg["batch"] / (e0.elapsed_time(e1) / 1e3), 2)
             del stages, opts
-        key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
-        out[key] = {"samples_per_s": round(n_batches * cfg["batch"] / secs[-1], 2), "s": round(secs[-1], 4),
-                    "final_loss": rep.losses[-1]}
-    out["stage_params"] = stage_params
+        if with_roofline:
+            stages, _ = module_stages_for(torch, name, device)
+            kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
+            opts = [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in stages]
+            t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction",
+                                 reps=5)
+            roof = pipeline_roofline(t, cfg["batch"], n_batches, cfg["depth"], out["boundary_bytes"])
+            out[key]["roofline"] = roof
+            out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] /
+                                                            roof["single_gpu_samples_per_s"], 4)
+            out[key]["frac_of_multi_gpu_roofline"] = round(out[key]["samples_per_s"] /
+                                                           roof["multi_gpu_samples_per_s"], 4)
+            del stages, opts
+        torch.cuda.empty_cache()
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4))
+    if with_roofline:
+        r_on, r_off = out["pred_on"]["roofline"], out["pred_off"]["roofline"]
+        out["multi_gpu_roofline_prediction_overhead"] = round(
+            1.0 - r_on["multi_gpu_samples_per_s"] / r_off["multi_gpu_samples_per_s"], 4)
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     return out
