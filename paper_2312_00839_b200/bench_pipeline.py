@@ -254,9 +254,10 @@ def projected_multi_gpu(torch, device, depth: int = 8, n_batches: int = 64, tf32
 
 MODULE_CONFIGS = {
     # BASELINE configs[1..3] (SURVEY.md §8d pipeline synthetic inputs)
-    "config2_vgg16": dict(blocks="vgg16", in_shape=(3, 32, 32), classes=100, batch=128, depth=4, opt="sgdm", lr=0.01),
+    "config2_vgg16": dict(blocks="vgg16", in_shape=(3, 32, 32), classes=100, batch=128, depth=4, opt="sgdm", lr=0.01,
+                          channels_last=True),
     "config3_resnet101": dict(blocks="resnet101", in_shape=(3, 224, 224), classes=200, batch=64, depth=8,
-                              opt="adamw", lr=1e-3),
+                              opt="adamw", lr=1e-3, channels_last=True),
     "config4_gnmt8": dict(blocks="gnmt8", in_shape=(50,), classes=32000, batch=64, depth=8, opt="adam", lr=1e-3,
                           tokens=True),
 }
@@ -298,7 +299,7 @@ def module_block_costs(torch, name, device):
     in_dtype = torch.long if cfg.get("tokens") else torch.float32
     if name not in _COSTS:
         _COSTS[name] = profile_block_costs(make_blocks(cfg["blocks"], cfg["classes"]), cfg["in_shape"], cfg["batch"],
-                                           device, in_dtype=in_dtype)
+                                           device, in_dtype=in_dtype, channels_last=cfg.get("channels_last", False))
     return _COSTS[name]
 
 
@@ -311,7 +312,8 @@ def module_stages_for(torch, name, device, depth=None, costs=None):
     costs = costs if costs is not None else module_block_costs(torch, name, device)
     torch.manual_seed(0)
     blocks = make_blocks(cfg["blocks"], cfg["classes"])
-    return build_module_stages(blocks, depth, device, cfg["in_shape"], costs=costs, in_dtype=in_dtype), costs
+    return build_module_stages(blocks, depth, device, cfg["in_shape"], costs=costs, in_dtype=in_dtype,
+                               channels_last=cfg.get("channels_last", False)), costs
 
 
 def _module_setup(torch, device, name, strategy, n_batches):

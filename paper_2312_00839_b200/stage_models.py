@@ -283,8 +283,14 @@ class ModuleStage:
     run_forward / run_backward.
     """
 
-    def __init__(self, rank: int, blocks: list[nn.Module], device, in_shape: tuple, in_dtype=torch.float32):
+    def __init__(self, rank: int, blocks: list[nn.Module], device, in_shape: tuple, in_dtype=torch.float32,
+                 channels_last: bool = False):
+        """channels_last=True runs the stage's image tensors in NHWC inside the
+        stage (cuDNN's native tensor-core layout); boundary activations and
+        gradients stay NCHW-contiguous, so transports and the other stages are
+        unaffected. Parameters keep their flat NCHW views either way."""
         self.rank = rank
+        self.channels_last = channels_last
         self.device = torch.device(device)
         self.module = nn.Sequential(*blocks).to(self.device)
         self.module.train()
@@ -333,7 +339,12 @@ class ModuleStage:
             if self.rank > 0 and x_in.is_floating_point():
                 x_in.requires_grad_(True)
             with torch.enable_grad():
-                out = self.module(x_in)
+                h = x_in
+                if self.channels_last and h.dim() == 4:
+                    h = h.contiguous(memory_format=torch.channels_last)
+                out = self.module(h)
+                if not out.is_contiguous():
+                    out = out.contiguous()
         finally:
             self._point(self._live)
         if check_finite:
@@ -358,7 +369,8 @@ class ModuleStage:
         return g_in, self.flat.grads
 
 
-def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32, reps=3) -> list[float]:
+def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32, reps=3,
+                        channels_last: bool = False) -> list[float]:
     """Per-block forward+backward time on the device for one batch (a tiny
     profiling partitioner, in the spirit of PipeDream's), used to balance
     stages by time instead of parameter count."""
@@ -366,6 +378,8 @@ def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32,
     x = torch.zeros((batch, *in_shape), device=dev, dtype=in_dtype)
     if in_dtype == torch.float32:
         x.normal_()
+    if channels_last and x.dim() == 4:
+        x = x.contiguous(memory_format=torch.channels_last)
     costs = []
     for b in blocks:
         b.to(dev).train()
@@ -388,14 +402,15 @@ def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32,
     return costs
 
 
-def build_module_stages(blocks, depth, device, in_shape, costs=None, in_dtype=torch.float32):
+def build_module_stages(blocks, depth, device, in_shape, costs=None, in_dtype=torch.float32,
+                        channels_last: bool = False):
     """Partition `blocks` into `depth` contiguous stages balanced by `costs`
     (default: parameter counts) and build them in order."""
     costs = costs if costs is not None else [max(1, c) for c in block_param_counts(blocks)]
     ranges = balanced_partition(costs, depth)
     stages, shape, dtype = [], tuple(in_shape), in_dtype
     for k, (lo, hi) in enumerate(ranges):
-        st = ModuleStage(k, blocks[lo:hi], device, shape, dtype)
+        st = ModuleStage(k, blocks[lo:hi], device, shape, dtype, channels_last=channels_last)
         stages.append(st)
         shape, dtype = st.out_shape, torch.float32
     return stages

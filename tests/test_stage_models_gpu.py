@@ -78,3 +78,38 @@ def test_fused_equals_unfused_on_vgg_stages():
         finals.append((rep.losses, [s.flat.data.clone() for s in stages]))
     assert finals[0][0] == finals[1][0]
     assert all(torch.equal(a, b) for a, b in zip(finals[0][1], finals[1][1]))
+
+
+@pytest.mark.parametrize("name", ["config2_vgg16", "config3_resnet101"])
+def test_channels_last_stage_matches_nchw(name):
+    """channels_last only changes the in-stage layout: forward output, input
+    gradient and every flat parameter gradient agree with the NCHW stage
+    (fp32, TF32 off) and the boundary tensors stay NCHW-contiguous."""
+    import torch
+
+    from paper_2312_00839_b200.bench_pipeline import MODULE_CONFIGS, make_blocks
+    from paper_2312_00839_b200.stage_models import ModuleStage
+
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dev = torch.device("cuda", 0)
+    cfg = MODULE_CONFIGS[name]
+    g = torch.Generator(device=dev).manual_seed(0)
+    outs = []
+    for cl in (False, True):
+        torch.manual_seed(0)
+        blocks = make_blocks(cfg["blocks"], cfg["classes"])
+        stem = blocks[0].to(dev)
+        with torch.no_grad():
+            x = stem(torch.randn((4, *cfg["in_shape"]), device=dev, generator=g.manual_seed(1)))
+        shape = tuple(x.shape[1:])
+        st = ModuleStage(1, blocks[1:3], dev, shape, channels_last=cl)
+        out = st.run_forward(st.params, (1, 0), x, 1)
+        assert out.is_contiguous()
+        gout = torch.randn(out.shape, device=dev, generator=g.manual_seed(2))
+        g_in, _ = st.run_backward(st.params, (1, 0), gout)
+        assert g_in.is_contiguous()
+        outs.append((out, g_in, st.flat.grad.clone()))
+    (o0, gi0, gf0), (o1, gi1, gf1) = outs
+    for a, b in ((o0, o1), (gi0, gi1), (gf0, gf1)):
+        assert float((a - b).abs().max()) <= 1e-4 * float(b.abs().max())
