@@ -416,6 +416,8 @@ def e2e_leg(args, torch, dist, world, device):
     }
     del w_h, g_h, wo_h, wh_h, streamer, opt
     torch.cuda.empty_cache()
+    if hasattr(torch._C, "_host_emptyCache"):  # hand the 16 GB of pinned host buffers back to the OS
+        torch._C._host_emptyCache()
     return res
 
 
@@ -424,17 +426,27 @@ def pipeline_leg(args, torch, dist, rank, world, device):
     samples/s with prediction on vs off."""
     from paper_2312_00839_b200 import bench_pipeline as bp
 
+    t_leg = time.perf_counter()
+
+    def progress(what):
+        print(f"[bench] pipeline leg: {what} done at {time.perf_counter() - t_leg:.1f} s", file=sys.stderr,
+              flush=True)
+
     if world == 1:
         out = bp.single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches)
+        progress("config 1 fp32")
         t = bp.single_gpu_pipeline(torch, device, n_batches=args.pipeline_batches, tf32=True, with_eager=False,
                                    with_roofline=False)
         out["tf32"] = {k: t[k] for k in ("pred_on", "pred_off", "prediction_overhead", "serial_streams", "config")}
+        progress("config 1 tf32")
         out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
+        progress("projected 8-GPU")
         if not args.no_cpu:
             try:
                 out["cpu_baseline"] = cpu_pipeline_baseline()
             except Exception as exc:
                 out["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+            progress("cpu baseline")
     else:
         staged = args.dist_backend != "nccl"
         out = bp.multi_gpu_pipeline(torch, dist, rank, world, device, n_batches=args.pipeline_batches,
@@ -460,6 +472,7 @@ def pipeline_leg(args, torch, dist, rank, world, device):
             except Exception as exc:
                 configs[name] = {"error": f"{type(exc).__name__}: {exc}"}
             torch.cuda.empty_cache()
+            progress(name)
         out["configs"] = configs
     return out
 
@@ -497,6 +510,9 @@ def ours(args):
                 print(json.dumps(line), flush=True)
             os._exit(0)
 
+        import faulthandler
+
+        faulthandler.dump_traceback_later(max(1.0, args.pipeline_timeout - 2.0), exit=False)  # where it hung
         dog = threading.Timer(args.pipeline_timeout, _expire)
         dog.daemon = True
         dog.start()
@@ -505,6 +521,7 @@ def ours(args):
         except Exception as exc:  # reported, never silently dropped
             pipe = {"error": f"{type(exc).__name__}: {exc}"}
         dog.cancel()
+        faulthandler.cancel_dump_traceback_later()
     line["pipeline"] = pipe
     if rank == 0:  # printed before any teardown that could fail
         print(json.dumps(line), flush=True)

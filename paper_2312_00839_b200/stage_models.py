@@ -275,6 +275,28 @@ def block_param_counts(blocks: list[nn.Module]) -> list[int]:
 # ---- the stage --------------------------------------------------------------------------------
 
 
+class _GridSafeBatchNorm2d(nn.BatchNorm2d):
+    """BatchNorm2d on PyTorch's native kernels instead of cuDNN's.
+
+    cuDNN's training-mode batch-norm kernels (`bn_fw_tr_1C11_singleread`,
+    `batchnorm_fwtr_nhwc_semiPersist` and their backward twins) synchronise
+    across their whole grid, sized for an otherwise idle GPU. When the
+    stage-concurrent runner puts two such launches on different stage streams,
+    each can hold SMs while it waits for CTAs that never become resident: a
+    GPU deadlock (reproduced on the B200 with config 3 within ~6 runs). The
+    native kernels reduce with a last-block pattern, which never waits for
+    other CTAs to be co-resident. The autograd node is chosen at forward time,
+    so the backward stays native too."""
+
+    def forward(self, x):
+        prev = torch.backends.cudnn.enabled
+        torch.backends.cudnn.enabled = False
+        try:
+            return super().forward(x)
+        finally:
+            torch.backends.cudnn.enabled = prev
+
+
 class ModuleStage:
     """A pipeline stage made of torch modules over a flat parameter buffer.
 
@@ -294,6 +316,9 @@ class ModuleStage:
         self.device = torch.device(device)
         self.module = nn.Sequential(*blocks).to(self.device)
         self.module.train()
+        for m in self.module.modules():
+            if type(m) is nn.BatchNorm2d:
+                m.__class__ = _GridSafeBatchNorm2d
         named = list(self.module.named_parameters())
         self._params = [p for _, p in named]
         self.param_names = [n for n, _ in named]
