@@ -90,49 +90,69 @@ def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=5, stre
     return {k: (graphs[k].report(), statistics.median(times[k]), graphs[k].launches, times[k]) for k in graphs}
 
 
-def stage_unit_times(torch, device, stages, opts, data, loss_kind, predictive: bool, reps: int = 20):
-    """Per-stage device time of one mini-batch's work — forward (+ loss on the
-    last stage) + backward + update (K3 when predictive and not last, else
-    K2) — each captured in a CUDA graph and replayed `reps` times on
-    THROWAWAY stages (it trains them). SURVEY.md §8d's t_f,k + t_b,k (+ t_u,k)."""
+def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
+    """CUDA graph of stage k's work for one mini-batch: forward (+ loss on the
+    last stage) + backward + update (K3 when predictive and not last, else K2)."""
     from .stages import loss_and_grad
 
-    times = []
-    for k, (st, opt) in enumerate(zip(stages, opts)):
-        last = k == len(stages) - 1
-        x0, y0 = data.batch(1)
-        x = x0 if k == 0 else torch.randn((x0.shape[0], *st.in_shape), device=device)
-        g_last = None if last else torch.randn((x0.shape[0], *st.out_shape), device=device)
-        staging = st.flat.layout.empty(device)
-        opt._bind(st.flat.layout)
-        opt._ensure_state()
+    last = k == depth - 1
+    x0, y0 = data.batch(1)
+    x = x0 if k == 0 else torch.randn((x0.shape[0], *st.in_shape), device=device)
+    g_last = None if last else torch.randn((x0.shape[0], *st.out_shape), device=device)
+    staging = st.flat.layout.empty(device)
+    opt._bind(st.flat.layout)
+    opt._ensure_state()
 
-        def unit():
-            out = st.run_forward(st.params, (0, 0), x, 1, check_finite=False)
-            g = loss_and_grad(out, y0, loss_kind)[1] if last else g_last
-            st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0)
-            if predictive and not last:
-                opt.step_predict_(st.flat, 1e-4, 1e-4, len(stages) - k - 1, staging)
-            else:
-                opt.step_(st.flat, 1e-4)
+    def unit():
+        out = st.run_forward(st.params, (0, 0), x, 1, check_finite=False)
+        g = loss_and_grad(out, y0, loss_kind)[1] if last else g_last
+        st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0)
+        if predictive and not last:
+            opt.step_predict_(st.flat, 1e-4, 1e-4, depth - k - 1, staging)
+        else:
+            opt.step_(st.flat, 1e-4)
 
-        opt.eager_checks = False
-        for _ in range(2):
-            unit()
-        torch.cuda.synchronize(device)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            unit()
-        graph.replay()
-        torch.cuda.synchronize(device)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
-            graph.replay()
-        e1.record()
-        torch.cuda.synchronize(device)
-        times.append(e0.elapsed_time(e1) / 1e3 / reps)
-    return times
+    opt.eager_checks = False
+    for _ in range(2):
+        unit()
+    torch.cuda.synchronize(device)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        unit()
+    graph.replay()
+    torch.cuda.synchronize(device)
+    return graph
+
+
+def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 20, trials: int = 5):
+    """Per-stage device time of one mini-batch's work — SURVEY.md §8d's
+    t_f,k + t_b,k (+ t_u,k) — with prediction off (K2 update) and on (K3),
+    each captured in a CUDA graph on THROWAWAY stages from `make()` ->
+    (stages, opts) (replays train them), the two modes replayed in
+    alternation (`reps` replays per sample, median of `trials`) so that drift
+    hits both alike. Returns {"pred_off": [s per stage], "pred_on": [...]}."""
+    import statistics
+
+    out = {"pred_off": [], "pred_on": []}
+    sets = {key: make() for key in out}
+    depth = len(sets["pred_off"][0])
+    for k in range(depth):
+        graphs = {key: _unit_graph(torch, device, k, sets[key][0][k], sets[key][1][k], data, loss_kind,
+                                   key == "pred_on", depth) for key in out}
+        samples = {key: [] for key in out}
+        for _ in range(trials):
+            for key, graph in graphs.items():
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    graph.replay()
+                e1.record()
+                torch.cuda.synchronize(device)
+                samples[key].append(e0.elapsed_time(e1) / 1e3 / reps)
+        for key in out:
+            out[key].append(statistics.median(samples[key]))
+        del graphs
+    return out
 
 
 def pipeline_roofline(stage_times, batch, n, depth, boundary_bytes, link_gbs=770.0):
@@ -171,6 +191,13 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
                      f"fp32 master weights"}
     launches = 0
     pair = _graphed_pair(torch, device, depth, n_batches, data, replays)
+    if with_roofline:
+        def make():
+            st = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), depth, torch_init(7, device), device=device)
+            return st, [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in st]
+
+        units = stage_unit_times(torch, device, make, data, "softmax_xent")
+        boundary = [4 * BATCH * s_.out_dim for s_ in make()[0][:-1]]
     out["serial_streams"] = {}
     for strategy in ("async_raw", "optimizer_prediction"):
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
@@ -189,10 +216,7 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
             _, esec, _ = _run_once(torch, device, strategy, depth, n_batches, data)
             out[key]["eager_samples_per_s"] = round(n_batches * BATCH / esec, 1)
         if with_roofline:
-            stages = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), depth, torch_init(7, device), device=device)
-            opts = [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in stages]
-            t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction")
-            roof = pipeline_roofline(t, BATCH, n_batches, depth, [4 * BATCH * s_.out_dim for s_ in stages[:-1]])
+            roof = pipeline_roofline(units[key], BATCH, n_batches, depth, boundary)
             out[key]["roofline"] = roof
             # serialised stages are bounded by B / sum_k t_k; concurrent stages on
             # one GPU by neither (they share the SMs) — both fractions reported
@@ -241,11 +265,14 @@ def projected_multi_gpu(torch, device, depth: int = 8, n_batches: int = 64, tf32
     data = DeviceBatches(torch, device, dims=dims)
     out = {"config": f"MLP {dims}, B={BATCH}, Adam, D={depth} (one stage per GPU), "
                      f"{'TF32' if tf32 else 'fp32'} GEMMs; projected from per-stage graphed unit times"}
-    for strategy, key in (("async_raw", "pred_off"), ("optimizer_prediction", "pred_on")):
-        stages = build_stages(build_layers(dims, acts), depth, torch_init(11, device), device=device)
-        opts = [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in stages]
-        t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction")
-        out[key] = pipeline_roofline(t, BATCH, n_batches, depth, [4 * BATCH * s_.out_dim for s_ in stages[:-1]])
+    def make():
+        st = build_stages(build_layers(dims, acts), depth, torch_init(11, device), device=device)
+        return st, [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in st]
+
+    units = stage_unit_times(torch, device, make, data, "softmax_xent")
+    boundary = [4 * BATCH * s_.out_dim for s_ in make()[0][:-1]]
+    for key in ("pred_off", "pred_on"):
+        out[key] = pipeline_roofline(units[key], BATCH, n_batches, depth, boundary)
     out["prediction_overhead"] = round(
         1.0 - out["pred_on"]["multi_gpu_samples_per_s"] / out["pred_off"]["multi_gpu_samples_per_s"], 4)
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -371,6 +398,14 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
     finally:
         graphs = g = stages = opts = None  # noqa: F841 (drop the graphs' memory pools)
         torch.cuda.empty_cache()
+    if with_roofline:
+        def make():
+            st, _ = module_stages_for(torch, name, device)
+            kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
+            return st, [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in st]
+
+        units = stage_unit_times(torch, device, make, data, "softmax_xent", reps=3, trials=3)
+        torch.cuda.empty_cache()
     for strategy in ("async_raw", "optimizer_prediction"):
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
         if with_eager:
@@ -384,18 +419,12 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
             out[key]["eager_serial_samples_per_s"] = round(n_batches * cfg["batch"] / (e0.elapsed_time(e1) / 1e3), 2)
             del stages, opts
         if with_roofline:
-            stages, _ = module_stages_for(torch, name, device)
-            kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
-            opts = [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in stages]
-            t = stage_unit_times(torch, device, stages, opts, data, "softmax_xent", strategy == "optimizer_prediction",
-                                 reps=5)
-            roof = pipeline_roofline(t, cfg["batch"], n_batches, cfg["depth"], out["boundary_bytes"])
+            roof = pipeline_roofline(units[key], cfg["batch"], n_batches, cfg["depth"], out["boundary_bytes"])
             out[key]["roofline"] = roof
             out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] /
                                                             roof["single_gpu_samples_per_s"], 4)
             out[key]["frac_of_multi_gpu_roofline"] = round(out[key]["samples_per_s"] /
                                                            roof["multi_gpu_samples_per_s"], 4)
-            del stages, opts
         torch.cuda.empty_cache()
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4))

@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--strategy", default="optimizer_prediction")
 ap.add_argument("--n", type=int, default=16)
 ap.add_argument("--tf32", action="store_true")
+ap.add_argument("--streams", default="stage", choices=["stage", "serial"])
 a = ap.parse_args()
 torch.backends.cuda.matmul.allow_tf32 = a.tf32
 dev = torch.device("cuda", 0)
@@ -29,7 +30,7 @@ data = DeviceBatches(torch, dev)
 stages = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), 4, torch_init(0, dev), device=dev)
 opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=dev) for s in stages]
 g = GraphedExecute(build_timeline(a.strategy, 4, a.n), stages, opts, a.strategy, data, "softmax_xent",
-                   lambda mb: 1e-4, warmup_runs=1)
+                   lambda mb: 1e-4, warmup_runs=1, streams=a.streams)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
 g.replay()
