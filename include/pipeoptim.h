@@ -193,6 +193,15 @@ int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void
 int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t rows, int64_t cols, float* grad,
                  float* loss, float* scratch, void* stream);
 
+/* Backward elementwise part of a ReLU layer fused with its bias gradient
+ * (stages.py:200-206, linalg.py:185-194): dpre = g * (pre > 0) written to
+ * dpre, and db = colsum(dpre) (accumulate != 0: db += colsum). h is the
+ * layer's OUTPUT relu(pre) (relu(pre) > 0 <=> pre > 0, so the stash keeps h).
+ * g, h, dpre: row-major [rows x cols]; db: [cols]. Deterministic (fixed
+ * summation order); g may alias dpre. */
+int po_relu_bwd_bias(const float* g, const float* h, int64_t rows, int64_t cols, float* dpre, float* db,
+                     int32_t accumulate, void* stream);
+
 /* ---- live-weight LSTM cell (pipeoptim_lstm.cu) --------------------------
  * One time step of an LSTM layer whose GEMMs run in cuBLAS (PyTorch gate
  * order i, f, g, o; hidden % 4 == 0; all pointers 16-byte aligned). Used by

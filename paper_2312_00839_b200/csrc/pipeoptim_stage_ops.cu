@@ -10,6 +10,10 @@
 //   po_loss_grad    softmax cross-entropy or MSE loss AND its gradient
 //                   (linalg.py:212-241), the loss reduced in a fixed order by
 //                   the last CTA to finish (deterministic, no float atomics).
+//   po_relu_bwd_bias  a ReLU layer's backward elementwise part AND its bias
+//                   gradient: dpre = g * (h > 0), db (+)= colsum(dpre)
+//                   (stages.py:200-206) — replaces compare + multiply +
+//                   column-sum (3 launches, dpre written then re-read).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -121,6 +125,37 @@ __global__ void loss_grad_kernel(const float* __restrict__ pred, const float* __
   }
 }
 
+// One CTA per 32 columns; warp w walks rows w, w + nwarps, ... with lane =
+// column (128-byte coalesced rows), keeps its column partial in a register,
+// then the warps' partials are summed in warp order through shared memory:
+// a fixed reduction order, so the bias gradient is deterministic.
+constexpr int kReluWarps = 8;
+
+// g and dpre may alias (each element is read, then written, by one thread)
+__global__ void relu_bwd_bias_kernel(const float* g, const float* __restrict__ h, int64_t rows, int64_t cols,
+                                     float* dpre, float* __restrict__ db, int accumulate) {
+  __shared__ float part[kReluWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  float acc = 0.f;
+  if (c < cols) {
+    for (int64_t r = w; r < rows; r += kReluWarps) {
+      const int64_t i = r * cols + c;
+      const float v = h[i] > 0.f ? g[i] : 0.f;  // g * (pre > 0): relu(pre) > 0 <=> pre > 0
+      dpre[i] = v;
+      acc += v;
+    }
+  }
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kReluWarps; ++k) s += part[k][lane];
+    db[c] = accumulate ? db[c] + s : s;
+  }
+}
+
 int sm_count_ops() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -140,6 +175,25 @@ int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void
   int64_t want = (n / 4 + block - 1) / block;
   int64_t grid = want < 1 ? 1 : (want > 4 * sms ? 4 * sms : want);
   all_finite_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(x, n, flags, index);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+int po_relu_bwd_bias(const float* g, const float* h, int64_t rows, int64_t cols, float* dpre, float* db,
+                     int32_t accumulate, void* stream) {
+  if (rows < 0 || cols < 0) return PO_EINVAL;
+  if (rows == 0 || cols == 0) {
+    if (cols > 0 && !accumulate && db != nullptr) {
+      cudaError_t e = cudaMemsetAsync(db, 0, (size_t)cols * sizeof(float), (cudaStream_t)stream);
+      return e == cudaSuccess ? 0 : (int)e;
+    }
+    return 0;
+  }
+  if (g == nullptr || h == nullptr || dpre == nullptr || db == nullptr) return PO_EINVAL;
+  const int64_t grid = (cols + 31) / 32;
+  if (grid > 0x7fffffff) return PO_EINVAL;
+  relu_bwd_bias_kernel<<<(unsigned)grid, 32 * kReluWarps, 0, (cudaStream_t)stream>>>(g, h, rows, cols, dpre, db,
+                                                                                     accumulate);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }

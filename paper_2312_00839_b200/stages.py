@@ -228,10 +228,17 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
         raise DimensionError(f"stage {stage.rank}: input has {x.shape[1]} cols, expected {stage.in_dim}")
     inputs, pres = [], []
     h = x
+    fused = x.is_cuda
     for i, spec in enumerate(stage.layers):
         w, b = weights[2 * i], weights[2 * i + 1]
         inputs.append(h)
-        pre = torch.addmm(b, h, w)
+        if fused and spec.activation == "relu":
+            # bias + ReLU in the GEMM epilogue (cuBLASLt); the stash keeps
+            # relu(pre) — its sign pattern is pre's, all the backward needs
+            h = torch._addmm_activation(b.view(-1), h, w)
+            pres.append(h)
+            continue
+        pre = torch.addmm(b.view(-1), h, w) if fused else torch.addmm(b, h, w)
         pres.append(pre)
         h = _activate(pre, spec.activation)
     if check_finite:
@@ -271,15 +278,31 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
     g = grad_out
     for i in reversed(range(len(stage.layers))):
         spec = stage.layers[i]
-        dpre = _activation_grad_mul(g, entry.pre_acts[i], spec.activation)
         x = entry.layer_inputs[i]
         gw, gb = gviews[2 * i], gviews[2 * i + 1]
-        if accumulate:
-            gw.addmm_(x.t(), dpre)
-            gb.add_(dpre.sum(dim=0, keepdim=True))
+        if g.is_cuda and spec.activation == "relu":
+            # dpre = g * (pre > 0) and db = colsum(dpre) in one launch
+            from . import _lib
+
+            gc = g if g.is_contiguous() else g.contiguous()
+            dpre = torch.empty_like(gc)
+            rows, cols = gc.shape
+            rc = _lib.load().po_relu_bwd_bias(gc.data_ptr(), entry.pre_acts[i].data_ptr(), rows, cols,
+                                              dpre.data_ptr(), gb.data_ptr(), int(accumulate),
+                                              torch.cuda.current_stream(g.device).cuda_stream)
+            _lib.check(rc, "po_relu_bwd_bias")
+            if accumulate:
+                gw.addmm_(x.t(), dpre)
+            else:
+                torch.mm(x.t(), dpre, out=gw)
         else:
-            torch.mm(x.t(), dpre, out=gw)
-            torch.sum(dpre, dim=0, keepdim=True, out=gb)
+            dpre = _activation_grad_mul(g, entry.pre_acts[i], spec.activation)
+            if accumulate:
+                gw.addmm_(x.t(), dpre)
+                gb.add_(dpre.sum(dim=0, keepdim=True))
+            else:
+                torch.mm(x.t(), dpre, out=gw)
+                torch.sum(dpre, dim=0, keepdim=True, out=gb)
         if i > 0 or need_input_grad:
             g = torch.mm(dpre, weights[2 * i].t())
         else:

@@ -340,6 +340,34 @@ def test_fused_loss_grad_matches_reference_formulas(kind, rows, cols):
         assert R.inf_norm_rel(host(grad), want_grad) <= 2e-6
 
 
+@pytest.mark.parametrize("rows,cols,accumulate,alias", [(128, 1024, 0, False), (128, 1024, 1, False),
+                                                        (7, 33, 0, True), (1, 1, 1, False), (300, 70, 0, False),
+                                                        (0, 5, 0, False), (0, 5, 1, False)])
+def test_relu_bwd_bias_matches_reference(rows, cols, accumulate, alias):
+    """po_relu_bwd_bias: dpre = g * (pre > 0) exactly (a select), and
+    db (+)= colsum(dpre) vs a float64 column sum (stages.py:200-206)."""
+    import torch
+
+    from paper_2312_00839_b200 import _lib
+
+    rng = np.random.default_rng(rows * 1000 + cols)
+    g = rng.normal(size=(rows, cols)).astype(np.float32)
+    pre = rng.normal(size=(rows, cols)).astype(np.float32)
+    pre[rng.random((rows, cols)) < 0.1] = 0.0  # relu'(0) = 0 in the reference
+    h = np.maximum(pre, 0.0)
+    db0 = rng.normal(size=cols).astype(np.float32)
+    gd, hd = torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda()
+    dpre = gd if alias else torch.empty_like(gd)
+    db = torch.from_numpy(db0).cuda()
+    rc = _lib.load().po_relu_bwd_bias(gd.data_ptr(), hd.data_ptr(), rows, cols, dpre.data_ptr(), db.data_ptr(),
+                                      accumulate, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    want = g * (pre > 0)
+    assert np.array_equal(host(dpre), want)
+    want_db = want.astype(np.float64).sum(axis=0) + (db0.astype(np.float64) if accumulate else 0.0)
+    np.testing.assert_allclose(host(db), want_db, rtol=1e-5, atol=1e-5)
+
+
 def test_more_than_2_31_elements(lib):
     """64-bit indexing: a 2^31 + 13 element stage (8 GB per buffer); K3 checked
     bit-exact against the fp32 emulation on the first and last 2^20 elements."""
