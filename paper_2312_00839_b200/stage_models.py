@@ -297,6 +297,12 @@ class _GridSafeBatchNorm2d(nn.BatchNorm2d):
             torch.backends.cudnn.enabled = prev
 
 
+def _use_grid_safe_bn(module: nn.Module) -> None:
+    for m in module.modules():
+        if type(m) is nn.BatchNorm2d:
+            m.__class__ = _GridSafeBatchNorm2d
+
+
 class ModuleStage:
     """A pipeline stage made of torch modules over a flat parameter buffer.
 
@@ -316,9 +322,7 @@ class ModuleStage:
         self.device = torch.device(device)
         self.module = nn.Sequential(*blocks).to(self.device)
         self.module.train()
-        for m in self.module.modules():
-            if type(m) is nn.BatchNorm2d:
-                m.__class__ = _GridSafeBatchNorm2d
+        _use_grid_safe_bn(self.module)
         named = list(self.module.named_parameters())
         self._params = [p for _, p in named]
         self.param_names = [n for n, _ in named]
@@ -394,8 +398,8 @@ class ModuleStage:
         return g_in, self.flat.grads
 
 
-def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32, reps=3,
-                        channels_last: bool = False) -> list[float]:
+def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32, reps=7,
+                        channels_last: bool = False, warmup: int = 2) -> list[float]:
     """Per-block forward+backward time on the device for one batch (a tiny
     profiling partitioner, in the spirit of PipeDream's), used to balance
     stages by time instead of parameter count."""
@@ -409,6 +413,10 @@ def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32,
     for b in blocks:
         b.to(dev).train()
         xin = x.detach().requires_grad_(x.is_floating_point())
+        _use_grid_safe_bn(b)  # profile the kernels the stages will run
+        for _ in range(warmup):  # cuDNN/cuBLAS algorithm selection, lazy allocations
+            y = b(xin)
+            y.backward(torch.ones_like(y))
         times = []
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
