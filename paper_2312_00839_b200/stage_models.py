@@ -16,9 +16,14 @@ Convolution and batch-norm autograd nodes save the parameter object itself,
 so their input gradients use the live weights at backward time, as the
 reference does; `nn.Linear` would save a transposed view of the forward-time
 storage, so linear layers use `LiveLinear`, whose backward reads the live
-weight explicitly. (cuDNN LSTMs save their own packed copy: LSTM stages
-therefore back-propagate through the forward-time weights — a documented
-deviation the reference cannot pin, it has no LSTM.)
+weight explicitly; LSTM layers use `LiveLSTM` (cuBLAS GEMMs + the
+po_lstm_cell_fwd/bwd kernels), whose backward propagates through the live
+weights (cuDNN's LSTM would keep its own packed forward-time copy).
+
+Image stages can run NHWC inside the stage (`channels_last=True`; boundary
+tensors stay NCHW), and their batch norms run on PyTorch's native kernels:
+cuDNN's training batch-norm kernels synchronise across their grid and can
+deadlock when two stages run concurrently on one GPU (runtime streams="stage").
 """
 
 from __future__ import annotations
