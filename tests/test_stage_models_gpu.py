@@ -117,3 +117,50 @@ def test_channels_last_stage_matches_nchw(name):
     # ResNet output, ~1e-5 elementwise typical; a layout bug would be O(1)
     for a, b in ((o0, o1), (gi0, gi1), (gf0, gf1)):
         assert float((a - b).norm()) <= 1e-3 * float(b.norm())
+
+
+@pytest.mark.parametrize("name,kind", [("config2_vgg16", "sgdm"), ("config4_gnmt8", "adam")])
+def test_module_stages_graphed_stage_streams_equal_eager_serial(name, kind):
+    """Module stages through GraphedExecute(streams="stage") — the configs 2-4
+    bench path — replay to the same losses and weights as eager serial runs
+    (deterministic cuDNN algorithms)."""
+    import torch
+
+    from paper_2312_00839_b200.bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import GraphedExecute, build_timeline, execute
+
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dev = torch.device("cuda", 0)
+    cfg = dict(MODULE_CONFIGS[name], batch=8)
+    if name == "config4_gnmt8":
+        cfg["in_shape"] = (6,)
+    data = ModuleBatches(torch, dev, cfg)
+    costs = [1.0] * 10
+    runs = {}
+    for mode in ("eager", "graphed"):
+        stages, _ = module_stages_for(torch, name, dev, depth=4, costs=costs if name == "config4_gnmt8" else None)
+        opts = [OptimizerState(OptimizerConfig(kind), s.param_names, device=dev) for s in stages]
+        tl = build_timeline("optimizer_prediction", 4, 7)
+        if mode == "eager":
+            losses = []
+            for _ in range(3):
+                for s in stages:
+                    s.version = 1
+                losses.append(execute(tl, stages, opts, "optimizer_prediction", data, "softmax_xent",
+                                      lambda mb: 1e-3, checks="deferred").losses)
+        else:
+            g = GraphedExecute(tl, stages, opts, "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-3,
+                               streams="stage")
+            losses = [None]
+            for _ in range(2):
+                g.replay()
+                losses.append(g.report().losses)
+        torch.cuda.synchronize()
+        runs[mode] = (losses[1:], [s.flat.data.clone() for s in stages])
+    np.testing.assert_allclose(runs["graphed"][0], runs["eager"][0], rtol=1e-5, atol=1e-6)
+    for a, b in zip(runs["graphed"][1], runs["eager"][1]):
+        assert float((a - b).abs().max()) <= 1e-5 * float(b.abs().max()) + 1e-7
