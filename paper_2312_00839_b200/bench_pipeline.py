@@ -76,7 +76,7 @@ def _time_replays(torch, device, g, replays):
     return e0.elapsed_time(e1) / 1e3 / replays
 
 
-def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=5, streams=("stage", "serial")):
+def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=9, streams=("stage", "serial")):
     """Prediction off/on graphs (per stream mode) timed in alternation (median
     of `trials`), so clock and thermal drift hit every arm alike."""
     import statistics

@@ -1,4 +1,4 @@
-"""Configs 2-3 on the device (SURVEY.md §8c "Configs 2-4"): the reference has
+"""Configs 2-4 on the device (SURVEY.md §8c "Configs 2-4"): the reference has
 no conv/LSTM stages, so what is pinned is (a) K3 on each stage's REAL flat
 buffers vs the oracle on the same fp32 values, (b) the schedule/version
 records (model-independent) vs the oracle, (c) the S9 weight views."""
@@ -24,7 +24,8 @@ def _oracle_records(depth, n, strategy):
     return [tuple(r) for r in out["records"]]
 
 
-@pytest.mark.parametrize("name,kind", [("config2_vgg16", "sgdm"), ("config3_resnet101", "adamw")])
+@pytest.mark.parametrize("name,kind", [("config2_vgg16", "sgdm"), ("config3_resnet101", "adamw"),
+                                       ("config4_gnmt8", "adam")])
 def test_stage_buffers_k3_parity_and_records(name, kind):
     import torch
 
@@ -34,7 +35,8 @@ def test_stage_buffers_k3_parity_and_records(name, kind):
 
     dev = torch.device("cuda", 0)
     cfg = dict(MODULE_CONFIGS[name], batch=8)
-    stages, _ = module_stages_for(torch, name, dev)
+    costs = [1.0] * 10 if name == "config4_gnmt8" else None  # GNMT: embed, 8 LSTMs, head
+    stages, _ = module_stages_for(torch, name, dev, costs=costs)
     opts = [OptimizerState(OptimizerConfig(kind), s.param_names, device=dev) for s in stages]
     D, n = len(stages), len(stages) + 2
     rep = execute(build_timeline("optimizer_prediction", D, n), stages, opts, "optimizer_prediction",
