@@ -466,6 +466,11 @@ def pipeline_leg(args, torch, dist, rank, world, device):
             try:
                 if world == 1:
                     configs[name] = bp.single_gpu_module_pipeline(torch, device, name, n_batches=16)
+                    if bp.MODULE_CONFIGS[name].get("channels_last"):  # conv configs: bf16 stage compute too
+                        b = bp.single_gpu_module_pipeline(torch, device, name, n_batches=16, amp="bf16",
+                                                          with_eager=False, with_roofline=False)
+                        configs[name]["bf16"] = {k: b[k] for k in ("config", "pred_off", "pred_on",
+                                                                   "prediction_overhead")}
                 else:
                     configs[name] = bench_module_pipeline(torch, dist, rank, world, device, name, n_batches=16,
                                                           host_staging=args.dist_backend != "nccl")

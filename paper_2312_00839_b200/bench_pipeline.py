@@ -330,7 +330,7 @@ def module_block_costs(torch, name, device):
     return _COSTS[name]
 
 
-def module_stages_for(torch, name, device, depth=None, costs=None):
+def module_stages_for(torch, name, device, depth=None, costs=None, amp=None):
     from .stage_models import build_module_stages
 
     cfg = MODULE_CONFIGS[name]
@@ -339,23 +339,24 @@ def module_stages_for(torch, name, device, depth=None, costs=None):
     costs = costs if costs is not None else module_block_costs(torch, name, device)
     torch.manual_seed(0)
     blocks = make_blocks(cfg["blocks"], cfg["classes"])
+    amp_dtype = {None: None, "bf16": torch.bfloat16}[amp]
     return build_module_stages(blocks, depth, device, cfg["in_shape"], costs=costs, in_dtype=in_dtype,
-                               channels_last=cfg.get("channels_last", False)), costs
+                               channels_last=cfg.get("channels_last", False), amp_dtype=amp_dtype), costs
 
 
-def _module_setup(torch, device, name, strategy, n_batches):
+def _module_setup(torch, device, name, strategy, n_batches, amp=None):
     from .optim import OptimizerConfig, OptimizerState
     from .runtime import build_timeline
 
     cfg = MODULE_CONFIGS[name]
-    stages, _ = module_stages_for(torch, name, device)
+    stages, _ = module_stages_for(torch, name, device, amp=amp)
     kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
     opts = [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in stages]
     return stages, opts, build_timeline(strategy, cfg["depth"], n_batches)
 
 
 def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf32: bool = True, trials: int = 3,
-                               with_eager: bool = True, with_roofline: bool = True):
+                               with_eager: bool = True, with_roofline: bool = True, amp: str | None = None):
     """Configs 2-4 through the single-GPU 1F1B runner (all D stages on one
     GPU). Headline: whole n_batches-mini-batch runs captured into CUDA graphs
     with one stream per stage (`GraphedExecute(streams="stage")`), prediction
@@ -374,11 +375,13 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
     lr = cfg["lr"]
     out = {"config": f"{name}: D={cfg['depth']} stages on 1 GPU (single-process runner, one CUDA stream per stage, "
                      f"CUDA-graph replay of whole {n_batches}-mini-batch runs), batch {cfg['batch']}, "
-                     f"{cfg['opt']} lr {lr}, {'TF32' if tf32 else 'fp32'} convs/GEMMs, fp32 master weights"}
+                     f"{cfg['opt']} lr {lr}, "
+                     f"{'bf16 autocast' if amp == 'bf16' else 'TF32' if tf32 else 'fp32'} convs/GEMMs, "
+                     f"fp32 master weights"}
     try:
         graphs = {}
         for strategy in ("async_raw", "optimizer_prediction"):
-            stages, opts, tl = _module_setup(torch, device, name, strategy, n_batches)
+            stages, opts, tl = _module_setup(torch, device, name, strategy, n_batches, amp)
             graphs[strategy] = (GraphedExecute(tl, stages, opts, strategy, data, "softmax_xent", lambda mb: lr,
                                                warmup_runs=1, streams="stage"), stages)
             graphs[strategy][0].replay()
@@ -400,7 +403,7 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
         torch.cuda.empty_cache()
     if with_roofline:
         def make():
-            st, _ = module_stages_for(torch, name, device)
+            st, _ = module_stages_for(torch, name, device, amp=amp)
             kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
             return st, [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in st]
 
@@ -409,7 +412,7 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
     for strategy in ("async_raw", "optimizer_prediction"):
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
         if with_eager:
-            stages, opts, tl = _module_setup(torch, device, name, strategy, n_batches)
+            stages, opts, tl = _module_setup(torch, device, name, strategy, n_batches, amp)
             torch.cuda.synchronize(device)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()

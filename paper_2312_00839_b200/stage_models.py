@@ -41,28 +41,39 @@ from .stages import ActivationStash, StashEntry, record_finite
 
 
 class _LiveLinearFn(torch.autograd.Function):
-    """y = x W^T + b; backward: dx = g W_live, dW = g^T x, db = colsum(g)."""
+    """y = x W^T + b; backward: dx = g W_live, dW = g^T x, db = colsum(g).
+    `dt` (autocast): the forward computes in dt from dt casts of x, W, b; the
+    backward multiplies by the LIVE weight cast to dt; autograd returns the
+    parameter gradients to the fp32 flat buffer in fp32."""
 
     @staticmethod
-    def forward(ctx, x, weight, bias, module):
+    def forward(ctx, x, weight, bias, module, dt=None):
         ctx.save_for_backward(x)
-        ctx.module = module
+        ctx.module, ctx.dt = module, dt
+        if dt is not None:
+            return F.linear(x, weight.to(dt), None if bias is None else bias.to(dt))
         return F.linear(x, weight, bias)
 
     @staticmethod
     def backward(ctx, g):
         (x,) = ctx.saved_tensors
         w_live = ctx.module.weight  # points at the live buffer again by now
+        if ctx.dt is not None:
+            w_live = w_live.to(ctx.dt)
         gx = g.matmul(w_live)
         g2 = g.reshape(-1, g.shape[-1])
         x2 = x.reshape(-1, x.shape[-1])
         gw = g2.t().matmul(x2)
         gb = g2.sum(0) if ctx.module.bias is not None else None
-        return gx, gw, gb, None
+        return gx, gw, gb, None, None
 
 
 class LiveLinear(nn.Linear):
     def forward(self, x):
+        if x.is_cuda and torch.is_autocast_enabled("cuda"):
+            dt = torch.get_autocast_dtype("cuda")
+            with torch.autocast("cuda", enabled=False):
+                return _LiveLinearFn.apply(x.to(dt), self.weight, self.bias, self, dt)
         return _LiveLinearFn.apply(x, self.weight, self.bias, self)
 
 
@@ -317,13 +328,17 @@ class ModuleStage:
     """
 
     def __init__(self, rank: int, blocks: list[nn.Module], device, in_shape: tuple, in_dtype=torch.float32,
-                 channels_last: bool = False):
+                 channels_last: bool = False, amp_dtype=None):
         """channels_last=True runs the stage's image tensors in NHWC inside the
         stage (cuDNN's native tensor-core layout); boundary activations and
         gradients stay NCHW-contiguous, so transports and the other stages are
-        unaffected. Parameters keep their flat NCHW views either way."""
+        unaffected. Parameters keep their flat NCHW views either way.
+        amp_dtype (e.g. torch.bfloat16): the stage's forward runs under
+        autocast in that dtype (tensor-core convs/GEMMs); the parameters,
+        gradients, optimizer state and boundary tensors stay fp32."""
         self.rank = rank
         self.channels_last = channels_last
+        self.amp_dtype = amp_dtype
         self.device = torch.device(device)
         self.module = nn.Sequential(*blocks).to(self.device)
         self.module.train()
@@ -376,7 +391,14 @@ class ModuleStage:
                 h = x_in
                 if self.channels_last and h.dim() == 4:
                     h = h.contiguous(memory_format=torch.channels_last)
-                out = self.module(h)
+                if self.amp_dtype is not None:
+                    # no cast cache: the parameters are re-pointed every forward
+                    # (and the forward may be captured into a CUDA graph)
+                    with torch.autocast("cuda", dtype=self.amp_dtype, cache_enabled=False):
+                        out = self.module(h)
+                    out = out.float()
+                else:
+                    out = self.module(h)
                 if not out.is_contiguous():
                     out = out.contiguous()
         finally:
@@ -441,14 +463,14 @@ def profile_block_costs(blocks, in_shape, batch, device, in_dtype=torch.float32,
 
 
 def build_module_stages(blocks, depth, device, in_shape, costs=None, in_dtype=torch.float32,
-                        channels_last: bool = False):
+                        channels_last: bool = False, amp_dtype=None):
     """Partition `blocks` into `depth` contiguous stages balanced by `costs`
     (default: parameter counts) and build them in order."""
     costs = costs if costs is not None else [max(1, c) for c in block_param_counts(blocks)]
     ranges = balanced_partition(costs, depth)
     stages, shape, dtype = [], tuple(in_shape), in_dtype
     for k, (lo, hi) in enumerate(ranges):
-        st = ModuleStage(k, blocks[lo:hi], device, shape, dtype, channels_last=channels_last)
+        st = ModuleStage(k, blocks[lo:hi], device, shape, dtype, channels_last=channels_last, amp_dtype=amp_dtype)
         stages.append(st)
         shape, dtype = st.out_shape, torch.float32
     return stages

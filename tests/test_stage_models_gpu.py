@@ -166,3 +166,37 @@ def test_module_stages_graphed_stage_streams_equal_eager_serial(name, kind):
     np.testing.assert_allclose(runs["graphed"][0], runs["eager"][0], rtol=1e-5, atol=1e-6)
     for a, b in zip(runs["graphed"][1], runs["eager"][1]):
         assert float((a - b).abs().max()) <= 1e-5 * float(b.abs().max()) + 1e-7
+
+
+def test_bf16_autocast_stage_keeps_fp32_master_and_live_weight_backward():
+    """amp_dtype=bf16: the forward computes in bf16 (tensor cores), the
+    boundary tensors, parameter gradients and flat buffers stay fp32, and the
+    LiveLinear input gradient uses the LIVE weight (S9) under autocast too."""
+    import copy
+
+    import torch
+
+    from paper_2312_00839_b200.stage_models import ModuleStage, vgg16_cifar_blocks
+
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(0)
+    blocks = vgg16_cifar_blocks(10)[-2:]
+    ref_blocks = copy.deepcopy(blocks)
+    st = ModuleStage(3, blocks, dev, (512, 1, 1), channels_last=True, amp_dtype=torch.bfloat16)
+    ref = ModuleStage(3, ref_blocks, dev, (512, 1, 1))
+    ref.flat.data.copy_(st.flat.data)
+    x = torch.randn(16, 512, 1, 1, device=dev)
+    w_hat = st.flat.data + 0.01 * torch.randn_like(st.flat.data)
+    views = st.flat.layout.views(w_hat)
+    out = st.run_forward(views, (1, 0), x, 1)
+    assert out.dtype == torch.float32
+    ref_out = ref.run_forward(ref.flat.layout.views(w_hat.clone()), (1, 0), x, 1)
+    assert float((out - ref_out).norm()) <= 2e-2 * float(ref_out.norm())
+    g = torch.randn_like(out)
+    g_in, _ = st.run_backward(st.params, (1, 0), g)
+    ref_in, _ = ref.run_backward(ref.params, (1, 0), g)
+    assert g_in.dtype == torch.float32 and st.flat.grad.dtype == torch.float32
+    # bf16 rounding through two layers (ReLU masks flip near 0): measured
+    # 3.7e-2; backpropagating through W_hat instead of W would be ~25% off
+    assert float((g_in - ref_in).norm()) <= 6e-2 * float(ref_in.norm())
+    assert float((st.flat.grad - ref.flat.grad).norm()) <= 6e-2 * float(ref.flat.grad.norm())
