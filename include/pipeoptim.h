@@ -202,6 +202,29 @@ int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t r
 int po_relu_bwd_bias(const float* g, const float* h, int64_t rows, int64_t cols, float* dpre, float* db,
                      int32_t accumulate, void* stream);
 
+/* ---- peer-memory boundary transport (pipeoptim_p2p.cu) ------------------
+ * Replaces the simulated hand-off dicts of the reference executor
+ * (runtime.py:390-391, 420-433): one direction of a pipeline boundary is a
+ * ring of `slots` message buffers of slot_elems floats on the RECEIVING GPU,
+ * mapped into the sender (CUDA IPC). ctl is a zeroed int64[4] control block
+ * local to each rank (sent count + arrival counter, received count + arrival
+ * counter); flags are int64 counters, monotonic, zero-initialised. Both calls
+ * are stream-ordered, host-free and CUDA-graph capturable; a wait that
+ * exceeds timeout_ms sets *status = 1 and the transfer is skipped (no hang).
+ * slot_elems % 4 == 0. */
+
+/* Wait for ring credit (*ack_flag >= sent + 1 - slots), store src[0..n) into
+ * peer_ring[sent % slots], then release-store *peer_ready_flag = ++sent. */
+int po_p2p_send(const float* src, int64_t n, float* peer_ring, int64_t slot_elems, int32_t slots, int64_t* ctl,
+                const int64_t* ack_flag, int64_t* peer_ready_flag, int64_t timeout_ms, int32_t* status,
+                void* stream);
+
+/* Wait for the next message (*ready_flag >= recvd + 1), copy ring[recvd % slots]
+ * into dst[0..n), then release-store *peer_ack_flag = ++recvd. */
+int po_p2p_recv(const float* ring, int64_t slot_elems, int32_t slots, float* dst, int64_t n, int64_t* ctl,
+                const int64_t* ready_flag, int64_t* peer_ack_flag, int64_t timeout_ms, int32_t* status,
+                void* stream);
+
 /* ---- live-weight LSTM cell (pipeoptim_lstm.cu) --------------------------
  * One time step of an LSTM layer whose GEMMs run in cuBLAS (PyTorch gate
  * order i, f, g, o; hidden % 4 == 0; all pointers 16-byte aligned). Used by

@@ -36,6 +36,8 @@ EXPORTS = (
     "po_relu_bwd_bias",
     "po_dp_signal",
     "po_step_predict_dp",
+    "po_p2p_send",
+    "po_p2p_recv",
     "po_lstm_cell_fwd",
     "po_lstm_cell_bwd",
 )
@@ -106,6 +108,8 @@ _SIGNATURES = {
     "po_dp_signal": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _P]),
     "po_step_predict_dp": (ctypes.c_int, [_HP, _P, _P, ctypes.c_int32, _P, _P, _P, _I64, _D, _D, _I64, _P, _P, _I64,
                                           _I64, _P, _P]),
+    "po_p2p_send": (ctypes.c_int, [_P, _I64, _P, _I64, ctypes.c_int32, _P, _P, _P, _I64, _P, _P]),
+    "po_p2p_recv": (ctypes.c_int, [_P, _I64, ctypes.c_int32, _P, _I64, _P, _P, _P, _I64, _P, _P]),
     "po_lstm_cell_fwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
     "po_lstm_cell_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _I64, _I64, _P]),
 }

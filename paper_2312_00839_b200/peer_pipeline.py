@@ -1,0 +1,323 @@
+"""One-process-per-GPU 1F1B runner whose boundary tensors move by peer-memory
+stores (NVLink / NVSwitch) instead of host-driven NCCL calls, so a rank's
+whole run is one stream of device work — captured into ONE CUDA graph and
+replayed with no host involvement.
+
+Same program, policies, version bookkeeping and kernels as the NCCL runner
+(`pipeline.PipelineStageRunner`): rank k executes `stage_program(tl, k)`,
+i.e. the reference's `tl.stage_events(k)` order (pkg/src/pipesim/
+schedule.py:80-81), which the reference simulates in one thread with
+hand-off dicts (runtime.py:390-391, 420-433). Here each hand-off direction
+of a boundary is a ring on the receiving GPU (csrc/pipeoptim_p2p.cu):
+`po_p2p_send` stores the tensor into the peer's ring slot and release-stores
+the peer's ready counter; `po_p2p_recv` waits for it, copies the slot into a
+fresh input buffer (kept by the stash until the backward) and release-stores
+the sender's ack counter (ring credit).
+
+Deadlock freedom: a ring has `slots` = 1 + the most messages ever in flight
+on that link in the reference's global event order (`ring_slots`). Then the
+globally-earliest pending op of any blocked configuration can always
+proceed — its message was produced earlier in that order, and the credit it
+needs was returned earlier in it — so ranks never wait on each other in a
+cycle.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import torch
+
+from . import _lib
+from .errors import NumericError
+from .optim import CoefTape, MbLr
+from .pipeline import StageReport
+from .runtime import PREDICTIVE_STRATEGIES, STRATEGY_SCHEDULE, VersionRecord, _make_policy, _StageRt, _to_device
+from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
+from .stages import loss_and_grad
+
+# flag word offsets in each rank's int64 flag block
+_ACT_READY, _GRAD_READY, _ACT_ACK, _GRAD_ACK = 0, 1, 2, 3
+
+
+def ring_slots(tl: Timeline) -> dict[tuple[str, int], int]:
+    """1 + the most messages simultaneously in flight per link in the global
+    event order: ("act", k) is stage k -> k+1 (produced by F(m, k), consumed
+    by F(m, k+1)); ("grad", k) is stage k+1 -> k (B(m, k+1) -> B(m, k))."""
+    live: dict[tuple[str, int], int] = {}
+    peak: dict[tuple[str, int], int] = {}
+
+    def bump(key, d):
+        live[key] = live.get(key, 0) + d
+        peak[key] = max(peak.get(key, 0), live[key])
+
+    for e in tl.events:
+        if e.kind == FORWARD:
+            if e.stage > 0:
+                bump(("act", e.stage - 1), -1)
+            if e.stage < tl.depth - 1:
+                bump(("act", e.stage), +1)
+        elif e.kind == BACKWARD:
+            if e.stage < tl.depth - 1:
+                bump(("grad", e.stage), -1)
+            if e.stage > 0:
+                bump(("grad", e.stage - 1), +1)
+    return {k: v + 1 for k, v in peak.items()}
+
+
+def _slot_elems(rows: int, shape: tuple) -> int:
+    n = rows * math.prod(shape)
+    return (n + 63) // 64 * 64  # 256-byte aligned slots
+
+
+class PeerLinks:
+    """This rank's rings, flags and control blocks, and its neighbours' peer
+    mappings (CUDA IPC handles exchanged with one object all-gather)."""
+
+    def __init__(self, dist, rank: int, depth: int, rows: int, in_shape: tuple, out_shape: tuple, slots: dict,
+                 device, group=None, stage_ranks: list[int] | None = None, timeout_ms: int = 60_000):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.rank, self.depth, self.device = rank, depth, torch.device(device)
+        self.timeout_ms = timeout_ms
+        self.in_elems = rows * math.prod(in_shape)
+        self.out_elems = rows * math.prod(out_shape)
+        self.in_shape, self.out_shape, self.rows = tuple(in_shape), tuple(out_shape), rows
+        dev = self.device
+        self.flags = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.ctl_act = torch.zeros(4, dtype=torch.int64, device=dev)   # [sent to k+1, arr, recvd from k-1, arr]
+        self.ctl_grad = torch.zeros(4, dtype=torch.int64, device=dev)  # [sent to k-1, arr, recvd from k+1, arr]
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        # rings this rank RECEIVES into (stage k-1's activations, stage k+1's
+        # gradients) and the geometry of the neighbours' rings it SENDS into
+        # (same rule on both sides: the receiver's in_shape is the sender's out_shape)
+        self.act_slots = slots.get(("act", rank - 1), 1)
+        self.grad_slots = slots.get(("grad", rank), 1)
+        self.act_slot_elems = _slot_elems(rows, in_shape)
+        self.grad_slot_elems = _slot_elems(rows, out_shape)
+        self.next_act_slots = slots.get(("act", rank), 1)
+        self.next_act_slot_elems = _slot_elems(rows, out_shape)
+        self.prev_grad_slots = slots.get(("grad", rank - 1), 1)
+        self.prev_grad_slot_elems = _slot_elems(rows, in_shape)
+        self.act_ring = (torch.zeros(self.act_slots * self.act_slot_elems, device=dev) if rank > 0 else None)
+        self.grad_ring = (torch.zeros(self.grad_slots * self.grad_slot_elems, device=dev)
+                          if rank < depth - 1 else None)
+        torch.cuda.synchronize(dev)
+        mine = (reduce_tensor(self.flags),
+                None if self.act_ring is None else reduce_tensor(self.act_ring),
+                None if self.grad_ring is None else reduce_tensor(self.grad_ring))
+        world = dist.get_world_size(group) if group is not None else dist.get_world_size()
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        ranks = stage_ranks or list(range(depth))
+
+        def open_(h):
+            fn, args = h
+            return fn(*args)
+
+        self.next = self.prev = None
+        if rank < depth - 1:
+            h = handles[ranks[rank + 1]]
+            self.next = (open_(h[0]), open_(h[1]))  # (flags, act_ring) of stage k+1
+        if rank > 0:
+            h = handles[ranks[rank - 1]]
+            self.prev = (open_(h[0]), open_(h[2]))  # (flags, grad_ring) of stage k-1
+        self._lib = _lib.load()
+        dist.barrier(group=group)
+
+    def _flag(self, t: torch.Tensor, word: int) -> int:
+        return t.data_ptr() + 8 * word
+
+    def send_act(self, out: torch.Tensor) -> None:
+        """Activation of this stage's forward -> stage k+1's ring."""
+        flags, ring = self.next
+        self._check_shape(out, self.out_elems)
+        rc = self._lib.po_p2p_send(out.data_ptr(), out.numel(), ring.data_ptr(), self.next_act_slot_elems,
+                                   self.next_act_slots, self.ctl_act.data_ptr(), self._flag(self.flags, _ACT_ACK),
+                                   self._flag(flags, _ACT_READY), self.timeout_ms, self.status.data_ptr(),
+                                   _stream(self.device))
+        _lib.check(rc, "po_p2p_send")
+
+    def recv_act(self) -> torch.Tensor:
+        flags, _ = self.prev
+        buf = torch.empty((self.rows, *self.in_shape), dtype=torch.float32, device=self.device)
+        rc = self._lib.po_p2p_recv(self.act_ring.data_ptr(), self.act_slot_elems, self.act_slots, buf.data_ptr(),
+                                   buf.numel(), self.ctl_act.data_ptr(), self._flag(self.flags, _ACT_READY),
+                                   self._flag(flags, _ACT_ACK), self.timeout_ms, self.status.data_ptr(),
+                                   _stream(self.device))
+        _lib.check(rc, "po_p2p_recv")
+        return buf
+
+    def send_grad(self, g: torch.Tensor) -> None:
+        """Input gradient of this stage's backward -> stage k-1's ring."""
+        flags, ring = self.prev
+        self._check_shape(g, self.in_elems)
+        rc = self._lib.po_p2p_send(g.data_ptr(), g.numel(), ring.data_ptr(), self.prev_grad_slot_elems,
+                                   self.prev_grad_slots, self.ctl_grad.data_ptr(), self._flag(self.flags, _GRAD_ACK),
+                                   self._flag(flags, _GRAD_READY), self.timeout_ms, self.status.data_ptr(),
+                                   _stream(self.device))
+        _lib.check(rc, "po_p2p_send")
+
+    def recv_grad(self) -> torch.Tensor:
+        flags, _ = self.next
+        buf = torch.empty((self.rows, *self.out_shape), dtype=torch.float32, device=self.device)
+        rc = self._lib.po_p2p_recv(self.grad_ring.data_ptr(), self.grad_slot_elems, self.grad_slots, buf.data_ptr(),
+                                   buf.numel(), self.ctl_grad.data_ptr(), self._flag(self.flags, _GRAD_READY),
+                                   self._flag(flags, _GRAD_ACK), self.timeout_ms, self.status.data_ptr(),
+                                   _stream(self.device))
+        _lib.check(rc, "po_p2p_recv")
+        return buf
+
+    @staticmethod
+    def _check_shape(t: torch.Tensor, n: int) -> None:
+        if t.numel() != n or not t.is_contiguous() or t.dtype != torch.float32:
+            raise ValueError(f"boundary tensor must be contiguous fp32 with {n} elements, got {tuple(t.shape)}")
+
+    def check(self) -> None:
+        """Raise if a transfer timed out (syncs)."""
+        if int(self.status.item()) != 0:
+            raise RuntimeError(f"stage {self.rank}: peer transfer timed out (a neighbour never signalled)")
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class PeerStageRunner:
+    """Runs one stage's 1F1B program on this rank over peer-memory rings;
+    `capture()` turns one full run into a CUDA graph that `replay()` re-runs
+    (continuing training: optimizer scalars come from a CoefTape refreshed
+    before each replay). Data must be device-resident; checks are deferred."""
+
+    def __init__(self, dist, tl: Timeline, stage, opt, strategy: str, data, loss_kind: str, lr_for_mb, rows: int,
+                 *, fuse: bool = True, group=None, stage_ranks: list[int] | None = None, timeout_ms: int = 60_000):
+        if STRATEGY_SCHEDULE.get(strategy) != "1f1b" or tl.kind != "1f1b":
+            raise ValueError(f"the peer runner executes 1f1b strategies, got {strategy!r} on {tl.kind!r}")
+        if strategy == "spectrain" and opt.config.kind != "sgdm":
+            raise ValueError("spectrain requires the sgdm optimizer")
+        validate_timeline(tl)
+        self.tl, self.stage, self.opt, self.strategy = tl, stage, opt, strategy
+        self.rank, self.depth = stage.rank, tl.depth
+        self.data, self.loss_kind, self.lr_for_mb, self.rows, self.fuse = data, loss_kind, lr_for_mb, rows, fuse
+        self.device = stage.flat.device
+        self.predictive = strategy in PREDICTIVE_STRATEGIES
+        self.program = stage_program(tl, self.rank, predictive=self.predictive)
+        slots = ring_slots(tl)
+        self.links = PeerLinks(dist, self.rank, self.depth, rows, stage.in_shape, stage.out_shape, slots,
+                               self.device, group=group, stage_ranks=stage_ranks, timeout_ms=timeout_ms)
+        opt.eager_checks = False
+        self.graph = None
+        self.runs = 0
+        self._pending = None
+
+    def _issue(self, lr_fn):
+        """Enqueue one full run of this rank's program on the current stream."""
+        st, links, last = self.stage, self.links, self.rank == self.depth - 1
+        policy = _make_policy(self.strategy, self.tl)
+        rt = _StageRt(st, self.opt, self.depth)
+        st.version = 1
+        work = [op for op in self.program if op.kind != UPDATE]
+        flags = torch.ones(len(work), dtype=torch.bool, device=self.device)
+        losses = torch.zeros(self.tl.n_batches, dtype=torch.float32, device=self.device) if last else None
+        records: dict[int, VersionRecord] = {}
+        order: list[VersionRecord] = []
+        local_grads: dict[int, torch.Tensor] = {}
+        snapshot_peak, wi = 1, 0
+        for op in self.program:
+            if op.kind == UPDATE:
+                lr = lr_fn(op.mb)
+                if self.fuse and op.fuse_predict:
+                    self.opt.step_predict_(st.flat, lr, lr_fn(op.next_mb), op.next_gap, rt.staging_buffer())
+                    rt.prepared = (op.next_mb, op.next_gap)
+                else:
+                    self.opt.step_(st.flat, lr)
+                st.version += 1
+                rt.pending_count = 0
+                policy.after_update(rt)
+            elif op.kind == FORWARD:
+                x = links.recv_act() if self.rank > 0 else _to_device(self.data.batch(op.mb)[0], self.device)
+                weights, fv, predicted, target = policy.forward_view(rt, op.mb, 0, lr_fn(op.mb))
+                out = st.run_forward(weights, (op.mb, 0), x, fv, check_finite=False, finite_flags=flags,
+                                     flag_index=wi)
+                rec = VersionRecord(op.mb, 0, self.rank, fv, predicted, target)
+                records[op.mb] = rec
+                order.append(rec)
+                if last:
+                    loss, grad = loss_and_grad(out, _to_device(self.data.batch(op.mb)[1], self.device), self.loss_kind)
+                    losses[op.mb - 1] = loss
+                    local_grads[op.mb] = grad
+                else:
+                    links.send_act(out if out.is_contiguous() else out.contiguous())
+                wi += 1
+            else:
+                g_out = local_grads.pop(op.mb) if last else links.recv_grad()
+                rec = records[op.mb]
+                weights, bv = policy.backward_view(rt, op.mb, 0, rec.forward_version)
+                g_in, _ = st.run_backward(weights, (op.mb, 0), g_out, accumulate=False, need_input_grad=self.rank > 0)
+                rt.pending_count = 1
+                rec.backward_version = bv
+                rec.live_backward_version = st.version
+                if self.rank > 0:
+                    links.send_grad(g_in if g_in.is_contiguous() else g_in.contiguous())
+                wi += 1
+            snapshot_peak = max(snapshot_peak, policy.snapshot_count(rt))
+        return order, flags, losses, snapshot_peak, work
+
+    def run(self) -> StageReport:
+        """One eager run (asynchronous device work, one sync at the end)."""
+        t0 = time.perf_counter()
+        self._pending = self._issue(self.lr_for_mb)
+        self.runs += 1
+        return self.report(time.perf_counter() - t0)
+
+    def capture(self) -> None:
+        """Capture one full run into a CUDA graph (run() at least once first:
+        it warms cuBLAS/cuDNN and the optimizer state)."""
+        if self.runs == 0:
+            raise RuntimeError("run() once before capture()")
+        self.opt._ensure_state()
+        torch.cuda.synchronize(self.device)
+        self.tape = CoefTape(self.device)
+        base = self.opt.step_count
+        self.graph = torch.cuda.CUDAGraph()
+        self.tape.begin([self.opt])
+        try:
+            with torch.cuda.graph(self.graph):
+                self._pending = self._issue(lambda mb: MbLr(self.lr_for_mb(mb), mb))
+        finally:
+            self.tape.end([self.opt])
+        self.updates = self.opt.step_count - base
+        self.opt.step_count = base  # nothing ran during capture
+        self.launches = len(self.tape.entries)
+
+    def replay(self) -> None:
+        """Enqueue one more full run (asynchronous)."""
+        self.tape.refresh({id(self.opt): self.opt.step_count}, self.lr_for_mb)
+        self.graph.replay()
+        self.opt.step_count += self.updates
+        self.stage.version = self.tl.n_batches + 1
+        self.runs += 1
+
+    def report(self, seconds: float = 0.0) -> StageReport:
+        """StageReport of the most recent run (synchronises; raises on a
+        transfer timeout or a non-finite forward output / loss / update)."""
+        order, flags, losses, snapshot_peak, work = self._pending
+        self.links.check()
+        if not bool(flags.all()):
+            bad = int((~flags).nonzero()[0].item())
+            raise NumericError(f"mb {work[bad].mb} stage {self.rank}: non-finite value in stage forward output")
+        self.opt.check_finite()
+        host_losses = None
+        if losses is not None:
+            host_losses = losses.cpu().tolist()
+            if not all(v == v and abs(v) != float("inf") for v in host_losses):
+                raise NumericError(f"stage {self.rank}: non-finite loss under {self.loss_kind}")
+        if self.stage.version != self.tl.n_batches + 1 or len(self.stage.stash):
+            raise RuntimeError(f"stage {self.rank} did not drain: version {self.stage.version}")
+        executed = [(op.kind, op.mb) for op in self.program]
+        return StageReport(self.rank, order, host_losses, self.stage.version, self.stage.stash.peak, snapshot_peak,
+                           seconds, executed)
+
+
+__all__ = ["PeerLinks", "PeerStageRunner", "ring_slots"]

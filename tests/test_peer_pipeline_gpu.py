@@ -1,0 +1,148 @@
+"""The peer-memory 1F1B runner (peer_pipeline.PeerStageRunner) with the REAL
+kernels: several processes on one B200 map each other's rings over CUDA IPC
+(NVLink peer memory on a multi-GPU node). Eager runs must reproduce the
+reference (records exact, losses/params vs the oracle); a run captured into
+ONE CUDA graph per rank and replayed must continue training exactly like
+further single-process runs of the same stages."""
+
+import json
+import os
+import socket
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import optim_ref, rng_ref, runtime_ref
+
+pytestmark = pytest.mark.gpu
+
+DIMS = [16, 24, 24, 24, 20, 10]
+ACTS = ["tanh", "tanh", "relu", "tanh", "linear"]
+ROWS = 8
+
+
+class DevSrc:
+    """Reference-seeded batches, resident on the device (graph replays read them)."""
+
+    def __init__(self, dev):
+        import torch
+
+        self.b = {}
+        for mb in range(1, 64):
+            s = rng_ref.Stream(7, f"batch-{mb}")
+            x, y = s.normal(ROWS, DIMS[0]), s.normal(ROWS, DIMS[-1])
+            self.b[mb] = (torch.tensor(np.asarray(getattr(x, "a", x)), dtype=torch.float32, device=dev),
+                          torch.tensor(np.asarray(getattr(y, "a", y)), dtype=torch.float32, device=dev))
+
+    def batch(self, mb):
+        return self.b[mb]
+
+
+def _stage(rank, world, kind, dev):
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+    group = partition_layers(build_layers(DIMS, ACTS), world)[rank]
+    stage = StageModel(rank, group, lambda sp: rng_ref.layer_init(3, sp.index, sp.in_dim, sp.out_dim), dev)
+    kw = {"weight_decay": 0.0} if kind == "sgdm" else {}
+    return stage, OptimizerState(OptimizerConfig(kind, **kw), stage.param_names, device=dev)
+
+
+def _worker(rank, world, port, strategy, kind, n, replays, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.peer_pipeline import PeerStageRunner
+        from paper_2312_00839_b200.pipeline import gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+
+        torch.backends.cuda.matmul.allow_tf32 = False
+        dev = torch.device("cuda", 0)
+        stage, opt = _stage(rank, world, kind, dev)
+        tl = build_timeline(strategy, world, n)
+        runner = PeerStageRunner(dist, tl, stage, opt, strategy, DevSrc(dev), "mse", lambda mb: 0.01, ROWS,
+                                 timeout_ms=120_000)
+        reps = [runner.run()]
+        if replays:
+            runner.capture()
+            for _ in range(replays):
+                runner.replay()
+                reps.append(runner.report())
+        allr = gather_reports(dist, reps[0], world)
+        lastr = gather_reports(dist, reps[-1], world)
+        if rank == 0:
+            Path(out_dir, "out.json").write_text(json.dumps({
+                "records": sorted([[r.mb, r.micro, r.stage, r.forward_version, r.predicted, r.prediction_target,
+                                    r.backward_version, r.live_backward_version] for rp in allr for r in rp.records]),
+                "losses_first": allr[-1].losses, "losses_last": lastr[-1].losses,
+                "executed": [[list(e) for e in rp.executed] for rp in allr]}))
+        Path(out_dir, f"params{rank}.json").write_text(json.dumps(
+            {n_: p.detach().double().cpu().numpy().tolist() for n_, p in zip(stage.param_names, stage.params)}))
+    finally:
+        dist.destroy_process_group()
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("async_raw", "sgdm")])
+def test_peer_runner_eager_matches_reference(tmp_path, world, strategy, kind):
+    import torch.multiprocessing as mp
+
+    from paper_2312_00839_b200.runtime import build_timeline
+
+    n = 2 * world + 3
+    mp.spawn(_worker, args=(world, _port(), strategy, kind, n, 0, str(tmp_path)), nprocs=world, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    src = DevSrc("cpu")
+    ref = runtime_ref.run(DIMS, ACTS, world, n, strategy, optim_ref.Hyper(kind, weight_decay=0.0),
+                          lambda mb: tuple(t.numpy() for t in src.batch(mb)), "mse", lambda mb: 0.01,
+                          lambda i, a, b: rng_ref.layer_init(3, i, a, b))
+    tl = build_timeline(strategy, world, n)
+    assert [[tuple(e) for e in ex] for ex in got["executed"]] == [
+        [(e.kind, e.mb) for e in tl.stage_events(k)] for k in range(world)]
+    assert got["records"] == sorted(list(r) for r in ref["records"])
+    assert np.allclose(got["losses_first"], ref["losses"], rtol=1e-4, atol=1e-6)
+    for k in range(world):
+        params = json.loads((tmp_path / f"params{k}.json").read_text())
+        for name, want in zip(ref["names"][k], ref["params"][k]):
+            assert optim_ref.inf_norm_rel(np.array(params[name]), want) <= 1e-4
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("async_raw", "adamw")])
+def test_peer_runner_graph_replays_continue_training(tmp_path, world, strategy, kind):
+    """eager run + capture + 2 replays (one CUDA graph per rank, no host in the
+    loop) == 3 runs of the single-process runner on the same stages."""
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2312_00839_b200.runtime import build_timeline, execute
+
+    n = 2 * world + 2
+    mp.spawn(_worker, args=(world, _port(), strategy, kind, n, 2, str(tmp_path)), nprocs=world, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dev = torch.device("cuda", 0)
+    pairs = [_stage(k, world, kind, dev) for k in range(world)]
+    stages, opts = [p[0] for p in pairs], [p[1] for p in pairs]
+    tl = build_timeline(strategy, world, n)
+    src = DevSrc(dev)
+    for _ in range(3):
+        for s in stages:
+            s.version = 1
+        rep = execute(tl, stages, opts, strategy, src, "mse", lambda mb: 0.01, checks="deferred")
+    np.testing.assert_allclose(got["losses_last"], rep.losses, rtol=1e-6, atol=1e-9)
+    for k, st in enumerate(stages):
+        params = json.loads((tmp_path / f"params{k}.json").read_text())
+        for name, p in zip(st.param_names, st.params):
+            want = p.detach().double().cpu().numpy()
+            assert optim_ref.inf_norm_rel(np.array(params[name]), want) <= 1e-6
