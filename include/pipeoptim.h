@@ -225,6 +225,15 @@ int po_p2p_recv(const float* ring, int64_t slot_elems, int32_t slots, float* dst
                 const int64_t* ready_flag, int64_t* peer_ack_flag, int64_t timeout_ms, int32_t* status,
                 void* stream);
 
+/* Node-shared device buffers (CUDA IPC). po_ipc_alloc: cudaMalloc `bytes`
+ * (zero-filled) on the current device and export its 64-byte handle.
+ * po_ipc_open: map a peer's buffer into the CURRENT device (peer access over
+ * NVLink enabled as needed). po_ipc_close / po_ipc_free release them. */
+int po_ipc_alloc(int64_t bytes, void** ptr, uint8_t* handle64);
+int po_ipc_open(const uint8_t* handle64, void** ptr);
+int po_ipc_close(void* ptr);
+int po_ipc_free(void* ptr);
+
 /* ---- live-weight LSTM cell (pipeoptim_lstm.cu) --------------------------
  * One time step of an LSTM layer whose GEMMs run in cuBLAS (PyTorch gate
  * order i, f, g, o; hidden % 4 == 0; all pointers 16-byte aligned). Used by

@@ -38,6 +38,10 @@ EXPORTS = (
     "po_step_predict_dp",
     "po_p2p_send",
     "po_p2p_recv",
+    "po_ipc_alloc",
+    "po_ipc_open",
+    "po_ipc_close",
+    "po_ipc_free",
     "po_lstm_cell_fwd",
     "po_lstm_cell_bwd",
 )
@@ -110,6 +114,10 @@ _SIGNATURES = {
                                           _I64, _P, _P]),
     "po_p2p_send": (ctypes.c_int, [_P, _I64, _P, _I64, ctypes.c_int32, _P, _P, _P, _I64, _P, _P]),
     "po_p2p_recv": (ctypes.c_int, [_P, _I64, ctypes.c_int32, _P, _I64, _P, _P, _P, _I64, _P, _P]),
+    "po_ipc_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p]),
+    "po_ipc_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "po_ipc_close": (ctypes.c_int, [_P]),
+    "po_ipc_free": (ctypes.c_int, [_P]),
     "po_lstm_cell_fwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
     "po_lstm_cell_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _I64, _I64, _P]),
 }

@@ -27,6 +27,7 @@
 //   ctl[2] messages received  ctl[3] arrival counter of the receive copy kernel
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "pipeoptim.h"
 
@@ -144,6 +145,53 @@ int po_p2p_recv(const float* ring, int64_t slot_elems, int32_t slots, float* dst
                                                            reinterpret_cast<unsigned long long*>(c + 1),
                                                            reinterpret_cast<long long*>(peer_ack_flag), status);
   cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+}  // extern "C"
+
+// ---- CUDA IPC buffers ----------------------------------------------------------------------
+// Buffers shared between the ranks of a node are plain cudaMalloc
+// allocations (zero-filled) exported with cudaIpcGetMemHandle; a peer maps
+// one with cudaIpcOpenMemHandle(cudaIpcMemLazyEnablePeerAccess) while ITS OWN
+// device is current, so the mapping lives in the device that dereferences it
+// and peer access (NVLink) is enabled as needed.
+extern "C" {
+
+int po_ipc_alloc(int64_t bytes, void** ptr, uint8_t* handle64) {
+  if (bytes <= 0 || ptr == nullptr || handle64 == nullptr) return PO_EINVAL;
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaMemset(*ptr, 0, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, *ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return (int)e;
+  }
+  memcpy(handle64, &h, sizeof(h));
+  return 0;
+}
+
+int po_ipc_open(const uint8_t* handle64, void** ptr) {
+  if (handle64 == nullptr || ptr == nullptr) return PO_EINVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+int po_ipc_close(void* ptr) {
+  if (ptr == nullptr) return PO_EINVAL;
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+int po_ipc_free(void* ptr) {
+  if (ptr == nullptr) return PO_EINVAL;
+  cudaError_t e = cudaFree(ptr);
   return e == cudaSuccess ? 0 : (int)e;
 }
 

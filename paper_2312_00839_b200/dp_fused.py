@@ -31,26 +31,33 @@ class FusedDPGroup:
     """Peer-mapped, double-buffered gradients of one stage's DP replicas."""
 
     def __init__(self, dist, group, dp_rank: int, dp_size: int, numel: int, device, timeout_ms: int = 60_000):
-        from torch.multiprocessing.reductions import reduce_tensor
+        from .ipc import IpcBuffer, open_peer
 
         if not 1 <= dp_size <= 8:
             raise ValueError(f"fused DP supports 1..8 replicas, got {dp_size}")
         self.dp_rank, self.dp_size, self.numel = dp_rank, dp_size, numel
         self.device = torch.device(device)
         self.timeout_ms = timeout_ms
-        self.bufs = [torch.zeros(numel, dtype=torch.float32, device=self.device) for _ in range(2)]
-        self.flags = torch.zeros(dp_size, dtype=torch.int64, device=self.device)
+        # node-shared (CUDA IPC) gradients and flags, mapped by each peer into
+        # its own device (ipc.py)
+        self._ipc = [IpcBuffer(numel, torch.float32, self.device) for _ in range(2)]
+        self._ipc.append(IpcBuffer(dp_size, torch.int64, self.device))
+        self.bufs = [self._ipc[0].tensor, self._ipc[1].tensor]
+        self.flags = self._ipc[2].tensor
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         torch.cuda.synchronize(self.device)
-        mine = [reduce_tensor(t) for t in (self.bufs[0], self.bufs[1], self.flags)]
+        mine = [b.export() for b in self._ipc]
         handles = [None] * dp_size
         dist.all_gather_object(handles, mine, group=group)
         self.peers = []
+        self._opened = []
         for r, h in enumerate(handles):
             if r == dp_rank:
                 self.peers.append((self.bufs[0], self.bufs[1], self.flags))
             else:
-                self.peers.append(tuple(fn(*args) for fn, args in h))
+                opened = [open_peer(x, self.device) for x in h]
+                self._opened += opened
+                self.peers.append(tuple(pb.tensor for pb in opened))
         # slot of THIS replica in every replica's flag array
         self.slots = torch.tensor([p[2].data_ptr() + 8 * dp_rank for p in self.peers], dtype=torch.int64,
                                   device=self.device)

@@ -31,6 +31,7 @@ import torch
 
 from . import _lib
 from .errors import NumericError
+from .ipc import IpcBuffer, open_peer
 from .optim import CoefTape, MbLr
 from .pipeline import StageReport
 from .runtime import PREDICTIVE_STRATEGIES, STRATEGY_SCHEDULE, VersionRecord, _make_policy, _StageRt, _to_device
@@ -77,15 +78,14 @@ class PeerLinks:
 
     def __init__(self, dist, rank: int, depth: int, rows: int, in_shape: tuple, out_shape: tuple, slots: dict,
                  device, group=None, stage_ranks: list[int] | None = None, timeout_ms: int = 60_000):
-        from torch.multiprocessing.reductions import reduce_tensor
-
         self.rank, self.depth, self.device = rank, depth, torch.device(device)
         self.timeout_ms = timeout_ms
         self.in_elems = rows * math.prod(in_shape)
         self.out_elems = rows * math.prod(out_shape)
         self.in_shape, self.out_shape, self.rows = tuple(in_shape), tuple(out_shape), rows
         dev = self.device
-        self.flags = torch.zeros(4, dtype=torch.int64, device=dev)
+        self._flags_buf = IpcBuffer(4, torch.int64, dev)  # written by the neighbours
+        self.flags = self._flags_buf.tensor
         self.ctl_act = torch.zeros(4, dtype=torch.int64, device=dev)   # [sent to k+1, arr, recvd from k-1, arr]
         self.ctl_grad = torch.zeros(4, dtype=torch.int64, device=dev)  # [sent to k-1, arr, recvd from k+1, arr]
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -100,21 +100,23 @@ class PeerLinks:
         self.next_act_slot_elems = _slot_elems(rows, out_shape)
         self.prev_grad_slots = slots.get(("grad", rank - 1), 1)
         self.prev_grad_slot_elems = _slot_elems(rows, in_shape)
-        self.act_ring = (torch.zeros(self.act_slots * self.act_slot_elems, device=dev) if rank > 0 else None)
-        self.grad_ring = (torch.zeros(self.grad_slots * self.grad_slot_elems, device=dev)
-                          if rank < depth - 1 else None)
+        self._rings = [IpcBuffer(self.act_slots * self.act_slot_elems, torch.float32, dev) if rank > 0 else None,
+                       IpcBuffer(self.grad_slots * self.grad_slot_elems, torch.float32, dev)
+                       if rank < depth - 1 else None]
+        self.act_ring = None if self._rings[0] is None else self._rings[0].tensor
+        self.grad_ring = None if self._rings[1] is None else self._rings[1].tensor
         torch.cuda.synchronize(dev)
-        mine = (reduce_tensor(self.flags),
-                None if self.act_ring is None else reduce_tensor(self.act_ring),
-                None if self.grad_ring is None else reduce_tensor(self.grad_ring))
+        mine = (self._flags_buf.export(), *(None if b is None else b.export() for b in self._rings))
         world = dist.get_world_size(group) if group is not None else dist.get_world_size()
         handles = [None] * world
         dist.all_gather_object(handles, mine, group=group)
         ranks = stage_ranks or list(range(depth))
+        self._peers = []
 
         def open_(h):
-            fn, args = h
-            return fn(*args)
+            pb = open_peer(h, dev)
+            self._peers.append(pb)
+            return pb.tensor
 
         self.next = self.prev = None
         if rank < depth - 1:
@@ -321,3 +323,53 @@ class PeerStageRunner:
 
 
 __all__ = ["PeerLinks", "PeerStageRunner", "ring_slots"]
+
+
+# ---- bench support ---------------------------------------------------------------------------
+
+
+def bench_peer_pipeline(torch_mod, dist, rank, world, device, make_stage, data, loss_kind, lr, rows, n_batches,
+                        replays: int = 5, trials: int = 3, opt_kind: str = "adam", opt_kw: dict | None = None):
+    """Prediction off/on through the peer runner, one CUDA graph per rank per
+    run: eager warm-up run, capture, one warm replay, then `trials` x
+    `replays` timed replays per arm in alternation (median; device time of
+    the replays, max over ranks). `make_stage()` -> this rank's stage."""
+    import statistics
+
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import build_timeline
+
+    runners = {}
+    for strategy in ("async_raw", "optimizer_prediction"):
+        stage = make_stage()
+        opt = OptimizerState(OptimizerConfig(opt_kind, **(opt_kw or {})), stage.param_names, device=device)
+        r = PeerStageRunner(dist, build_timeline(strategy, world, n_batches), stage, opt, strategy, data, loss_kind,
+                            lambda mb: lr, rows)
+        r.run()
+        r.capture()
+        r.replay()
+        r.report()
+        runners[strategy] = r
+    times = {s: [] for s in runners}
+    for _ in range(trials):
+        for s, r in runners.items():
+            torch_mod.cuda.synchronize(device)
+            dist.barrier()
+            e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(replays):
+                r.replay()
+            e1.record()
+            torch_mod.cuda.synchronize(device)
+            t = torch_mod.tensor([e0.elapsed_time(e1) / 1e3 / replays], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            times[s].append(float(t.item()))
+    out = {}
+    for s, r in runners.items():
+        r.report()  # raises on a transfer timeout or a non-finite value
+        key = "pred_on" if s == "optimizer_prediction" else "pred_off"
+        sec = statistics.median(times[s])
+        out[key] = {"samples_per_s": round(n_batches * rows / sec, 1), "s_per_run": round(sec, 5),
+                    "s_per_run_trials": [round(t, 5) for t in times[s]], "graph_launches_per_run": r.launches}
+    out["prediction_overhead"] = round(1.0 - out["pred_on"]["samples_per_s"] / out["pred_off"]["samples_per_s"], 4)
+    return out

@@ -589,6 +589,22 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
     gon, goff = out["graphed_pred_on"]["samples_per_s"], out["graphed_pred_off"]["samples_per_s"]
     out.update(value=max(on, gon), unit="samples/s", prediction_overhead=round(1.0 - on / off, 4),
                graphed_prediction_overhead=round(1.0 - gon / goff, 4), launches=n_batches * 2)
+    # the peer-memory transport: a rank's whole run is one CUDA graph (no NCCL,
+    # no host in the loop); reported beside the NCCL runner and, when faster,
+    # as the value
+    try:
+        from .peer_pipeline import bench_peer_pipeline
+
+        peer = bench_peer_pipeline(
+            torch_mod, dist, rank, world, device,
+            lambda: StageModel(rank, partition_layers(layers, world)[rank], torch_init(0, device), device),
+            data, "softmax_xent", 1e-4, BATCH, n_batches)
+        out["peer_graphed"] = peer
+        if peer["pred_on"]["samples_per_s"] > out["value"]:
+            out.update(value=peer["pred_on"]["samples_per_s"], transport="peer memory (one CUDA graph per rank)",
+                       prediction_overhead=peer["prediction_overhead"])
+    except Exception as exc:  # the NCCL numbers above still stand
+        out["peer_graphed"] = {"error": f"{type(exc).__name__}: {exc}"}
     return out
 
 
