@@ -117,7 +117,9 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
         unit()
     torch.cuda.synchronize(device)
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
+    from .runtime import capture
+
+    with capture(graph):
         unit()
     graph.replay()
     torch.cuda.synchronize(device)

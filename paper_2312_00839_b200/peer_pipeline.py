@@ -34,7 +34,15 @@ from .errors import NumericError
 from .ipc import IpcBuffer, open_peer
 from .optim import CoefTape, MbLr
 from .pipeline import StageReport
-from .runtime import PREDICTIVE_STRATEGIES, STRATEGY_SCHEDULE, VersionRecord, _make_policy, _StageRt, _to_device
+from .runtime import (
+    PREDICTIVE_STRATEGIES,
+    STRATEGY_SCHEDULE,
+    VersionRecord,
+    _make_policy,
+    _StageRt,
+    _to_device,
+    capture,
+)
 from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
 from .stages import loss_and_grad
 
@@ -176,10 +184,45 @@ class PeerLinks:
         if t.numel() != n or not t.is_contiguous() or t.dtype != torch.float32:
             raise ValueError(f"boundary tensor must be contiguous fp32 with {n} elements, got {tuple(t.shape)}")
 
+    def close(self) -> None:
+        """Unmap the neighbours' buffers and free this rank's (after a device
+        sync and a barrier-free contract: call it on every rank once no rank
+        will send any more)."""
+        torch.cuda.synchronize(self.device)
+        for pb in self._peers:
+            pb.close()
+        self._peers = []
+        for b in (self._flags_buf, *self._rings):
+            if b is not None:
+                b.free()
+
     def check(self) -> None:
         """Raise if a transfer timed out (syncs)."""
         if int(self.status.item()) != 0:
             raise RuntimeError(f"stage {self.rank}: peer transfer timed out (a neighbour never signalled)")
+
+
+def _capture_debugger():
+    """PO_DEBUG_CAPTURE=1: report the first op after which the current
+    stream's capture became invalidated (diagnostics only)."""
+    import os
+
+    if os.environ.get("PO_DEBUG_CAPTURE") != "1":
+        return None
+    import ctypes
+    import sys
+
+    cudart = ctypes.CDLL("libcudart.so.12")
+    st = ctypes.c_int()
+    seen = [False]
+
+    def probe(where):
+        cudart.cudaStreamIsCapturing(ctypes.c_void_p(torch.cuda.current_stream().cuda_stream), ctypes.byref(st))
+        if st.value == 2 and not seen[0]:
+            seen[0] = True
+            print(f"[peer] capture invalidated by {where}", file=sys.stderr, flush=True)
+
+    return probe
 
 
 def _stream(device) -> int:
@@ -226,7 +269,10 @@ class PeerStageRunner:
         order: list[VersionRecord] = []
         local_grads: dict[int, torch.Tensor] = {}
         snapshot_peak, wi = 1, 0
+        debug = _capture_debugger()
         for op in self.program:
+            if debug is not None:
+                debug(f"rank {self.rank} before {op.kind}{op.mb}")
             if op.kind == UPDATE:
                 lr = lr_fn(op.mb)
                 if self.fuse and op.fuse_predict:
@@ -285,7 +331,7 @@ class PeerStageRunner:
         self.graph = torch.cuda.CUDAGraph()
         self.tape.begin([self.opt])
         try:
-            with torch.cuda.graph(self.graph):
+            with capture(self.graph):
                 self._pending = self._issue(lambda mb: MbLr(self.lr_for_mb(mb), mb))
         finally:
             self.tape.end([self.opt])
@@ -372,4 +418,11 @@ def bench_peer_pipeline(torch_mod, dist, rank, world, device, make_stage, data, 
         out[key] = {"samples_per_s": round(n_batches * rows / sec, 1), "s_per_run": round(sec, 5),
                     "s_per_run_trials": [round(t, 5) for t in times[s]], "graph_launches_per_run": r.launches}
     out["prediction_overhead"] = round(1.0 - out["pred_on"]["samples_per_s"] / out["pred_off"]["samples_per_s"], 4)
+    torch_mod.cuda.synchronize(device)
+    dist.barrier()  # no rank sends any more: free the rings
+    for r in runners.values():
+        r.graph = None
+        r.links.close()
+    runners.clear()
+    torch_mod.cuda.empty_cache()
     return out

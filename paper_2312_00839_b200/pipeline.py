@@ -32,6 +32,7 @@ from .runtime import (
     _make_policy,
     _StageRt,
     _to_device,
+    capture,
 )
 from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
 from .stages import StageModel, loss_and_grad
@@ -214,7 +215,7 @@ class _OpGraphs:
             return fn()
         if n == 1:
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
+            with capture(graph):
                 outs = fn()
             self.graphs[key] = (graph, outs)
         graph, outs = self.graphs[key]
@@ -291,7 +292,7 @@ class _OpGraphs:
                 r.opt.tape = self.tape
                 graph = torch.cuda.CUDAGraph()
                 try:
-                    with torch.cuda.graph(graph):
+                    with capture(graph):
                         fn()
                 finally:
                     r.opt.tape = None
@@ -604,7 +605,11 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
             out.update(value=peer["pred_on"]["samples_per_s"], transport="peer memory (one CUDA graph per rank)",
                        prediction_overhead=peer["prediction_overhead"])
     except Exception as exc:  # the NCCL numbers above still stand
-        out["peer_graphed"] = {"error": f"{type(exc).__name__}: {exc}"}
+        import sys
+        import traceback
+
+        traceback.print_exc(file=sys.stderr)
+        out["peer_graphed"] = {"error": f"rank {rank}: {type(exc).__name__}: {exc}"}
     return out
 
 
@@ -655,6 +660,30 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
         out[key] = {"samples_per_s": round(n_batches * cfg["batch"] / float(t.item()), 2), "s": round(float(t.item()), 4)}
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4))
+    try:  # the peer-memory transport, one CUDA graph per rank per run
+        from .peer_pipeline import bench_peer_pipeline
+
+        def make_stage():
+            stages, _ = module_stages_for(torch_mod, name, device, depth=world, costs=costs)
+            for k, st in enumerate(stages):
+                if k != rank:
+                    st.module.to("cpu")
+            return stages[rank]
+
+        kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
+        peer = bench_peer_pipeline(torch_mod, dist, rank, world, device, make_stage, data, "softmax_xent",
+                                   cfg["lr"], cfg["batch"], n_batches, replays=2, trials=3, opt_kind=cfg["opt"],
+                                   opt_kw=kw)
+        out["peer_graphed"] = peer
+        if peer["pred_on"]["samples_per_s"] > out["value"]:
+            out.update(value=peer["pred_on"]["samples_per_s"], transport="peer memory (one CUDA graph per rank)",
+                       prediction_overhead=peer["prediction_overhead"])
+    except Exception as exc:
+        import sys
+        import traceback
+
+        traceback.print_exc(file=sys.stderr)
+        out["peer_graphed"] = {"error": f"rank {rank}: {type(exc).__name__}: {exc}"}
     torch_mod.backends.cuda.matmul.allow_tf32 = False
     torch_mod.backends.cudnn.allow_tf32 = False
     return out

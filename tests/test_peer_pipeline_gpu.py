@@ -146,3 +146,71 @@ def test_peer_runner_graph_replays_continue_training(tmp_path, world, strategy, 
         for name, p in zip(st.param_names, st.params):
             want = p.detach().double().cpu().numpy()
             assert optim_ref.inf_norm_rel(np.array(params[name]), want) <= 1e-6
+
+
+def _module_worker(rank, world, port, n, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
+        from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+        from paper_2312_00839_b200.peer_pipeline import PeerStageRunner
+        from paper_2312_00839_b200.pipeline import gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+
+        torch.backends.cudnn.deterministic = True
+        torch.backends.cudnn.allow_tf32 = torch.backends.cuda.matmul.allow_tf32 = False
+        dev = torch.device("cuda", 0)
+        cfg = dict(MODULE_CONFIGS["config2_vgg16"], batch=8)
+        torch.manual_seed(0)
+        stages, _ = module_stages_for(torch, "config2_vgg16", dev, depth=world, costs=[1.0] * 15)
+        stage = stages[rank]
+        opt = OptimizerState(OptimizerConfig("sgdm"), stage.param_names, device=dev)
+        tl = build_timeline("optimizer_prediction", world, n)
+        runner = PeerStageRunner(dist, tl, stage, opt, "optimizer_prediction", ModuleBatches(torch, dev, cfg),
+                                 "softmax_xent", lambda mb: 1e-2, 8, timeout_ms=120_000)
+        runner.run()
+        runner.capture()
+        runner.replay()
+        reps = gather_reports(dist, runner.report(), world)
+        if rank == 0:
+            Path(out_dir, "out.json").write_text(json.dumps({"losses": reps[-1].losses}))
+        torch.save(stage.flat.data.cpu(), Path(out_dir, f"w{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_runner_module_stages(tmp_path):
+    """VGG-16 module stages (conv/BN/LiveLinear) through the peer runner, one
+    graph per rank: eager run + 1 replay == 2 single-process runs."""
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2312_00839_b200.bench_pipeline import MODULE_CONFIGS, ModuleBatches, module_stages_for
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import build_timeline, execute
+
+    world, n = 2, 5
+    mp.spawn(_module_worker, args=(world, _port(), n, str(tmp_path)), nprocs=world, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.allow_tf32 = torch.backends.cuda.matmul.allow_tf32 = False
+    dev = torch.device("cuda", 0)
+    cfg = dict(MODULE_CONFIGS["config2_vgg16"], batch=8)
+    torch.manual_seed(0)
+    stages, _ = module_stages_for(torch, "config2_vgg16", dev, depth=world, costs=[1.0] * 15)
+    opts = [OptimizerState(OptimizerConfig("sgdm"), s.param_names, device=dev) for s in stages]
+    tl = build_timeline("optimizer_prediction", world, n)
+    data = ModuleBatches(torch, dev, cfg)
+    for _ in range(2):
+        for s in stages:
+            s.version = 1
+        rep = execute(tl, stages, opts, "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-2,
+                      checks="deferred")
+    np.testing.assert_allclose(got["losses"], rep.losses, rtol=1e-5, atol=1e-7)
+    for k, st in enumerate(stages):
+        w = torch.load(tmp_path / f"w{k}.pt")
+        assert float((w - st.flat.data.cpu()).abs().max()) <= 1e-5 * float(st.flat.data.abs().max())
