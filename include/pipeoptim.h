@@ -193,6 +193,14 @@ int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void
 int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t rows, int64_t cols, float* grad,
                  float* loss, float* scratch, void* stream);
 
+/* Reduction of a split-K GEMM fused with the layer epilogue (stages.py:175-178
+ * affine + activation): out = act(sum_{s=0..splits-1} part[s] + bias), the
+ * partials summed in that fixed order (deterministic). part: [splits x rows x
+ * cols], bias: [cols] or NULL, act: 0 linear, 1 relu, 2 tanh; pre_out
+ * (nullable) receives the pre-activation. */
+int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t cols, const float* bias,
+                       int32_t act, float* out, float* pre_out, void* stream);
+
 /* Backward elementwise part of a ReLU layer fused with its bias gradient
  * (stages.py:200-206, linalg.py:185-194): dpre = g * (pre > 0) written to
  * dpre, and db = colsum(dpre) (accumulate != 0: db += colsum). h is the

@@ -10,6 +10,11 @@
 //   po_loss_grad    softmax cross-entropy or MSE loss AND its gradient
 //                   (linalg.py:212-241), the loss reduced in a fixed order by
 //                   the last CTA to finish (deterministic, no float atomics).
+//   po_splitk_bias_act  the reduction of a split-K GEMM (S partial products
+//                   summed in a fixed order) fused with the layer's bias and
+//                   activation — the config-1 GEMMs have M = batch = 128 rows and
+//                   a long K, so cuBLAS runs them on a handful of output tiles;
+//                   split-K bmm + this kernel is 2-3x faster (scripts/gemm_splitk.py)
 //   po_relu_bwd_bias  a ReLU layer's backward elementwise part AND its bias
 //                   gradient: dpre = g * (h > 0), db (+)= colsum(dpre)
 //                   (stages.py:200-206) — replaces compare + multiply +
@@ -156,6 +161,21 @@ __global__ void relu_bwd_bias_kernel(const float* g, const float* __restrict__ h
   }
 }
 
+// out[i] = act(sum_s part[s*n + i] + bias[i % cols]), s in order 0..S-1;
+// pre_out (nullable) receives the pre-activation. act: 0 linear, 1 relu, 2 tanh.
+__global__ void splitk_bias_act_kernel(const float* __restrict__ part, int S, int64_t n, int64_t cols,
+                                       const float* __restrict__ bias, int act, float* __restrict__ out,
+                                       float* __restrict__ pre_out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float acc = part[i];
+    for (int s = 1; s < S; ++s) acc += part[(int64_t)s * n + i];
+    if (bias != nullptr) acc += bias[i % cols];
+    if (pre_out != nullptr) pre_out[i] = acc;
+    out[i] = act == 1 ? (acc > 0.f ? acc : 0.f) : act == 2 ? tanhf(acc) : acc;
+  }
+}
+
 int sm_count_ops() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -175,6 +195,23 @@ int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void
   int64_t want = (n / 4 + block - 1) / block;
   int64_t grid = want < 1 ? 1 : (want > 4 * sms ? 4 * sms : want);
   all_finite_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(x, n, flags, index);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t cols, const float* bias,
+                       int32_t act, float* out, float* pre_out, void* stream) {
+  if (splits < 1 || rows < 0 || cols < 1 || act < 0 || act > 2 || out == nullptr || (rows > 0 && part == nullptr))
+    return PO_EINVAL;
+  const int64_t n = rows * cols;
+  if (n == 0) return 0;
+  static int sms = 0;
+  if (sms == 0) sms = sm_count_ops();
+  const int block = 256;
+  int64_t want = (n + block - 1) / block;
+  const int64_t grid = want > 8 * sms ? 8 * sms : want;
+  splitk_bias_act_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(part, splits, n, cols, bias, act, out,
+                                                                            pre_out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }

@@ -214,6 +214,72 @@ def _activation_grad_mul(g: torch.Tensor, pre: torch.Tensor, kind: str) -> torch
     return g
 
 
+_ACT_CODE = {"linear": 0, "relu": 1, "tanh": 2}
+
+
+def _splitk(rows: int, k: int, n: int) -> int:
+    """Split count for a GEMM of `rows` x k @ k x n on the device: the 1F1B
+    stages multiply a batch of ~128 rows by wide weights, a long-K, few-tile
+    shape cuBLAS runs on a handful of CTAs (scripts/gemm_splitk.py: 3072x1024
+    59 us as one GEMM, 19 us as 8 batched K-slices). Split K into S power-of-
+    two slices of >= 256 (>= 32 for narrow outputs) while S <= 8 (32)."""
+    if rows > 512 or k < 512:
+        return 1
+    cap, floor = (32, 32) if n < 64 else (8, 256)
+    s = 1
+    while s * 2 <= cap and k % (s * 2) == 0 and k // (s * 2) >= floor:
+        s *= 2
+    return s
+
+
+def _splitk_reduce(part: torch.Tensor, bias, act: str, pre_out=None) -> torch.Tensor:
+    """act(sum_s part[s] + bias) in one launch (po_splitk_bias_act)."""
+    from . import _lib
+
+    splits, rows, cols = part.shape
+    out = torch.empty((rows, cols), dtype=torch.float32, device=part.device)
+    rc = _lib.load().po_splitk_bias_act(part.data_ptr(), splits, rows, cols,
+                                        None if bias is None else bias.data_ptr(), _ACT_CODE[act], out.data_ptr(),
+                                        None if pre_out is None else pre_out.data_ptr(),
+                                        torch.cuda.current_stream(part.device).cuda_stream)
+    _lib.check(rc, "po_splitk_bias_act")
+    return out
+
+
+def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str):
+    """Device forward of one layer: (pre, h_out) with the stash's convention —
+    relu layers stash relu(pre) (its sign pattern is pre's), others pre."""
+    rows, k = h.shape
+    n = w.shape[1]
+    s = _splitk(rows, k, n)
+    if s > 1:
+        h = h if h.is_contiguous() else h.contiguous()
+        part = torch.bmm(h.view(rows, s, k // s).transpose(0, 1), w.view(s, k // s, n))
+        bias = b.view(-1)
+        if act == "tanh":
+            pre = torch.empty((rows, n), dtype=torch.float32, device=h.device)
+            return pre, _splitk_reduce(part, bias, act, pre_out=pre)
+        out = _splitk_reduce(part, bias, act)
+        return out, out
+    if act == "relu":
+        out = torch._addmm_activation(b.view(-1), h, w)
+        return out, out
+    pre = torch.addmm(b.view(-1), h, w)
+    return pre, _activate(pre, act)
+
+
+def _input_grad(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """dpre @ w^T on the device, split-K over the layer's output width."""
+    rows, n = dpre.shape
+    k = w.shape[0]
+    s = _splitk(rows, n, k)
+    if s > 1:
+        dpre = dpre if dpre.is_contiguous() else dpre.contiguous()
+        part = torch.bmm(dpre.view(rows, s, n // s).transpose(0, 1), w.view(k, s, n // s).permute(1, 2, 0))
+        return _splitk_reduce(part, None, "linear")
+    return torch.mm(dpre, w.t())
+
+
 def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int,
                   check_finite: bool = True, finite_flags: torch.Tensor | None = None,
                   flag_index: int = 0) -> torch.Tensor:
@@ -232,13 +298,13 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
     for i, spec in enumerate(stage.layers):
         w, b = weights[2 * i], weights[2 * i + 1]
         inputs.append(h)
-        if fused and spec.activation == "relu":
-            # bias + ReLU in the GEMM epilogue (cuBLASLt); the stash keeps
-            # relu(pre) — its sign pattern is pre's, all the backward needs
-            h = torch._addmm_activation(b.view(-1), h, w)
-            pres.append(h)
+        if fused:
+            # split-K GEMM + one reduce/bias/activation launch, or bias + ReLU
+            # in the cuBLASLt epilogue; relu layers stash relu(pre)
+            pre, h = _affine(h, w, b, spec.activation)
+            pres.append(pre)
             continue
-        pre = torch.addmm(b.view(-1), h, w) if fused else torch.addmm(b, h, w)
+        pre = torch.addmm(b, h, w)
         pres.append(pre)
         h = _activate(pre, spec.activation)
     if check_finite:
@@ -304,7 +370,7 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
                 torch.mm(x.t(), dpre, out=gw)
                 torch.sum(dpre, dim=0, keepdim=True, out=gb)
         if i > 0 or need_input_grad:
-            g = torch.mm(dpre, weights[2 * i].t())
+            g = _input_grad(dpre, weights[2 * i]) if dpre.is_cuda else torch.mm(dpre, weights[2 * i].t())
         else:
             g = None
     return g, gviews

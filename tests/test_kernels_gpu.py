@@ -368,6 +368,38 @@ def test_relu_bwd_bias_matches_reference(rows, cols, accumulate, alias):
     np.testing.assert_allclose(host(db), want_db, rtol=1e-5, atol=1e-5)
 
 
+@pytest.mark.parametrize("rows,k,n", [(128, 3072, 1024), (128, 1024, 1024), (128, 1024, 10), (64, 512, 96),
+                                      (128, 24, 20)])
+@pytest.mark.parametrize("act", ["relu", "linear", "tanh"])
+def test_split_k_layer_forward_and_input_grad(rows, k, n, act):
+    """stages._affine (split-K bmm + po_splitk_bias_act, or the cuBLASLt
+    epilogue) and stages._input_grad vs float64 (stages.py:175-178, 200-208),
+    TF32 off; relu layers return relu(pre) as their stash value."""
+    import torch
+
+    from paper_2312_00839_b200.stages import _affine, _input_grad, _splitk
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    g = torch.Generator(device="cuda").manual_seed(rows + k + n)
+    x = torch.randn(rows, k, device="cuda", generator=g)
+    w = torch.randn(k, n, device="cuda", generator=g) / k ** 0.5
+    b = torch.randn(1, n, device="cuda", generator=g)
+    pre, h = _affine(x, w, b, act)
+    want_pre = x.double() @ w.double() + b.double()
+    want_h = {"relu": want_pre.clamp_min(0), "linear": want_pre, "tanh": torch.tanh(want_pre)}[act]
+    tol = 2e-6 * float(want_pre.abs().max()) * (k ** 0.5)
+    assert float((h.double() - want_h).abs().max()) <= tol
+    if act == "tanh":
+        assert float((pre.double() - want_pre).abs().max()) <= tol
+    else:
+        assert pre.data_ptr() == h.data_ptr()
+    dpre = torch.randn(rows, n, device="cuda", generator=g)
+    gi = _input_grad(dpre, w)
+    want_gi = dpre.double() @ w.double().t()
+    assert float((gi.double() - want_gi).abs().max()) <= 2e-6 * float(want_gi.abs().max()) * (n ** 0.5)
+    assert _splitk(128, 3072, 1024) == 8 and _splitk(128, 24, 20) == 1
+
+
 def test_more_than_2_31_elements(lib):
     """64-bit indexing: a 2^31 + 13 element stage (8 GB per buffer); K3 checked
     bit-exact against the fp32 emulation on the first and last 2^20 elements."""
