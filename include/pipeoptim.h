@@ -205,10 +205,12 @@ int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t 
  * (stages.py:200-206, linalg.py:185-194): dpre = g * (pre > 0) written to
  * dpre, and db = colsum(dpre) (accumulate != 0: db += colsum). h is the
  * layer's OUTPUT relu(pre) (relu(pre) > 0 <=> pre > 0, so the stash keeps h).
- * g, h, dpre: row-major [rows x cols]; db: [cols]. Deterministic (fixed
- * summation order); g may alias dpre. */
-int po_relu_bwd_bias(const float* g, const float* h, int64_t rows, int64_t cols, float* dpre, float* db,
-                     int32_t accumulate, void* stream);
+ * g: [splits x rows x cols] partial products (of a split-K input gradient)
+ * summed in order, or splits = 1; h, dpre: row-major [rows x cols]; db:
+ * [cols]. Deterministic (fixed summation orders); with splits = 1 g may
+ * alias dpre. */
+int po_relu_bwd_bias(const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols, float* dpre,
+                     float* db, int32_t accumulate, void* stream);
 
 /* ---- peer-memory boundary transport (pipeoptim_p2p.cu) ------------------
  * Replaces the simulated hand-off dicts of the reference executor

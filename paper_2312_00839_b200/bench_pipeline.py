@@ -123,6 +123,9 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
         unit()
     graph.replay()
     torch.cuda.synchronize(device)
+    # the graph replays into these addresses: keep the buffers allocated
+    # outside the capture alive as long as the graph
+    graph.keepalive = (staging, x, g_last, y0)
     return graph
 
 

@@ -18,7 +18,9 @@
 //   po_relu_bwd_bias  a ReLU layer's backward elementwise part AND its bias
 //                   gradient: dpre = g * (h > 0), db (+)= colsum(dpre)
 //                   (stages.py:200-206) — replaces compare + multiply +
-//                   column-sum (3 launches, dpre written then re-read).
+//                   column-sum (3 launches, dpre written then re-read); g may
+//                   arrive as the split-K partials of the next layer's input
+//                   gradient, summed here in a fixed order.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -130,33 +132,42 @@ __global__ void loss_grad_kernel(const float* __restrict__ pred, const float* __
   }
 }
 
-// One CTA per 32 columns; warp w walks rows w, w + nwarps, ... with lane =
-// column (128-byte coalesced rows), keeps its column partial in a register,
-// then the warps' partials are summed in warp order through shared memory:
-// a fixed reduction order, so the bias gradient is deterministic.
-constexpr int kReluWarps = 8;
+// One CTA per 8 columns: thread t handles column t % 8 and rows t / 8,
+// t / 8 + 32, ... (a warp reads 4 rows x 32 contiguous bytes per load), keeps
+// its column partial in a register, then the 32 row-lanes' partials of each
+// column are summed in row-lane order through shared memory: a fixed
+// reduction order, so the bias gradient is deterministic. 8-column CTAs put
+// 128 CTAs on a 1024-wide layer (one CTA per 32 columns left 32 SMs busy and
+// took 12.5 us for 128 x 1024).
+constexpr int kReluCols = 8, kReluLanes = 32;
 
-// g and dpre may alias (each element is read, then written, by one thread)
-__global__ void relu_bwd_bias_kernel(const float* g, const float* __restrict__ h, int64_t rows, int64_t cols,
-                                     float* dpre, float* __restrict__ db, int accumulate) {
-  __shared__ float part[kReluWarps][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+// g: `splits` partial products [splits x rows x cols], summed in order 0..S-1.
+// g and dpre may alias when splits == 1 (each element is read, then written,
+// by one thread)
+__global__ void relu_bwd_bias_kernel(const float* g, int splits, const float* __restrict__ h, int64_t rows,
+                                     int64_t cols, float* dpre, float* __restrict__ db, int accumulate) {
+  const int64_t n = rows * cols;
+  __shared__ float part[kReluLanes][kReluCols];
+  const int cl = threadIdx.x % kReluCols, lane = threadIdx.x / kReluCols;
+  const int64_t c = (int64_t)blockIdx.x * kReluCols + cl;
   float acc = 0.f;
   if (c < cols) {
-    for (int64_t r = w; r < rows; r += kReluWarps) {
+#pragma unroll 4
+    for (int64_t r = lane; r < rows; r += kReluLanes) {
       const int64_t i = r * cols + c;
-      const float v = h[i] > 0.f ? g[i] : 0.f;  // g * (pre > 0): relu(pre) > 0 <=> pre > 0
+      float gi = g[i];
+      for (int s = 1; s < splits; ++s) gi += g[(int64_t)s * n + i];
+      const float v = h[i] > 0.f ? gi : 0.f;  // g * (pre > 0): relu(pre) > 0 <=> pre > 0
       dpre[i] = v;
       acc += v;
     }
   }
-  part[w][lane] = acc;
+  part[lane][cl] = acc;
   __syncthreads();
-  if (w == 0 && c < cols) {
+  if (lane == 0 && c < cols) {
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < kReluWarps; ++k) s += part[k][lane];
+    for (int k = 0; k < kReluLanes; ++k) s += part[k][cl];
     db[c] = accumulate ? db[c] + s : s;
   }
 }
@@ -216,9 +227,9 @@ int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t 
   return e == cudaSuccess ? 0 : (int)e;
 }
 
-int po_relu_bwd_bias(const float* g, const float* h, int64_t rows, int64_t cols, float* dpre, float* db,
-                     int32_t accumulate, void* stream) {
-  if (rows < 0 || cols < 0) return PO_EINVAL;
+int po_relu_bwd_bias(const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols, float* dpre,
+                     float* db, int32_t accumulate, void* stream) {
+  if (rows < 0 || cols < 0 || splits < 1) return PO_EINVAL;
   if (rows == 0 || cols == 0) {
     if (cols > 0 && !accumulate && db != nullptr) {
       cudaError_t e = cudaMemsetAsync(db, 0, (size_t)cols * sizeof(float), (cudaStream_t)stream);
@@ -227,10 +238,11 @@ int po_relu_bwd_bias(const float* g, const float* h, int64_t rows, int64_t cols,
     return 0;
   }
   if (g == nullptr || h == nullptr || dpre == nullptr || db == nullptr) return PO_EINVAL;
-  const int64_t grid = (cols + 31) / 32;
+  const int64_t grid = (cols + kReluCols - 1) / kReluCols;
   if (grid > 0x7fffffff) return PO_EINVAL;
-  relu_bwd_bias_kernel<<<(unsigned)grid, 32 * kReluWarps, 0, (cudaStream_t)stream>>>(g, h, rows, cols, dpre, db,
-                                                                                     accumulate);
+  relu_bwd_bias_kernel<<<(unsigned)grid, kReluCols * kReluLanes, 0, (cudaStream_t)stream>>>(g, splits, h, rows,
+                                                                                           cols, dpre, db,
+                                                                                           accumulate);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }

@@ -268,16 +268,22 @@ def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str):
     return pre, _activate(pre, act)
 
 
-def _input_grad(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-    """dpre @ w^T on the device, split-K over the layer's output width."""
+def _input_grad_parts(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """dpre @ w^T on the device as [splits, rows, in] partial products,
+    split-K over the layer's output width (splits = 1: the product itself)."""
     rows, n = dpre.shape
     k = w.shape[0]
     s = _splitk(rows, n, k)
     if s > 1:
         dpre = dpre if dpre.is_contiguous() else dpre.contiguous()
-        part = torch.bmm(dpre.view(rows, s, n // s).transpose(0, 1), w.view(k, s, n // s).permute(1, 2, 0))
-        return _splitk_reduce(part, None, "linear")
-    return torch.mm(dpre, w.t())
+        return torch.bmm(dpre.view(rows, s, n // s).transpose(0, 1), w.view(k, s, n // s).permute(1, 2, 0))
+    return torch.mm(dpre, w.t()).unsqueeze(0)
+
+
+def _input_grad(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """dpre @ w^T on the device (split-K partials reduced in one launch)."""
+    part = _input_grad_parts(dpre, w)
+    return part[0] if part.shape[0] == 1 else _splitk_reduce(part, None, "linear")
 
 
 def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int,
@@ -338,31 +344,38 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
     """Backpropagate through the stash (stages.py:187-209). Parameter grads go
     into stage.flat.grad's views (overwritten, or added when `accumulate`);
     the input gradient uses `weights` — the view at BACKWARD time.
-    Returns (grad wrt stage input or None, list of parameter-grad views)."""
+    Returns (grad wrt stage input or None, list of parameter-grad views).
+
+    On the device an input gradient that feeds a ReLU layer stays as its
+    split-K partial products: po_relu_bwd_bias sums them (fixed order) in the
+    same launch that applies the ReLU mask and forms the bias gradient."""
     entry = stage.stash.pop(key)
     gviews = stage.flat.grads
-    g = grad_out
+    if not grad_out.is_cuda:
+        return _stage_backward_host(stage, entry, weights, gviews, grad_out, accumulate, need_input_grad)
+    from . import _lib
+
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(grad_out.device).cuda_stream
+    g = (grad_out if grad_out.is_contiguous() else grad_out.contiguous()).unsqueeze(0)  # [splits, rows, cols]
     for i in reversed(range(len(stage.layers))):
         spec = stage.layers[i]
         x = entry.layer_inputs[i]
         gw, gb = gviews[2 * i], gviews[2 * i + 1]
-        if g.is_cuda and spec.activation == "relu":
-            # dpre = g * (pre > 0) and db = colsum(dpre) in one launch
-            from . import _lib
-
-            gc = g if g.is_contiguous() else g.contiguous()
-            dpre = torch.empty_like(gc)
-            rows, cols = gc.shape
-            rc = _lib.load().po_relu_bwd_bias(gc.data_ptr(), entry.pre_acts[i].data_ptr(), rows, cols,
-                                              dpre.data_ptr(), gb.data_ptr(), int(accumulate),
-                                              torch.cuda.current_stream(g.device).cuda_stream)
+        if spec.activation == "relu":
+            # sum of the partials, dpre = g * (pre > 0) and db = colsum(dpre) in one launch
+            splits, rows, cols = g.shape
+            dpre = torch.empty((rows, cols), dtype=torch.float32, device=g.device)
+            rc = lib.po_relu_bwd_bias(g.data_ptr(), splits, entry.pre_acts[i].data_ptr(), rows, cols,
+                                      dpre.data_ptr(), gb.data_ptr(), int(accumulate), stream)
             _lib.check(rc, "po_relu_bwd_bias")
             if accumulate:
                 gw.addmm_(x.t(), dpre)
             else:
                 torch.mm(x.t(), dpre, out=gw)
         else:
-            dpre = _activation_grad_mul(g, entry.pre_acts[i], spec.activation)
+            gfull = g[0] if g.shape[0] == 1 else _splitk_reduce(g, None, "linear")
+            dpre = _activation_grad_mul(gfull, entry.pre_acts[i], spec.activation)
             if accumulate:
                 gw.addmm_(x.t(), dpre)
                 gb.add_(dpre.sum(dim=0, keepdim=True))
@@ -370,9 +383,28 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
                 torch.mm(x.t(), dpre, out=gw)
                 torch.sum(dpre, dim=0, keepdim=True, out=gb)
         if i > 0 or need_input_grad:
-            g = _input_grad(dpre, weights[2 * i]) if dpre.is_cuda else torch.mm(dpre, weights[2 * i].t())
+            g = _input_grad_parts(dpre, weights[2 * i])
         else:
             g = None
+    if g is not None:
+        g = g[0] if g.shape[0] == 1 else _splitk_reduce(g, None, "linear")
+    return g, gviews
+
+
+def _stage_backward_host(stage, entry, weights, gviews, g, accumulate, need_input_grad):
+    """CPU tensors (the gloo tests of the distributed runner): plain torch."""
+    for i in reversed(range(len(stage.layers))):
+        spec = stage.layers[i]
+        x = entry.layer_inputs[i]
+        gw, gb = gviews[2 * i], gviews[2 * i + 1]
+        dpre = _activation_grad_mul(g, entry.pre_acts[i], spec.activation)
+        if accumulate:
+            gw.addmm_(x.t(), dpre)
+            gb.add_(dpre.sum(dim=0, keepdim=True))
+        else:
+            torch.mm(x.t(), dpre, out=gw)
+            torch.sum(dpre, dim=0, keepdim=True, out=gb)
+        g = torch.mm(dpre, weights[2 * i].t()) if (i > 0 or need_input_grad) else None
     return g, gviews
 
 

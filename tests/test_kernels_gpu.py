@@ -359,13 +359,22 @@ def test_relu_bwd_bias_matches_reference(rows, cols, accumulate, alias):
     gd, hd = torch.from_numpy(g).cuda(), torch.from_numpy(h).cuda()
     dpre = gd if alias else torch.empty_like(gd)
     db = torch.from_numpy(db0).cuda()
-    rc = _lib.load().po_relu_bwd_bias(gd.data_ptr(), hd.data_ptr(), rows, cols, dpre.data_ptr(), db.data_ptr(),
+    rc = _lib.load().po_relu_bwd_bias(gd.data_ptr(), 1, hd.data_ptr(), rows, cols, dpre.data_ptr(), db.data_ptr(),
                                       accumulate, torch.cuda.current_stream().cuda_stream)
     assert rc == 0
     want = g * (pre > 0)
     assert np.array_equal(host(dpre), want)
     want_db = want.astype(np.float64).sum(axis=0) + (db0.astype(np.float64) if accumulate else 0.0)
     np.testing.assert_allclose(host(db), want_db, rtol=1e-5, atol=1e-5)
+    if rows and not alias:  # g as 3 split-K partials, summed in order 0, 1, 2
+        parts = np.stack([g * 0.5, g * 0.25, g * 0.25]).astype(np.float32)
+        pd = torch.from_numpy(parts).cuda()
+        db2 = torch.zeros(cols, device="cuda")
+        rc = _lib.load().po_relu_bwd_bias(pd.data_ptr(), 3, hd.data_ptr(), rows, cols, dpre.data_ptr(),
+                                          db2.data_ptr(), 0, torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        summed = (parts[0] + parts[1]) + parts[2]
+        assert np.array_equal(host(dpre), summed * (pre > 0))
 
 
 @pytest.mark.parametrize("rows,k,n", [(128, 3072, 1024), (128, 1024, 1024), (128, 1024, 10), (64, 512, 96),
