@@ -197,9 +197,10 @@ int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t r
  * affine + activation): out = act(sum_{s=0..splits-1} part[s] + bias), the
  * partials summed in that fixed order (deterministic). part: [splits x rows x
  * cols], bias: [cols] or NULL, act: 0 linear, 1 relu, 2 tanh; pre_out
- * (nullable) receives the pre-activation. */
+ * (nullable) receives the pre-activation. flags (nullable): flags[flag_index]
+ * = 0 if any output is NaN/Inf (po_all_finite folded into the epilogue). */
 int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t cols, const float* bias,
-                       int32_t act, float* out, float* pre_out, void* stream);
+                       int32_t act, float* out, float* pre_out, uint8_t* flags, int64_t flag_index, void* stream);
 
 /* Backward elementwise part of a ReLU layer fused with its bias gradient
  * (stages.py:200-206, linalg.py:185-194): dpre = g * (pre > 0) written to
@@ -211,6 +212,11 @@ int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t 
  * alias dpre. */
 int po_relu_bwd_bias(const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols, float* dpre,
                      float* db, int32_t accumulate, void* stream);
+
+/* Same for act = 1 (relu, as above) or act = 0 (linear: dpre = g, no mask,
+ * h unused): a linear layer's bias gradient and summed split-K partials. */
+int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols,
+                    float* dpre, float* db, int32_t accumulate, void* stream);
 
 /* ---- peer-memory boundary transport (pipeoptim_p2p.cu) ------------------
  * Replaces the simulated hand-off dicts of the reference executor

@@ -35,6 +35,7 @@ EXPORTS = (
     "po_loss_grad",
     "po_relu_bwd_bias",
     "po_splitk_bias_act",
+    "po_act_bwd_bias",
     "po_dp_signal",
     "po_step_predict_dp",
     "po_p2p_send",
@@ -110,7 +111,10 @@ _SIGNATURES = {
     "po_all_finite": (ctypes.c_int, [_P, _I64, _P, _I64, _P]),
     "po_loss_grad": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, _I64, _P, _P, _P, _P]),
     "po_relu_bwd_bias": (ctypes.c_int, [_P, ctypes.c_int32, _P, _I64, _I64, _P, _P, ctypes.c_int32, _P]),
-    "po_splitk_bias_act": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _I64, _P, ctypes.c_int32, _P, _P, _P]),
+    "po_splitk_bias_act": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _I64, _P, ctypes.c_int32, _P, _P, _P, _I64,
+                                          _P]),
+    "po_act_bwd_bias": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int32, _P, _I64, _I64, _P, _P, ctypes.c_int32,
+                                       _P]),
     "po_dp_signal": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _P]),
     "po_step_predict_dp": (ctypes.c_int, [_HP, _P, _P, ctypes.c_int32, _P, _P, _P, _I64, _D, _D, _I64, _P, _P, _I64,
                                           _I64, _P, _P]),

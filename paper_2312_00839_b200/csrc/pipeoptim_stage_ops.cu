@@ -145,7 +145,7 @@ constexpr int kReluCols = 8, kReluLanes = 32;
 // g and dpre may alias when splits == 1 (each element is read, then written,
 // by one thread)
 __global__ void relu_bwd_bias_kernel(const float* g, int splits, const float* __restrict__ h, int64_t rows,
-                                     int64_t cols, float* dpre, float* __restrict__ db, int accumulate) {
+                                     int64_t cols, float* dpre, float* __restrict__ db, int accumulate, int mask) {
   const int64_t n = rows * cols;
   __shared__ float part[kReluLanes][kReluCols];
   const int cl = threadIdx.x % kReluCols, lane = threadIdx.x / kReluCols;
@@ -157,7 +157,7 @@ __global__ void relu_bwd_bias_kernel(const float* g, int splits, const float* __
       const int64_t i = r * cols + c;
       float gi = g[i];
       for (int s = 1; s < splits; ++s) gi += g[(int64_t)s * n + i];
-      const float v = h[i] > 0.f ? gi : 0.f;  // g * (pre > 0): relu(pre) > 0 <=> pre > 0
+      const float v = (!mask || h[i] > 0.f) ? gi : 0.f;  // g * (pre > 0): relu(pre) > 0 <=> pre > 0
       dpre[i] = v;
       acc += v;
     }
@@ -174,17 +174,63 @@ __global__ void relu_bwd_bias_kernel(const float* g, int splits, const float* __
 
 // out[i] = act(sum_s part[s*n + i] + bias[i % cols]), s in order 0..S-1;
 // pre_out (nullable) receives the pre-activation. act: 0 linear, 1 relu, 2 tanh.
+// flags (nullable): flags[flag_index] = 0 if any output is NaN/Inf — the
+// stage-output finiteness check (stages.py:182) folded into the epilogue.
+__device__ __forceinline__ float act_fn(float x, int act) {
+  return act == 1 ? (x > 0.f ? x : 0.f) : act == 2 ? tanhf(x) : x;
+}
+
+template <bool VEC4>
 __global__ void splitk_bias_act_kernel(const float* __restrict__ part, int S, int64_t n, int64_t cols,
                                        const float* __restrict__ bias, int act, float* __restrict__ out,
-                                       float* __restrict__ pre_out) {
+                                       float* __restrict__ pre_out, uint8_t* flags, int64_t flag_index) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    float acc = part[i];
-    for (int s = 1; s < S; ++s) acc += part[(int64_t)s * n + i];
-    if (bias != nullptr) acc += bias[i % cols];
-    if (pre_out != nullptr) pre_out[i] = acc;
-    out[i] = act == 1 ? (acc > 0.f ? acc : 0.f) : act == 2 ? tanhf(acc) : acc;
+  bool bad = false;
+  if constexpr (VEC4) {
+    const int64_t n4 = n / 4;
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+      float4 acc = p4[i];
+      int s = 1;
+      for (; s + 3 < S; s += 4) {  // four independent loads in flight, summed in order
+        const float4 a = p4[(int64_t)s * n4 + i], b = p4[(int64_t)(s + 1) * n4 + i];
+        const float4 c = p4[(int64_t)(s + 2) * n4 + i], d = p4[(int64_t)(s + 3) * n4 + i];
+        acc.x = (((acc.x + a.x) + b.x) + c.x) + d.x;
+        acc.y = (((acc.y + a.y) + b.y) + c.y) + d.y;
+        acc.z = (((acc.z + a.z) + b.z) + c.z) + d.z;
+        acc.w = (((acc.w + a.w) + b.w) + c.w) + d.w;
+      }
+      for (; s < S; ++s) {
+        const float4 a = p4[(int64_t)s * n4 + i];
+        acc.x += a.x;
+        acc.y += a.y;
+        acc.z += a.z;
+        acc.w += a.w;
+      }
+      if (bias != nullptr) {
+        const float4 bv = reinterpret_cast<const float4*>(bias)[(i * 4 % cols) / 4];
+        acc.x += bv.x;
+        acc.y += bv.y;
+        acc.z += bv.z;
+        acc.w += bv.w;
+      }
+      if (pre_out != nullptr) reinterpret_cast<float4*>(pre_out)[i] = acc;
+      float4 o = make_float4(act_fn(acc.x, act), act_fn(acc.y, act), act_fn(acc.z, act), act_fn(acc.w, act));
+      reinterpret_cast<float4*>(out)[i] = o;
+      bad |= !isfinite(o.x) | !isfinite(o.y) | !isfinite(o.z) | !isfinite(o.w);
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      float acc = part[i];
+      for (int s = 1; s < S; ++s) acc += part[(int64_t)s * n + i];
+      if (bias != nullptr) acc += bias[i % cols];
+      if (pre_out != nullptr) pre_out[i] = acc;
+      const float o = act_fn(acc, act);
+      out[i] = o;
+      bad |= !isfinite(o);
+    }
   }
+  if (flags != nullptr && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags[flag_index] = 0;
 }
 
 int sm_count_ops() {
@@ -196,6 +242,9 @@ int sm_count_ops() {
 }  // namespace
 
 extern "C" {
+
+int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols,
+                    float* dpre, float* db, int32_t accumulate, void* stream);
 
 int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void* stream) {
   if (n < 0 || flags == nullptr || index < 0 || (n > 0 && x == nullptr)) return PO_EINVAL;
@@ -211,25 +260,39 @@ int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void
 }
 
 int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t cols, const float* bias,
-                       int32_t act, float* out, float* pre_out, void* stream) {
-  if (splits < 1 || rows < 0 || cols < 1 || act < 0 || act > 2 || out == nullptr || (rows > 0 && part == nullptr))
+                       int32_t act, float* out, float* pre_out, uint8_t* flags, int64_t flag_index, void* stream) {
+  if (splits < 1 || rows < 0 || cols < 1 || act < 0 || act > 2 || out == nullptr || (rows > 0 && part == nullptr) ||
+      flag_index < 0)
     return PO_EINVAL;
   const int64_t n = rows * cols;
   if (n == 0) return 0;
   static int sms = 0;
   if (sms == 0) sms = sm_count_ops();
   const int block = 256;
-  int64_t want = (n + block - 1) / block;
+  const bool vec = cols % 4 == 0 && ((reinterpret_cast<uintptr_t>(part) | reinterpret_cast<uintptr_t>(out) |
+                                      reinterpret_cast<uintptr_t>(pre_out) | reinterpret_cast<uintptr_t>(bias)) &
+                                     15) == 0;
+  int64_t want = ((vec ? n / 4 : n) + block - 1) / block;
   const int64_t grid = want > 8 * sms ? 8 * sms : want;
-  splitk_bias_act_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(part, splits, n, cols, bias, act, out,
-                                                                            pre_out);
+  if (vec)
+    splitk_bias_act_kernel<true><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(part, splits, n, cols, bias, act,
+                                                                                    out, pre_out, flags, flag_index);
+  else
+    splitk_bias_act_kernel<false><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(part, splits, n, cols, bias,
+                                                                                     act, out, pre_out, flags,
+                                                                                     flag_index);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }
 
 int po_relu_bwd_bias(const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols, float* dpre,
                      float* db, int32_t accumulate, void* stream) {
-  if (rows < 0 || cols < 0 || splits < 1) return PO_EINVAL;
+  return po_act_bwd_bias(1, g, splits, h, rows, cols, dpre, db, accumulate, stream);
+}
+
+int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols,
+                    float* dpre, float* db, int32_t accumulate, void* stream) {
+  if (rows < 0 || cols < 0 || splits < 1 || (act != 0 && act != 1)) return PO_EINVAL;
   if (rows == 0 || cols == 0) {
     if (cols > 0 && !accumulate && db != nullptr) {
       cudaError_t e = cudaMemsetAsync(db, 0, (size_t)cols * sizeof(float), (cudaStream_t)stream);
@@ -237,12 +300,12 @@ int po_relu_bwd_bias(const float* g, int32_t splits, const float* h, int64_t row
     }
     return 0;
   }
-  if (g == nullptr || h == nullptr || dpre == nullptr || db == nullptr) return PO_EINVAL;
+  if (g == nullptr || (act == 1 && h == nullptr) || dpre == nullptr || db == nullptr) return PO_EINVAL;
   const int64_t grid = (cols + kReluCols - 1) / kReluCols;
   if (grid > 0x7fffffff) return PO_EINVAL;
   relu_bwd_bias_kernel<<<(unsigned)grid, kReluCols * kReluLanes, 0, (cudaStream_t)stream>>>(g, splits, h, rows,
                                                                                            cols, dpre, db,
-                                                                                           accumulate);
+                                                                                           accumulate, act);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }

@@ -232,8 +232,9 @@ def _splitk(rows: int, k: int, n: int) -> int:
     return s
 
 
-def _splitk_reduce(part: torch.Tensor, bias, act: str, pre_out=None) -> torch.Tensor:
-    """act(sum_s part[s] + bias) in one launch (po_splitk_bias_act)."""
+def _splitk_reduce(part: torch.Tensor, bias, act: str, pre_out=None, flags=None, flag_index: int = 0):
+    """act(sum_s part[s] + bias) in one launch (po_splitk_bias_act); with
+    `flags`, flags[flag_index] is cleared if any output is non-finite."""
     from . import _lib
 
     splits, rows, cols = part.shape
@@ -241,14 +242,17 @@ def _splitk_reduce(part: torch.Tensor, bias, act: str, pre_out=None) -> torch.Te
     rc = _lib.load().po_splitk_bias_act(part.data_ptr(), splits, rows, cols,
                                         None if bias is None else bias.data_ptr(), _ACT_CODE[act], out.data_ptr(),
                                         None if pre_out is None else pre_out.data_ptr(),
+                                        None if flags is None else flags.data_ptr(), flag_index,
                                         torch.cuda.current_stream(part.device).cuda_stream)
     _lib.check(rc, "po_splitk_bias_act")
     return out
 
 
-def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str):
-    """Device forward of one layer: (pre, h_out) with the stash's convention —
-    relu layers stash relu(pre) (its sign pattern is pre's), others pre."""
+def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str, flags=None, flag_index: int = 0):
+    """Device forward of one layer: (pre, h_out, checked) with the stash's
+    convention — relu layers stash relu(pre) (its sign pattern is pre's),
+    others pre. checked: the finiteness flag was already written (split-K
+    epilogue)."""
     rows, k = h.shape
     n = w.shape[1]
     s = _splitk(rows, k, n)
@@ -258,14 +262,15 @@ def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str):
         bias = b.view(-1)
         if act == "tanh":
             pre = torch.empty((rows, n), dtype=torch.float32, device=h.device)
-            return pre, _splitk_reduce(part, bias, act, pre_out=pre)
-        out = _splitk_reduce(part, bias, act)
-        return out, out
+            return pre, _splitk_reduce(part, bias, act, pre_out=pre, flags=flags, flag_index=flag_index), \
+                flags is not None
+        out = _splitk_reduce(part, bias, act, flags=flags, flag_index=flag_index)
+        return out, out, flags is not None
     if act == "relu":
         out = torch._addmm_activation(b.view(-1), h, w)
-        return out, out
+        return out, out, False
     pre = torch.addmm(b.view(-1), h, w)
-    return pre, _activate(pre, act)
+    return pre, _activate(pre, act), False
 
 
 def _input_grad_parts(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
@@ -301,13 +306,17 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
     inputs, pres = [], []
     h = x
     fused = x.is_cuda
+    checked = False
+    last = len(stage.layers) - 1
     for i, spec in enumerate(stage.layers):
         w, b = weights[2 * i], weights[2 * i + 1]
         inputs.append(h)
         if fused:
-            # split-K GEMM + one reduce/bias/activation launch, or bias + ReLU
-            # in the cuBLASLt epilogue; relu layers stash relu(pre)
-            pre, h = _affine(h, w, b, spec.activation)
+            # split-K GEMM + one reduce/bias/activation launch (which also
+            # writes the deferred finiteness flag of the stage output), or bias
+            # + ReLU in the cuBLASLt epilogue; relu layers stash relu(pre)
+            want_flag = i == last and not check_finite and finite_flags is not None
+            pre, h, checked = _affine(h, w, b, spec.activation, finite_flags if want_flag else None, flag_index)
             pres.append(pre)
             continue
         pre = torch.addmm(b, h, w)
@@ -319,7 +328,7 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
             raise NumericError(
                 f"non-finite value in stage {stage.rank} forward output at entry ({bad[0]}, {bad[1]})"
             )
-    elif finite_flags is not None:
+    elif finite_flags is not None and not checked:
         record_finite(h, finite_flags, flag_index)
     stage.stash.put(key, StashEntry(version, inputs, pres))
     return h
@@ -362,13 +371,14 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
         spec = stage.layers[i]
         x = entry.layer_inputs[i]
         gw, gb = gviews[2 * i], gviews[2 * i + 1]
-        if spec.activation == "relu":
-            # sum of the partials, dpre = g * (pre > 0) and db = colsum(dpre) in one launch
+        if spec.activation in ("relu", "linear"):
+            # sum of the partials, dpre = g * act'(pre) and db = colsum(dpre) in one launch
             splits, rows, cols = g.shape
             dpre = torch.empty((rows, cols), dtype=torch.float32, device=g.device)
-            rc = lib.po_relu_bwd_bias(g.data_ptr(), splits, entry.pre_acts[i].data_ptr(), rows, cols,
-                                      dpre.data_ptr(), gb.data_ptr(), int(accumulate), stream)
-            _lib.check(rc, "po_relu_bwd_bias")
+            relu = spec.activation == "relu"
+            rc = lib.po_act_bwd_bias(int(relu), g.data_ptr(), splits, entry.pre_acts[i].data_ptr() if relu else None,
+                                     rows, cols, dpre.data_ptr(), gb.data_ptr(), int(accumulate), stream)
+            _lib.check(rc, "po_act_bwd_bias")
             if accumulate:
                 gw.addmm_(x.t(), dpre)
             else:

@@ -393,7 +393,9 @@ def test_split_k_layer_forward_and_input_grad(rows, k, n, act):
     x = torch.randn(rows, k, device="cuda", generator=g)
     w = torch.randn(k, n, device="cuda", generator=g) / k ** 0.5
     b = torch.randn(1, n, device="cuda", generator=g)
-    pre, h = _affine(x, w, b, act)
+    flags = torch.ones(3, dtype=torch.bool, device="cuda")
+    pre, h, checked = _affine(x, w, b, act, flags, 1)
+    assert bool(flags.all()) and checked == (_splitk(rows, k, n) > 1)
     want_pre = x.double() @ w.double() + b.double()
     want_h = {"relu": want_pre.clamp_min(0), "linear": want_pre, "tanh": torch.tanh(want_pre)}[act]
     tol = 2e-6 * float(want_pre.abs().max()) * (k ** 0.5)
@@ -407,6 +409,33 @@ def test_split_k_layer_forward_and_input_grad(rows, k, n, act):
     want_gi = dpre.double() @ w.double().t()
     assert float((gi.double() - want_gi).abs().max()) <= 2e-6 * float(want_gi.abs().max()) * (n ** 0.5)
     assert _splitk(128, 3072, 1024) == 8 and _splitk(128, 24, 20) == 1
+    if checked:  # a non-finite output clears the stage-output flag in the same launch
+        x[3, 5] = float("inf")
+        _, h2, _ = _affine(x, w, b, act, flags, 2)
+        assert not bool(torch.isfinite(h2).all()) or act == "tanh"  # tanh(+-inf) is finite
+        assert flags.tolist() == [True, True, bool(torch.isfinite(h2).all())]
+
+
+@pytest.mark.parametrize("splits", [1, 4])
+def test_linear_act_bwd_bias(splits):
+    """po_act_bwd_bias(act=0): dpre = sum of the split-K partials (fixed
+    order), db = colsum(dpre) — a linear layer's backward epilogue."""
+    import torch
+
+    from paper_2312_00839_b200 import _lib
+
+    rows, cols = 128, 10
+    g = torch.randn(splits, rows, cols, device="cuda")
+    dpre = torch.empty(rows, cols, device="cuda")
+    db = torch.zeros(cols, device="cuda")
+    rc = _lib.load().po_act_bwd_bias(0, g.data_ptr(), splits, None, rows, cols, dpre.data_ptr(), db.data_ptr(), 0,
+                                     torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    want = g[0].clone()
+    for s_ in range(1, splits):
+        want = want + g[s_]
+    assert torch.equal(dpre, want)
+    np.testing.assert_allclose(host(db), want.double().sum(0).cpu().numpy(), rtol=1e-5, atol=1e-5)
 
 
 def test_more_than_2_31_elements(lib):
