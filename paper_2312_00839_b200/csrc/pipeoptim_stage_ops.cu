@@ -190,17 +190,21 @@ __global__ void splitk_bias_act_kernel(const float* __restrict__ part, int S, in
     const int64_t n4 = n / 4;
     const float4* p4 = reinterpret_cast<const float4*>(part);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-      float4 acc = p4[i];
-      int s = 1;
-      for (; s + 3 < S; s += 4) {  // four independent loads in flight, summed in order
-        const float4 a = p4[(int64_t)s * n4 + i], b = p4[(int64_t)(s + 1) * n4 + i];
-        const float4 c = p4[(int64_t)(s + 2) * n4 + i], d = p4[(int64_t)(s + 3) * n4 + i];
-        acc.x = (((acc.x + a.x) + b.x) + c.x) + d.x;
-        acc.y = (((acc.y + a.y) + b.y) + c.y) + d.y;
-        acc.z = (((acc.z + a.z) + b.z) + c.z) + d.z;
-        acc.w = (((acc.w + a.w) + b.w) + c.w) + d.w;
-      }
-      for (; s < S; ++s) {
+      // up to 8 partials' loads issued together, then summed in order 0..S-1
+      float4 v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < S) v[s] = p4[(int64_t)s * n4 + i];
+      float4 acc = v[0];
+#pragma unroll
+      for (int s = 1; s < 8; ++s)
+        if (s < S) {
+          acc.x += v[s].x;
+          acc.y += v[s].y;
+          acc.z += v[s].z;
+          acc.w += v[s].w;
+        }
+      for (int s = 8; s < S; ++s) {
         const float4 a = p4[(int64_t)s * n4 + i];
         acc.x += a.x;
         acc.y += a.y;
@@ -268,7 +272,7 @@ int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t 
   if (n == 0) return 0;
   static int sms = 0;
   if (sms == 0) sms = sm_count_ops();
-  const int block = 256;
+  const int block = 128;  // a 128 x 1024 output is 256 CTAs: every SM gets work
   const bool vec = cols % 4 == 0 && ((reinterpret_cast<uintptr_t>(part) | reinterpret_cast<uintptr_t>(out) |
                                       reinterpret_cast<uintptr_t>(pre_out) | reinterpret_cast<uintptr_t>(bias)) &
                                      15) == 0;
