@@ -270,6 +270,19 @@ int po_lstm_cell_fwd(float* gates, const float* c_prev, float* c_out, float* h_o
 int po_lstm_cell_bwd(const float* act, const float* c_prev, const float* c, const float* dy, int64_t dy_ld,
                      const float* dh_rec, float* dc, float* dgates, int64_t batch, int64_t hidden, void* stream);
 
+/* The same two steps with the recurrent GEMM run split-K: `rec` holds the
+ * `splits` partial products [splits x batch x 4*hidden] of h_{t-1} W_hh^T
+ * (added to `gates`, which then carries only the input projection), and
+ * `dh_rec` the partials [splits x batch x hidden] of dgates_{t+1} W_hh_live —
+ * each summed in order inside the cell kernel (no reduction pass). The batch
+ * x 4H / batch x H recurrent GEMMs have too few output tiles to fill the GPU
+ * as single GEMMs. */
+int po_lstm_cell_fwd_sk(float* gates, const float* rec, int32_t splits, const float* c_prev, float* c_out,
+                        float* h_out, float* y_out, int64_t y_ld, int64_t batch, int64_t hidden, void* stream);
+int po_lstm_cell_bwd_sk(const float* act, const float* c_prev, const float* c, const float* dy, int64_t dy_ld,
+                        const float* dh_rec, int32_t splits, float* dc, float* dgates, int64_t batch, int64_t hidden,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,8 @@ EXPORTS = (
     "po_ipc_free",
     "po_lstm_cell_fwd",
     "po_lstm_cell_bwd",
+    "po_lstm_cell_fwd_sk",
+    "po_lstm_cell_bwd_sk",
 )
 
 PO_LOSS_MSE, PO_LOSS_SOFTMAX_XENT = 0, 1
@@ -126,6 +128,8 @@ _SIGNATURES = {
     "po_ipc_free": (ctypes.c_int, [_P]),
     "po_lstm_cell_fwd": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
     "po_lstm_cell_bwd": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _P, _P, _I64, _I64, _P]),
+    "po_lstm_cell_fwd_sk": (ctypes.c_int, [_P, _P, ctypes.c_int32, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
+    "po_lstm_cell_bwd_sk": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, ctypes.c_int32, _P, _P, _I64, _I64, _P]),
 }
 
 _lock = threading.Lock()

@@ -350,11 +350,15 @@ def module_stages_for(torch, name, device, depth=None, costs=None, amp=None):
 
 
 def _module_setup(torch, device, name, strategy, n_batches, amp=None):
+    """Stages for the single-GPU runs: every stage shares the one GPU, so the
+    LSTM recurrences use the SM-time-efficient unsplit GEMMs."""
     from .optim import OptimizerConfig, OptimizerState
     from .runtime import build_timeline
+    from .stage_models import set_lstm_split_k
 
     cfg = MODULE_CONFIGS[name]
     stages, _ = module_stages_for(torch, name, device, amp=amp)
+    set_lstm_split_k(stages, False)
     kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
     opts = [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in stages]
     return stages, opts, build_timeline(strategy, cfg["depth"], n_batches)

@@ -37,7 +37,7 @@ import torch.nn.functional as F
 from . import _lib
 from .errors import NumericError
 from .optim import FlatParams
-from .stages import ActivationStash, StashEntry, record_finite
+from .stages import ActivationStash, StashEntry, _splitk, record_finite
 
 
 class _LiveLinearFn(torch.autograd.Function):
@@ -126,10 +126,11 @@ class _LiveLSTMFn(torch.autograd.Function):
 
     Layout: time-major inside (x^T (T, B, Din), gates (T, B, 4H), h (T+1, B, H),
     c (T, B, H)), batch-first at the boundary. Forward: one GEMM for all
-    input projections, then per step one cuBLAS GEMM (gates_t += h_{t-1}
-    W_hh^T) and one po_lstm_cell_fwd. Backward: per step one po_lstm_cell_bwd
-    and one GEMM (dh_{t-1} = dgates_t W_hh_live), then three GEMMs over all
-    steps (dx, dW_ih, dW_hh) and a column sum (db)."""
+    input projections, then per step one split-K batched GEMM (h_{t-1}
+    W_hh^T) and one po_lstm_cell_fwd_sk that sums its partials into the
+    gates. Backward: per step one po_lstm_cell_bwd_sk (summing the partials
+    of dh) and one split-K GEMM (dh_{t-1} = dgates_t W_hh_live), then three
+    GEMMs over all steps (dx, dW_ih, dW_hh) and a column sum (db)."""
 
     @staticmethod
     def forward(ctx, x, w_ih, w_hh, b_ih, b_hh, module):
@@ -145,12 +146,24 @@ class _LiveLSTMFn(torch.autograd.Function):
         cs = torch.empty((steps, bsz, hid), device=x.device, dtype=x.dtype)
         y = torch.empty((bsz, steps, hid), device=x.device, dtype=x.dtype)
         w_hh_t = w_hh.t()
+        # the recurrent GEMM (batch x H @ H x 4H) has few output tiles: run it
+        # split-K and let the cell kernel sum the partials (po_lstm_cell_fwd_sk)
+        sk = _splitk(bsz, hid, 4 * hid) if module.split_k else 1
+        if sk > 1:
+            w_split = w_hh.view(4 * hid, sk, hid // sk).permute(1, 2, 0)  # (S, H/S, 4H) slices of W_hh^T
+            part = torch.empty((sk, bsz, 4 * hid), device=x.device, dtype=x.dtype)
         for t in range(steps):
+            rec = None
             if t > 0:
-                gates[t].addmm_(hs[t], w_hh_t)
-            rc = lib.po_lstm_cell_fwd(gates[t].data_ptr(), cs[t - 1].data_ptr() if t else None, cs[t].data_ptr(),
-                                      hs[t + 1].data_ptr(), y[:, t].data_ptr(), steps * hid, bsz, hid, stream)
-            _lib.check(rc, "po_lstm_cell_fwd")
+                if sk > 1:
+                    torch.bmm(hs[t].view(bsz, sk, hid // sk).transpose(0, 1), w_split, out=part)
+                    rec = part.data_ptr()
+                else:
+                    gates[t].addmm_(hs[t], w_hh_t)
+            rc = lib.po_lstm_cell_fwd_sk(gates[t].data_ptr(), rec, sk, cs[t - 1].data_ptr() if t else None,
+                                         cs[t].data_ptr(), hs[t + 1].data_ptr(), y[:, t].data_ptr(), steps * hid, bsz,
+                                         hid, stream)
+            _lib.check(rc, "po_lstm_cell_fwd_sk")
         ctx.save_for_backward(xt, gates, hs, cs)
         ctx.module = module
         return y
@@ -168,16 +181,23 @@ class _LiveLSTMFn(torch.autograd.Function):
         dy = dy.contiguous()
         dg = torch.empty_like(gates)
         dc = torch.zeros((bsz, hid), device=dy.device, dtype=dy.dtype)
-        ping = torch.empty((2, bsz, hid), device=dy.device, dtype=dy.dtype)
+        # dh_{t-1} = dgates_t W_hh_live (batch x 4H @ 4H x H): split-K, the
+        # partials summed inside po_lstm_cell_bwd_sk
+        sk = _splitk(bsz, hid4, hid) if m.split_k else 1
+        w_split = w_hh.view(sk, hid4 // sk, hid)
+        ping = torch.empty((2, sk, bsz, hid), device=dy.device, dtype=dy.dtype)
         rec = None
         for t in range(steps - 1, -1, -1):
-            rc = lib.po_lstm_cell_bwd(gates[t].data_ptr(), cs[t - 1].data_ptr() if t else None, cs[t].data_ptr(),
-                                      dy[:, t].data_ptr(), steps * hid, rec, dc.data_ptr(), dg[t].data_ptr(), bsz,
-                                      hid, stream)
-            _lib.check(rc, "po_lstm_cell_bwd")
+            rc = lib.po_lstm_cell_bwd_sk(gates[t].data_ptr(), cs[t - 1].data_ptr() if t else None, cs[t].data_ptr(),
+                                         dy[:, t].data_ptr(), steps * hid, rec, sk, dc.data_ptr(), dg[t].data_ptr(),
+                                         bsz, hid, stream)
+            _lib.check(rc, "po_lstm_cell_bwd_sk")
             if t > 0:
                 buf = ping[t % 2]
-                torch.mm(dg[t], w_hh, out=buf)
+                if sk > 1:
+                    torch.bmm(dg[t].view(bsz, sk, hid4 // sk).transpose(0, 1), w_split, out=buf)
+                else:
+                    torch.mm(dg[t], w_hh, out=buf[0])
                 rec = buf.data_ptr()
         dg2 = dg.view(steps * bsz, hid4)
         dx = None
@@ -201,6 +221,10 @@ class LiveLSTM(nn.Module):
     def __init__(self, input_size: int, hidden_size: int):
         super().__init__()
         self.input_size, self.hidden_size = input_size, hidden_size
+        # split-K recurrent GEMMs: lower latency per step (a stage alone on its
+        # GPU, the pipeline's critical path) at more SM-time per step; stages
+        # sharing one GPU concurrently prefer the unsplit GEMMs (set_lstm_split_k)
+        self.split_k = True
         h4 = 4 * hidden_size
         self.weight_ih_l0 = nn.Parameter(torch.empty(h4, input_size))
         self.weight_hh_l0 = nn.Parameter(torch.empty(h4, hidden_size))
@@ -213,6 +237,15 @@ class LiveLSTM(nn.Module):
     def forward(self, x):
         return _LiveLSTMFn.apply(x, self.weight_ih_l0, self.weight_hh_l0, self.bias_ih_l0, self.bias_hh_l0,
                                  self), None
+
+
+def set_lstm_split_k(stages, flag: bool) -> None:
+    """Latency (split-K, one stage per GPU) or SM-time (unsplit, stages
+    sharing a GPU) recurrent GEMMs for every LiveLSTM of the stages."""
+    for st in stages:
+        for m in st.module.modules():
+            if isinstance(m, LiveLSTM):
+                m.split_k = flag
 
 
 class _LSTMBlock(nn.Module):

@@ -141,7 +141,7 @@ def test_live_lstm_matches_cudnn_when_weights_coincide(bsz, steps, d_in, hid):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("bsz,steps,d_in,hid", [(4, 9, 8, 12), (16, 30, 128, 64)])
+@pytest.mark.parametrize("bsz,steps,d_in,hid", [(4, 9, 8, 12), (16, 30, 128, 64), (8, 5, 256, 1024)])
 def test_live_lstm_backward_uses_live_weights(bsz, steps, d_in, hid):
     """Forward on W_hat, then the parameters point back at the live buffer:
     dx / dh use the live weights, dW the stashed activations (S9). Compared
