@@ -93,7 +93,8 @@ def _port():
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("async_raw", "sgdm")])
+@pytest.mark.parametrize("strategy,kind", [("optimizer_prediction", "adam"), ("async_raw", "sgdm"),
+                                           ("spectrain", "sgdm")])
 def test_peer_runner_eager_matches_reference(tmp_path, world, strategy, kind):
     import torch.multiprocessing as mp
 
