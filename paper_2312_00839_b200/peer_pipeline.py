@@ -127,14 +127,22 @@ class PeerLinks:
             return pb.tensor
 
         self.next = self.prev = None
-        if rank < depth - 1:
-            h = handles[ranks[rank + 1]]
-            self.next = (open_(h[0]), open_(h[1]))  # (flags, act_ring) of stage k+1
-        if rank > 0:
-            h = handles[ranks[rank - 1]]
-            self.prev = (open_(h[0]), open_(h[2]))  # (flags, grad_ring) of stage k-1
+        err = None
+        try:
+            if rank < depth - 1:
+                h = handles[ranks[rank + 1]]
+                self.next = (open_(h[0]), open_(h[1]))  # (flags, act_ring) of stage k+1
+            if rank > 0:
+                h = handles[ranks[rank - 1]]
+                self.prev = (open_(h[0]), open_(h[2]))  # (flags, grad_ring) of stage k-1
+        except Exception as exc:  # every rank must learn of it, or the group desynchronises
+            err = exc
         self._lib = _lib.load()
-        dist.barrier(group=group)
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32,
+                          device=dev if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            raise RuntimeError(f"peer mapping failed on a rank of the pipeline (here: {err!r})")
 
     def _flag(self, t: torch.Tensor, word: int) -> int:
         return t.data_ptr() + 8 * word
@@ -374,8 +382,12 @@ __all__ = ["PeerLinks", "PeerStageRunner", "ring_slots"]
 # ---- bench support ---------------------------------------------------------------------------
 
 
+_BENCH_BROKEN: list = []  # a failed peer leg disables the later ones (each would wait out its timeouts)
+
+
 def bench_peer_pipeline(torch_mod, dist, rank, world, device, make_stage, data, loss_kind, lr, rows, n_batches,
-                        replays: int = 5, trials: int = 3, opt_kind: str = "adam", opt_kw: dict | None = None):
+                        replays: int = 5, trials: int = 3, opt_kind: str = "adam", opt_kw: dict | None = None,
+                        timeout_ms: int = 15_000):
     """Prediction off/on through the peer runner, one CUDA graph per rank per
     run: eager warm-up run, capture, one warm replay, then `trials` x
     `replays` timed replays per arm in alternation (median; device time of
@@ -385,17 +397,23 @@ def bench_peer_pipeline(torch_mod, dist, rank, world, device, make_stage, data, 
     from .optim import OptimizerConfig, OptimizerState
     from .runtime import build_timeline
 
+    if _BENCH_BROKEN:
+        raise RuntimeError(f"skipped: an earlier peer leg failed ({_BENCH_BROKEN[0]})")
     runners = {}
-    for strategy in ("async_raw", "optimizer_prediction"):
-        stage = make_stage()
-        opt = OptimizerState(OptimizerConfig(opt_kind, **(opt_kw or {})), stage.param_names, device=device)
-        r = PeerStageRunner(dist, build_timeline(strategy, world, n_batches), stage, opt, strategy, data, loss_kind,
-                            lambda mb: lr, rows)
-        r.run()
-        r.capture()
-        r.replay()
-        r.report()
-        runners[strategy] = r
+    try:
+        for strategy in ("async_raw", "optimizer_prediction"):
+            stage = make_stage()
+            opt = OptimizerState(OptimizerConfig(opt_kind, **(opt_kw or {})), stage.param_names, device=device)
+            r = PeerStageRunner(dist, build_timeline(strategy, world, n_batches), stage, opt, strategy, data,
+                                loss_kind, lambda mb: lr, rows, timeout_ms=timeout_ms)
+            r.run()
+            r.capture()
+            r.replay()
+            r.report()
+            runners[strategy] = r
+    except Exception as exc:
+        _BENCH_BROKEN.append(f"{type(exc).__name__}: {exc}")
+        raise
     times = {s: [] for s in runners}
     for _ in range(trials):
         for s, r in runners.items():
