@@ -441,6 +441,8 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         progress("config 1 tf32")
         out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
         progress("projected 8-GPU")
+        out["depth_sweep_1gpu"] = bp.depth_sweep(torch, device, n_batches=args.pipeline_batches)
+        progress("depth sweep")
         if not args.no_cpu:
             try:
                 out["cpu_baseline"] = cpu_pipeline_baseline()

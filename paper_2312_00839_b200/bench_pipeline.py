@@ -76,12 +76,13 @@ def _time_replays(torch, device, g, replays):
     return e0.elapsed_time(e1) / 1e3 / replays
 
 
-def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=9, streams=("stage", "serial")):
+def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=9, streams=("stage", "serial"),
+                  dims=CONFIG1_DIMS, acts=CONFIG1_ACTS):
     """Prediction off/on graphs (per stream mode) timed in alternation (median
     of `trials`), so clock and thermal drift hit every arm alike."""
     import statistics
 
-    graphs = {(s, m): _graph_for(torch, device, s, depth, n_batches, data, streams=m)
+    graphs = {(s, m): _graph_for(torch, device, s, depth, n_batches, data, streams=m, dims=dims, acts=acts)
               for m in streams for s in ("async_raw", "optimizer_prediction")}
     times = {k: [] for k in graphs}
     for _ in range(trials):
@@ -251,6 +252,30 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
             1.0 - out["pred_on"]["eager_samples_per_s"] / out["pred_off"]["eager_samples_per_s"], 4)
     out["launches"] = launches
     torch.backends.cuda.matmul.allow_tf32 = False
+    return out
+
+
+def depth_sweep(torch, device, depths=(1, 2, 4, 8), n_batches: int = 64, replays: int = 5, trials: int = 5):
+    """Config 1 at D = 1, 2, 4, 8 pipeline stages on the one GPU (the
+    stage-concurrent graphed runner; prediction off/on in alternation). D <= 4
+    partitions config 1's four layers; D = 8 widens it to eight layers (one
+    more 1024-wide ReLU layer per extra stage, as bench.py --gpus 8 does)."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    out = {}
+    for d in depths:
+        dims = CONFIG1_DIMS if d <= 4 else [3072] + [1024] * (d - 1) + [10]
+        acts = CONFIG1_ACTS if d <= 4 else ["relu"] * (d - 1) + ["linear"]
+        data = DeviceBatches(torch, device, dims=dims)
+        pair = _graphed_pair(torch, device, d, n_batches, data, replays, trials=trials, streams=("stage",),
+                             dims=dims, acts=acts)
+        row = {"dims": dims}
+        for strategy, key in (("async_raw", "pred_off"), ("optimizer_prediction", "pred_on")):
+            _, sec, _, _ = pair[(strategy, "stage")]
+            row[key] = round(n_batches * BATCH / sec, 1)
+        row["prediction_overhead"] = round(1.0 - row["pred_on"] / row["pred_off"], 4)
+        out[f"D{d}"] = row
+        del pair
+        torch.cuda.empty_cache()
     return out
 
 

@@ -18,3 +18,6 @@ else:
     for c, v in p.get("configs", {}).items():
         print(c, v.get("pred_off", {}).get("samples_per_s"), v.get("pred_on", {}).get("samples_per_s"),
               v.get("prediction_overhead"), v.get("multi_gpu_roofline_prediction_overhead"), v.get("error"))
+    if "depth_sweep_1gpu" in p:
+        print("depth sweep (1 GPU)", {k: (v["pred_off"], v["pred_on"], v["prediction_overhead"])
+                                       for k, v in p["depth_sweep_1gpu"].items()})
