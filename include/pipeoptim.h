@@ -174,6 +174,16 @@ int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads
                        int64_t step_count, int64_t* nonfinite_index, const int64_t* flags, int64_t epoch,
                        int64_t timeout_ms, int32_t* status, void* stream);
 
+/* CUDA-graph forms of the two (whole runs captured once, replayed): the
+ * epoch is a device counter advanced by po_dp_signal_dev and read by the
+ * wait of po_step_predict_dp_dc, and the step's scalars come from a device
+ * po_coef (po_coef_fill, PO_COEF_STEP_PREDICT) refreshed before each replay. */
+int po_dp_signal_dev(long long* const* peer_flag_slots, int32_t dp, int64_t* epoch_ctr, void* stream);
+int po_step_predict_dp_dc(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp, float* state1,
+                          float* state2, float* w_hat, int64_t n, const po_coef* coef_dev, int64_t* nonfinite_index,
+                          const int64_t* flags, const int64_t* epoch_ctr, int64_t timeout_ms, int32_t* status,
+                          void* stream);
+
 /* ---- fused per-event stage ops (pipeoptim_stage_ops.cu) ---------------- */
 
 #define PO_LOSS_MSE 0

@@ -38,6 +38,8 @@ EXPORTS = (
     "po_act_bwd_bias",
     "po_dp_signal",
     "po_step_predict_dp",
+    "po_dp_signal_dev",
+    "po_step_predict_dp_dc",
     "po_p2p_send",
     "po_p2p_recv",
     "po_ipc_alloc",
@@ -118,6 +120,9 @@ _SIGNATURES = {
     "po_act_bwd_bias": (ctypes.c_int, [ctypes.c_int32, _P, ctypes.c_int32, _P, _I64, _I64, _P, _P, ctypes.c_int32,
                                        _P]),
     "po_dp_signal": (ctypes.c_int, [_P, ctypes.c_int32, _I64, _P]),
+    "po_dp_signal_dev": (ctypes.c_int, [_P, ctypes.c_int32, _P, _P]),
+    "po_step_predict_dp_dc": (ctypes.c_int, [_HP, _P, _P, ctypes.c_int32, _P, _P, _P, _I64, _P, _P, _P, _P, _I64,
+                                             _P, _P]),
     "po_step_predict_dp": (ctypes.c_int, [_HP, _P, _P, ctypes.c_int32, _P, _P, _P, _I64, _D, _D, _I64, _P, _P, _I64,
                                           _I64, _P, _P]),
     "po_p2p_send": (ctypes.c_int, [_P, _I64, _P, _I64, ctypes.c_int32, _P, _P, _P, _I64, _P, _P]),

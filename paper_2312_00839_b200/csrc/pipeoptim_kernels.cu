@@ -562,8 +562,9 @@ __device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
 // (a full-grid spin could starve them and close a dependency cycle across
 // replicas).
 __global__ void po_dp_wait_kernel(const long long* flags, int dp, long long epoch, long long timeout_cycles,
-                                  int* status) {
+                                  int* status, const long long* epoch_dev) {
   if (threadIdx.x != 0) return;
+  if (epoch_dev != nullptr) epoch = *(volatile const long long*)epoch_dev;  // graph replays: device counter
   const long long t0 = clock64();
   for (int r = 0; r < dp; ++r) {
     while (ld_acquire_sys(flags + r) < epoch) {
@@ -626,8 +627,12 @@ __global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
   if (a.bad != nullptr && bad != INT64_MAX) atomicMin(a.bad, (unsigned long long)bad);
 }
 
-__global__ void po_dp_signal_kernel(long long* const* slots, int dp, long long epoch) {
+__global__ void po_dp_signal_kernel(long long* const* slots, int dp, long long epoch, long long* epoch_ctr) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (epoch_ctr != nullptr) {  // device-side epoch: advanced here, read by the wait kernel
+      epoch = *(volatile long long*)epoch_ctr + 1;
+      *epoch_ctr = epoch;
+    }
     __threadfence_system();
     for (int r = 0; r < dp; ++r)
       asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(slots[r]), "l"(epoch) : "memory");
@@ -780,15 +785,48 @@ int po_step_predict_dc(const po_hparams* hp, float* w, const float* g, float* st
 
 int po_dp_signal(long long* const* peer_flag_slots, int32_t dp, int64_t epoch, void* stream) {
   if (peer_flag_slots == nullptr || dp < 1 || dp > kMaxDp) return PO_EINVAL;
-  po_dp_signal_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(peer_flag_slots, dp, (long long)epoch);
+  po_dp_signal_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(peer_flag_slots, dp, (long long)epoch, nullptr);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }
+
+int po_dp_signal_dev(long long* const* peer_flag_slots, int32_t dp, int64_t* epoch_ctr, void* stream) {
+  if (peer_flag_slots == nullptr || dp < 1 || dp > kMaxDp || epoch_ctr == nullptr) return PO_EINVAL;
+  po_dp_signal_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(peer_flag_slots, dp, 0,
+                                                          reinterpret_cast<long long*>(epoch_ctr));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+static int step_predict_dp_impl(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp,
+                                float* state1, float* state2, float* w_hat, int64_t n, double lr,
+                                double lr_pred_times_s, int64_t step_count, const po_coef* coef_dev,
+                                int64_t* nonfinite_index, const int64_t* flags, int64_t epoch,
+                                const int64_t* epoch_dev, int64_t timeout_ms, int32_t* status, void* stream);
 
 int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp, float* state1,
                        float* state2, float* w_hat, int64_t n, double lr, double lr_pred_times_s,
                        int64_t step_count, int64_t* nonfinite_index, const int64_t* flags, int64_t epoch,
                        int64_t timeout_ms, int32_t* status, void* stream) {
+  if (step_count < 0) return PO_EINVAL;
+  return step_predict_dp_impl(hp, w, grads_host, dp, state1, state2, w_hat, n, lr, lr_pred_times_s, step_count,
+                              nullptr, nonfinite_index, flags, epoch, nullptr, timeout_ms, status, stream);
+}
+
+int po_step_predict_dp_dc(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp, float* state1,
+                          float* state2, float* w_hat, int64_t n, const po_coef* coef_dev, int64_t* nonfinite_index,
+                          const int64_t* flags, const int64_t* epoch_ctr, int64_t timeout_ms, int32_t* status,
+                          void* stream) {
+  if (coef_dev == nullptr || epoch_ctr == nullptr) return PO_EINVAL;
+  return step_predict_dp_impl(hp, w, grads_host, dp, state1, state2, w_hat, n, 0.0, 0.0, 0, coef_dev,
+                              nonfinite_index, flags, 0, epoch_ctr, timeout_ms, status, stream);
+}
+
+static int step_predict_dp_impl(const po_hparams* hp, float* w, const float* const* grads_host, int32_t dp,
+                                float* state1, float* state2, float* w_hat, int64_t n, double lr,
+                                double lr_pred_times_s, int64_t step_count, const po_coef* coef_dev,
+                                int64_t* nonfinite_index, const int64_t* flags, int64_t epoch,
+                                const int64_t* epoch_dev, int64_t timeout_ms, int32_t* status, void* stream) {
   if (!valid_hp(hp) || step_count < 0 || dp < 1 || dp > kMaxDp || grads_host == nullptr || flags == nullptr ||
       status == nullptr || n < 0)
     return PO_EINVAL;
@@ -797,7 +835,7 @@ int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads
   DpArgs d;
   memset(&d, 0, sizeof(d));
   d.a = Args{w, nullptr, state1, hp->kind == PO_SGDM ? nullptr : state2, w_hat, n,
-             reinterpret_cast<unsigned long long*>(nonfinite_index), nullptr,
+             reinterpret_cast<unsigned long long*>(nonfinite_index), coef_dev,
              coef(hp, lr, lr_pred_times_s, step_count + 1)};
   for (int r = 0; r < dp; ++r) {
     if (n > 0 && grads_host[r] == nullptr) return PO_EINVAL;
@@ -826,7 +864,8 @@ int po_step_predict_dp(const po_hparams* hp, float* w, const float* const* grads
   if (want < 1) want = 1;
   int64_t cap = (int64_t)sm_count() * 8;
   const int64_t grid = want < cap ? want : cap;
-  po_dp_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d.flags, dp, d.epoch, d.timeout_cycles, status);
+  po_dp_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d.flags, dp, d.epoch, d.timeout_cycles, status,
+                                                        reinterpret_cast<const long long*>(epoch_dev));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   switch (hp->kind) {

@@ -66,6 +66,9 @@ class FusedDPGroup:
         self.epoch = 0
         self.parity = 0
         self._lib = _lib.load()
+        # CUDA-graph form (step_predict_dev): the epoch lives on the device
+        self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._slot = None
         dist.barrier(group=group)
 
     @property
@@ -91,6 +94,41 @@ class FusedDPGroup:
             self.epoch, self.timeout_ms, self.status.data_ptr(), stream,
         )
         _lib.check(rc, "po_step_predict_dp")
+        opt.step_count += 1
+        self.parity ^= 1
+
+    def step_predict_dev(self, opt, flat, lr, lr_pred, steps_ahead: int, out: torch.Tensor) -> None:
+        """step_predict for CUDA-graph capture and replay: the epoch is a device
+        counter (po_dp_signal_dev / po_step_predict_dp_dc) and the step's
+        scalars come from the optimizer's CoefTape while capturing (else from
+        a device po_coef filled here). The grad-buffer parity alternates per
+        call as in step_predict, so a captured run must hold an even number
+        of updates to replay consistently."""
+        if steps_ahead < 0:
+            raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
+        if flat.layout.numel != self.numel:
+            raise ValueError("stage size does not match the DP group's buffers")
+        opt._bind(flat.layout)
+        opt._ensure_state()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(self._lib.po_dp_signal_dev(self.slots.data_ptr(), self.dp_size, self.epoch_ctr.data_ptr(), stream),
+                   "po_dp_signal_dev")
+        if opt.tape is not None:
+            coef = opt.tape.record(opt, _lib.PO_COEF_STEP_PREDICT, lr, lr_pred, steps_ahead)
+        else:
+            if self._slot is None:
+                from .pipeline import _SlotTape
+
+                self._slot = _SlotTape(self.device)
+            self._slot.fill(opt, _lib.PO_COEF_STEP_PREDICT, lr, float(lr_pred) * steps_ahead)
+            coef = self._slot.dev.data_ptr()
+        rc = self._lib.po_step_predict_dp_dc(
+            ctypes.byref(opt._hp), flat.data.data_ptr(), self.grad_ptrs[self.parity], self.dp_size,
+            opt._s1.data_ptr(), None if opt._s2 is None else opt._s2.data_ptr(), out.data_ptr(), self.numel, coef,
+            opt._bad.data_ptr(), self.flags.data_ptr(), self.epoch_ctr.data_ptr(), self.timeout_ms,
+            self.status.data_ptr(), stream,
+        )
+        _lib.check(rc, "po_step_predict_dp_dc")
         opt.step_count += 1
         self.parity ^= 1
 

@@ -244,7 +244,13 @@ class PeerStageRunner:
     before each replay). Data must be device-resident; checks are deferred."""
 
     def __init__(self, dist, tl: Timeline, stage, opt, strategy: str, data, loss_kind: str, lr_for_mb, rows: int,
-                 *, fuse: bool = True, group=None, stage_ranks: list[int] | None = None, timeout_ms: int = 60_000):
+                 *, fuse: bool = True, group=None, stage_ranks: list[int] | None = None, timeout_ms: int = 60_000,
+                 dp_rank: int = 0, dp_size: int = 1, fused_dp=None):
+        """Hybrid DP x PP: stage_ranks[k] is the global rank of stage k in this
+        replica; replica `dp_rank` of `dp_size` trains on rows [dp_rank*rows,
+        (dp_rank+1)*rows) of every batch, and `fused_dp` (a
+        dp_fused.FusedDPGroup over the stage's replicas) folds the gradient
+        mean into the update (device epochs, so the run stays one graph)."""
         if STRATEGY_SCHEDULE.get(strategy) != "1f1b" or tl.kind != "1f1b":
             raise ValueError(f"the peer runner executes 1f1b strategies, got {strategy!r} on {tl.kind!r}")
         if strategy == "spectrain" and opt.config.kind != "sgdm":
@@ -263,6 +269,12 @@ class PeerStageRunner:
         self.graph = None
         self.runs = 0
         self._pending = None
+        if (dp_size > 1) != (fused_dp is not None):
+            raise ValueError("data parallelism (dp_size > 1) needs a fused_dp group, and only then")
+        self.dp_rank, self.dp_size, self.fused_dp = dp_rank, dp_size, fused_dp
+        self._scratch = None
+        if fused_dp is not None:
+            stage.set_grad_buffer(fused_dp.grad)
 
     def _issue(self, lr_fn):
         """Enqueue one full run of this rank's program on the current stream."""
@@ -283,16 +295,28 @@ class PeerStageRunner:
                 debug(f"rank {self.rank} before {op.kind}{op.mb}")
             if op.kind == UPDATE:
                 lr = lr_fn(op.mb)
-                if self.fuse and op.fuse_predict:
+                fuse = self.fuse and op.fuse_predict
+                if self.fused_dp is not None:  # replicas' gradient mean inside K3
+                    if fuse:
+                        out, lr_p, gap = rt.staging_buffer(), lr_fn(op.next_mb), op.next_gap
+                    else:  # a plain step: the prediction output goes to scratch
+                        if self._scratch is None:
+                            self._scratch = st.flat.layout.empty(self.device)
+                        out, lr_p, gap = self._scratch, 0.0, 0
+                    self.fused_dp.step_predict_dev(self.opt, st.flat, lr, lr_p, gap, out)
+                    st.set_grad_buffer(self.fused_dp.grad)
+                elif fuse:
                     self.opt.step_predict_(st.flat, lr, lr_fn(op.next_mb), op.next_gap, rt.staging_buffer())
-                    rt.prepared = (op.next_mb, op.next_gap)
                 else:
                     self.opt.step_(st.flat, lr)
+                if fuse:
+                    rt.prepared = (op.next_mb, op.next_gap)
                 st.version += 1
                 rt.pending_count = 0
                 policy.after_update(rt)
             elif op.kind == FORWARD:
-                x = links.recv_act() if self.rank > 0 else _to_device(self.data.batch(op.mb)[0], self.device)
+                x = links.recv_act() if self.rank > 0 else self._shard(_to_device(self.data.batch(op.mb)[0],
+                                                                                    self.device))
                 weights, fv, predicted, target = policy.forward_view(rt, op.mb, 0, lr_fn(op.mb))
                 out = st.run_forward(weights, (op.mb, 0), x, fv, check_finite=False, finite_flags=flags,
                                      flag_index=wi)
@@ -300,7 +324,8 @@ class PeerStageRunner:
                 records[op.mb] = rec
                 order.append(rec)
                 if last:
-                    loss, grad = loss_and_grad(out, _to_device(self.data.batch(op.mb)[1], self.device), self.loss_kind)
+                    y = self._shard(_to_device(self.data.batch(op.mb)[1], self.device))
+                    loss, grad = loss_and_grad(out, y, self.loss_kind)
                     losses[op.mb - 1] = loss
                     local_grads[op.mb] = grad
                 else:
@@ -320,6 +345,11 @@ class PeerStageRunner:
             snapshot_peak = max(snapshot_peak, policy.snapshot_count(rt))
         return order, flags, losses, snapshot_peak, work
 
+    def _shard(self, t):
+        if self.dp_size == 1:
+            return t
+        return t[self.dp_rank * self.rows : (self.dp_rank + 1) * self.rows]
+
     def run(self) -> StageReport:
         """One eager run (asynchronous device work, one sync at the end)."""
         t0 = time.perf_counter()
@@ -332,6 +362,8 @@ class PeerStageRunner:
         it warms cuBLAS/cuDNN and the optimizer state)."""
         if self.runs == 0:
             raise RuntimeError("run() once before capture()")
+        if self.fused_dp is not None and self.tl.n_batches % 2:
+            raise ValueError("a captured DP run must hold an even number of updates (grad-buffer parity)")
         self.opt._ensure_state()
         torch.cuda.synchronize(self.device)
         self.tape = CoefTape(self.device)
@@ -360,6 +392,8 @@ class PeerStageRunner:
         transfer timeout or a non-finite forward output / loss / update)."""
         order, flags, losses, snapshot_peak, work = self._pending
         self.links.check()
+        if self.fused_dp is not None:
+            self.fused_dp.check()
         if not bool(flags.all()):
             bad = int((~flags).nonzero()[0].item())
             raise NumericError(f"mb {work[bad].mb} stage {self.rank}: non-finite value in stage forward output")

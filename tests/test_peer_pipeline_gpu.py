@@ -215,3 +215,93 @@ def test_peer_runner_module_stages(tmp_path):
     for k, st in enumerate(stages):
         w = torch.load(tmp_path / f"w{k}.pt")
         assert float((w - st.flat.data.cpu()).abs().max()) <= 1e-5 * float(st.flat.data.abs().max())
+
+
+HDIMS = [16, 24, 24, 24, 10]
+HACTS = ["tanh", "tanh", "tanh", "linear"]
+
+
+class HSrc:
+    """Device-resident reference-seeded batches of 8 rows (DP shards them)."""
+
+    def __init__(self, dev):
+        import torch
+
+        self.b = {}
+        for mb in range(1, 64):
+            s = rng_ref.Stream(9, f"batch-{mb}")
+            x, y = s.normal(8, HDIMS[0]), s.normal(8, HDIMS[-1])
+            self.b[mb] = (torch.tensor(np.asarray(getattr(x, "a", x)), dtype=torch.float32, device=dev),
+                          torch.tensor(np.asarray(getattr(y, "a", y)), dtype=torch.float32, device=dev))
+
+    def batch(self, mb):
+        return self.b[mb]
+
+
+def _hybrid_worker(rank, world, port, dp, pp, n, kind, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.dp_fused import FusedDPGroup
+        from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+        from paper_2312_00839_b200.peer_pipeline import PeerStageRunner
+        from paper_2312_00839_b200.pipeline import gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+        from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+        torch.backends.cuda.matmul.allow_tf32 = False
+        dev = torch.device("cuda", 0)
+        r, k = divmod(rank, pp)
+        groups = [dist.new_group([q * pp + s for q in range(dp)]) for s in range(pp)]
+        kw = {"weight_decay": 0.0} if kind == "sgdm" else {}
+        data = HSrc(dev)
+        out = {}
+        for mode in ("graph", "eager"):
+            stage = StageModel(k, partition_layers(build_layers(HDIMS, HACTS), pp)[k],
+                               lambda sp: rng_ref.layer_init(4, sp.index, sp.in_dim, sp.out_dim), dev)
+            opt = OptimizerState(OptimizerConfig(kind, **kw), stage.param_names, device=dev)
+            fused = FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, dev, timeout_ms=120_000)
+            runner = PeerStageRunner(dist, build_timeline("optimizer_prediction", pp, n), stage, opt,
+                                     "optimizer_prediction", data, "mse", lambda mb: 0.01, 8 // dp,
+                                     stage_ranks=[r * pp + s for s in range(pp)], dp_rank=r, dp_size=dp,
+                                     fused_dp=fused, timeout_ms=120_000)
+            reps = [runner.run()]
+            if mode == "graph":
+                runner.capture()
+                for _ in range(2):
+                    runner.replay()
+                    reps.append(runner.report())
+            else:
+                for _ in range(2):
+                    reps.append(runner.run())
+            first = gather_reports(dist, reps[0], world)
+            out[mode] = {"first_losses": np.mean([rp.losses for rp in first if rp.rank == pp - 1], axis=0).tolist(),
+                         "params": {n_: p.detach().double().cpu().numpy().tolist()
+                                    for n_, p in zip(stage.param_names, stage.params)}}
+        Path(out_dir, f"h{rank}.json").write_text(json.dumps(out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["adam", "sgdm"])
+def test_peer_runner_hybrid_dp_graph(tmp_path, kind):
+    """DP 2 x PP 2 (4 processes on one GPU) through the peer runner with the
+    DP mean fused into K3 on device epochs: the first run equals the
+    full-batch 2-stage oracle pipeline, replicas stay bit-identical, and an
+    eager run + capture + 2 replays equals 3 eager runs bit for bit."""
+    import torch.multiprocessing as mp
+
+    dp, pp, n = 2, 2, 8
+    mp.spawn(_hybrid_worker, args=(dp * pp, _port(), dp, pp, n, kind, str(tmp_path)), nprocs=dp * pp, join=True)
+    res = [json.loads((tmp_path / f"h{i}.json").read_text()) for i in range(dp * pp)]
+    ref = runtime_ref.run(HDIMS, HACTS, pp, n, "optimizer_prediction", optim_ref.Hyper(kind, weight_decay=0.0),
+                          lambda mb: tuple(t.cpu().numpy() for t in HSrc("cpu").batch(mb)), "mse", lambda mb: 0.01,
+                          lambda i, a, b: rng_ref.layer_init(4, i, a, b))
+    assert np.allclose(res[0]["eager"]["first_losses"], ref["losses"], rtol=1e-4, atol=1e-6)
+    for k in range(pp):
+        a, b = res[k], res[pp + k]  # replicas 0 and 1 of stage k
+        assert a["graph"]["params"] == b["graph"]["params"]
+        assert a["graph"]["params"] == a["eager"]["params"]
