@@ -736,4 +736,37 @@ def bench_hybrid_dp_pp(torch_mod, dist, rank, world, device, n_batches: int = 32
         t = torch_mod.tensor([times[-1]], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         out[arm] = {"samples_per_s": round(n_batches * BATCH / float(t.item()), 1), "s": round(float(t.item()), 4)}
+    # the same hybrid on the peer runner: neighbour rings + the fused DP mean on
+    # device epochs, a rank's whole run as one CUDA graph
+    try:
+        from .peer_pipeline import PeerStageRunner
+
+        stage = StageModel(k, partition_layers(layers, pp)[k], torch_init(0, device), device)
+        opt = OptimizerState(OptimizerConfig("adam"), stage.param_names, device=device)
+        fused = FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, device, timeout_ms=15_000)
+        runner = PeerStageRunner(dist, build_timeline("optimizer_prediction", pp, n_batches), stage, opt,
+                                 "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-4, BATCH // dp,
+                                 stage_ranks=[r * pp + s for s in range(pp)], dp_rank=r, dp_size=dp, fused_dp=fused,
+                                 timeout_ms=15_000)
+        runner.run()
+        runner.capture()
+        runner.replay()
+        runner.report()
+        torch_mod.cuda.synchronize(device)
+        dist.barrier()
+        e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            runner.replay()
+        e1.record()
+        torch_mod.cuda.synchronize(device)
+        runner.report()
+        t = torch_mod.tensor([e0.elapsed_time(e1) / 1e3 / 3], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["peer_graphed_fused_mean"] = {"samples_per_s": round(n_batches * BATCH / float(t.item()), 1),
+                                          "s": round(float(t.item()), 4)}
+        dist.barrier()
+        runner.links.close()
+    except Exception as exc:
+        out["peer_graphed_fused_mean"] = {"error": f"rank {rank}: {type(exc).__name__}: {exc}"}
     return out
