@@ -437,7 +437,12 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
         torch.cuda.empty_cache()
     if with_roofline:
         def make():
+            # one stage per GPU: its work is alone on the device, so cuDNN's
+            # (grid-synchronising, faster) batch norm is safe there
+            from .stage_models import use_cudnn_bn
+
             st, _ = module_stages_for(torch, name, device, amp=amp)
+            use_cudnn_bn(st)
             kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
             return st, [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in st]
 

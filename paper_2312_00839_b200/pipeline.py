@@ -664,10 +664,15 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
         from .peer_pipeline import bench_peer_pipeline
 
         def make_stage():
+            from .stage_models import use_cudnn_bn
+
             stages, _ = module_stages_for(torch_mod, name, device, depth=world, costs=costs)
             for k, st in enumerate(stages):
                 if k != rank:
                     st.module.to("cpu")
+            # the peer runner keeps all of a rank's work on one stream (its waits
+            # included): cuDNN's grid-synchronising batch norm is safe there
+            use_cudnn_bn([stages[rank]])
             return stages[rank]
 
         kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}

@@ -16,13 +16,18 @@ ap.add_argument("--config", default="config3_resnet101")
 ap.add_argument("--stage", type=int, default=4)
 ap.add_argument("--amp", default=None)
 ap.add_argument("--top", type=int, default=25)
+ap.add_argument("--cudnn-bn", action="store_true", help="put cuDNN batch norm back (single-stream use only)")
 a = ap.parse_args()
 torch.backends.cudnn.allow_tf32 = torch.backends.cuda.matmul.allow_tf32 = True
 dev = torch.device("cuda", 0)
 cfg = bp.MODULE_CONFIGS[a.config]
 stages, _ = bp.module_stages_for(torch, a.config, dev, amp=a.amp)
 st = stages[a.stage]
-opt = OptimizerState(OptimizerConfig(cfg["opt"]), st.param_names, device=dev)
+if a.cudnn_bn:
+    from paper_2312_00839_b200.stage_models import use_cudnn_bn
+
+    use_cudnn_bn([st])
+opt = OptimizerState(OptimizerConfig(cfg["opt"]), st.param_names, device=dev, eager_checks=False)
 data = bp.ModuleBatches(torch, dev, cfg)
 x = data.batch(1)[0] if a.stage == 0 else torch.randn((cfg["batch"], *st.in_shape), device=dev)
 g = torch.randn((cfg["batch"], *st.out_shape), device=dev)
@@ -37,6 +42,20 @@ def unit():
 for _ in range(3):
     unit()
 torch.cuda.synchronize()
+from paper_2312_00839_b200.runtime import capture  # noqa: E402
+
+graph = torch.cuda.CUDAGraph()
+with capture(graph):
+    unit()
+graph.replay()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    graph.replay()
+e1.record()
+torch.cuda.synchronize()
+print(f"graphed unit: {e0.elapsed_time(e1) / 5:.3f} ms")
 with profile(activities=[ProfilerActivity.CUDA]) as p:
     for _ in range(3):
         unit()
