@@ -228,6 +228,21 @@ int po_relu_bwd_bias(const float* g, int32_t splits, const float* h, int64_t row
 int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols,
                     float* dpre, float* db, int32_t accumulate, void* stream);
 
+/* ---- FP32-accurate tensor-core GEMM (pipeoptim_gemm.cu) -----------------
+ * D[l] = A[l] @ B[l] for l < batch, fp32 in/out, computed by tcgen05 UMMA with
+ * each fp32 operand split into three bf16 pieces (CUTLASS SM100 fast-FP32
+ * mainloop): fp32-level accuracy at tensor-core throughput, for the fp32
+ * stage GEMMs (stages.py:175-208). A: M x K, row-major (a_col_major = 0:
+ * element (m,k) at m*lda + k) or column-major (1: at m + k*lda), batch stride
+ * sa; B: K x N, row-major (b_col_major = 0: (k,n) at k*ldb + n) or
+ * column-major (1: at k + n*ldb), batch stride sb; not both column-major.
+ * D: M x N row-major contiguous, batch stride M*N. lda, ldb, n, sa, sb
+ * multiples of 4 (16-byte TMA alignment). workspace may be NULL when the
+ * kernel needs none (the default schedule). */
+int po_gemm_f32x3(int32_t a_col_major, int32_t b_col_major, const float* a, int64_t lda, int64_t sa, const float* b,
+                  int64_t ldb, int64_t sb, float* d, int64_t m, int64_t n, int64_t k, int64_t batch, void* workspace,
+                  int64_t workspace_bytes, void* stream);
+
 /* ---- peer-memory boundary transport (pipeoptim_p2p.cu) ------------------
  * Replaces the simulated hand-off dicts of the reference executor
  * (runtime.py:390-391, 420-433): one direction of a pipeline boundary is a

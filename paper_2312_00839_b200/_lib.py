@@ -40,6 +40,7 @@ EXPORTS = (
     "po_step_predict_dp",
     "po_dp_signal_dev",
     "po_step_predict_dp_dc",
+    "po_gemm_f32x3",
     "po_p2p_send",
     "po_p2p_recv",
     "po_ipc_alloc",
@@ -125,6 +126,8 @@ _SIGNATURES = {
                                              _P, _P]),
     "po_step_predict_dp": (ctypes.c_int, [_HP, _P, _P, ctypes.c_int32, _P, _P, _P, _I64, _D, _D, _I64, _P, _P, _I64,
                                           _I64, _P, _P]),
+    "po_gemm_f32x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
+                                     _I64, _I64, _P, _I64, _P]),
     "po_p2p_send": (ctypes.c_int, [_P, _I64, _P, _I64, ctypes.c_int32, _P, _P, _P, _I64, _P, _P]),
     "po_p2p_recv": (ctypes.c_int, [_P, _I64, ctypes.c_int32, _P, _I64, _P, _P, _P, _I64, _P, _P]),
     "po_ipc_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p]),

@@ -21,6 +21,19 @@ LIB_NAME = "libpipeoptim.so"
 LIB_PATH = PKG_DIR / LIB_NAME
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _cutlass_include() -> list[str]:
+    """CUTLASS/CuTe header trees vendored in the environment (used by
+    csrc/pipeoptim_gemm.cu inside our own kernels)."""
+    import site
+
+    roots = [Path(p) for p in site.getsitepackages()]
+    for root in roots:
+        base = root / "flashinfer" / "data" / "cutlass"
+        if (base / "include" / "cutlass" / "cutlass.h").exists():
+            return [f"-I{base / 'include'}", f"-I{base / 'tools' / 'util' / 'include'}"]
+    raise RuntimeError("CUTLASS headers not found (flashinfer/data/cutlass)")
 NVCC_FLAGS = [
     "-O3",
     "-std=c++17",
@@ -56,7 +69,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale(LIB_PATH, deps):
         return LIB_PATH
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, f"-I{INCLUDE}", "-o", str(tmp), *map(str, srcs)]
+    cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, "--expt-relaxed-constexpr", "-diag-suppress", "20012",
+           f"-I{INCLUDE}", *_cutlass_include(), "-o", str(tmp), *map(str, srcs), "-lcuda"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

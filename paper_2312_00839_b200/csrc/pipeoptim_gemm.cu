@@ -1,0 +1,131 @@
+// pipeoptim_gemm.cu — FP32-accurate stage GEMMs on the tcgen05 tensor cores.
+//
+// The config-1 stage GEMMs are fp32 (the parity contract keeps TF32 off), so
+// cuBLAS runs them on the CUDA cores (SIMT SGEMM, 74 TFLOP/s peak, 13-35
+// TFLOP/s achieved at these shapes). This TU instantiates CUTLASS's SM100
+// "fast FP32" mainloop: each fp32 operand is split into three bf16 pieces in
+// shared memory and the products are accumulated in fp32 in TMEM by
+// tcgen05.mma (UMMA) — fp32-level accuracy at tensor-core throughput. It is
+// used as a batched GEMM so the caller can run the small-M, long-K stage
+// shapes split-K (batch = K slice) and reduce the partials in its own fused
+// epilogue (po_splitk_bias_act / po_act_bwd_bias).
+//
+//   D[l] (M x N, row-major) = A[l] (M x K) @ B[l] (K x N)
+//   A: row-major with leading dimension lda (K-major), batch stride sa
+//   B: row-major K x N with leading dimension ldb (N-major), batch stride sb
+//   D: row-major, leading dimension N, batch stride M*N
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cute/tensor.hpp"
+#include "cutlass/cutlass.h"
+#include "cutlass/epilogue/collective/collective_builder.hpp"
+#include "cutlass/gemm/collective/collective_builder.hpp"
+#include "cutlass/gemm/device/gemm_universal_adapter.h"
+#include "cutlass/gemm/kernel/gemm_universal.hpp"
+#include "cutlass/util/packed_stride.hpp"
+#include "pipeoptim.h"
+
+namespace {
+
+using namespace cute;
+
+using ElementAcc = float;
+using LayoutD = cutlass::layout::RowMajor;
+constexpr int kAlign = 4;  // 16-byte TMA alignment in floats
+
+using MmaTileShape = Shape<_128, _64, _32>;
+using ClusterShape = Shape<_1, _1, _1>;
+
+// The epilogue is layout-independent; one mainloop per operand-major pair.
+// (Written out per variant, not as a class template: nvcc's host stubs lose
+// the dependent `typename` of a templated CollectiveBuilder chain.)
+using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
+    cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, ElementAcc, void, LayoutD, kAlign, float, LayoutD,
+    kAlign, cutlass::epilogue::collective::EpilogueScheduleAuto>::CollectiveOp;
+constexpr int kEpiCarveout = static_cast<int>(sizeof(typename CollectiveEpilogue::SharedStorage));
+
+#define PO_FAST_F32_GEMM(NAME, LAYOUT_A, LAYOUT_B)                                                                 \
+  namespace NAME {                                                                                                 \
+  using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<                                         \
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, LAYOUT_A, kAlign, float, LAYOUT_B, kAlign,      \
+      ElementAcc, MmaTileShape, ClusterShape, cutlass::gemm::collective::StageCountAutoCarveout<kEpiCarveout>,      \
+      cutlass::gemm::KernelTmaWarpSpecialized1SmFastFP32SmemSm100>::CollectiveOp;                                  \
+  using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, CollectiveEpilogue,    \
+                                                      void>;                                                       \
+  struct G {                                                                                                       \
+    using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;                                              \
+  };                                                                                                               \
+  }
+
+PO_FAST_F32_GEMM(row_row, cutlass::layout::RowMajor, cutlass::layout::RowMajor)     // x @ W
+PO_FAST_F32_GEMM(col_row, cutlass::layout::ColumnMajor, cutlass::layout::RowMajor)  // x^T @ dpre
+PO_FAST_F32_GEMM(row_col, cutlass::layout::RowMajor, cutlass::layout::ColumnMajor)  // dpre @ W^T
+#undef PO_FAST_F32_GEMM
+
+template <class G>
+int run_gemm(typename G::Gemm::GemmKernel::StrideA sa_, typename G::Gemm::GemmKernel::StrideB sb_, const float* a,
+             const float* b, float* d, int64_t m, int64_t n, int64_t k, int64_t batch, void* workspace,
+             int64_t workspace_bytes, cudaStream_t stream) {
+  using Gemm = typename G::Gemm;
+  typename Gemm::GemmKernel::StrideD stride_d =
+      cute::make_stride(static_cast<int64_t>(n), cute::Int<1>{}, static_cast<int64_t>(m * n));
+  cutlass::KernelHardwareInfo hw;
+  hw.device_id = 0;
+  cudaGetDevice(&hw.device_id);
+  static int sms = 0;
+  if (sms == 0) sms = cutlass::KernelHardwareInfo::query_device_multiprocessor_count(hw.device_id);
+  hw.sm_count = sms;
+  typename Gemm::Arguments args{cutlass::gemm::GemmUniversalMode::kGemm,
+                                {static_cast<int>(m), static_cast<int>(n), static_cast<int>(k),
+                                 static_cast<int>(batch)},
+                                {a, sa_, b, sb_},
+                                {{1.0f, 0.0f}, nullptr, stride_d, d, stride_d},
+                                hw};
+  Gemm gemm;
+  if (gemm.can_implement(args) != cutlass::Status::kSuccess) return PO_EINVAL;
+  const size_t need = Gemm::get_workspace_size(args);
+  if (need > 0 && (workspace == nullptr || static_cast<size_t>(workspace_bytes) < need)) return PO_EINVAL;
+  if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return PO_EINVAL;
+  if (gemm.run(stream) != cutlass::Status::kSuccess) {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PO_EINVAL : (int)e;
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+using RowRow = row_row::G;
+using ColRow = col_row::G;
+using RowCol = row_col::G;
+
+}  // namespace
+
+extern "C" {
+
+int po_gemm_f32x3(int32_t a_col_major, int32_t b_col_major, const float* a, int64_t lda, int64_t sa, const float* b,
+                  int64_t ldb, int64_t sb, float* d, int64_t m, int64_t n, int64_t k, int64_t batch, void* workspace,
+                  int64_t workspace_bytes, void* stream) {
+  if (m < 1 || n < 1 || k < 1 || batch < 1 || a == nullptr || b == nullptr || d == nullptr) return PO_EINVAL;
+  if (lda % kAlign || ldb % kAlign || n % kAlign || sa % kAlign || sb % kAlign) return PO_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!a_col_major && !b_col_major) {  // A (m,k) at m*lda + k; B (k,n) at k*ldb + n
+    if (lda < k || ldb < n) return PO_EINVAL;
+    return run_gemm<RowRow>(cute::make_stride(lda, cute::Int<1>{}, sa), cute::make_stride(cute::Int<1>{}, ldb, sb),
+                            a, b, d, m, n, k, batch, workspace, workspace_bytes, s);
+  }
+  if (a_col_major && !b_col_major) {  // A (m,k) at m + k*lda
+    if (lda < m || ldb < n) return PO_EINVAL;
+    return run_gemm<ColRow>(cute::make_stride(cute::Int<1>{}, lda, sa), cute::make_stride(cute::Int<1>{}, ldb, sb),
+                            a, b, d, m, n, k, batch, workspace, workspace_bytes, s);
+  }
+  if (!a_col_major && b_col_major) {  // B (k,n) at k + n*ldb
+    if (lda < k || ldb < k) return PO_EINVAL;
+    return run_gemm<RowCol>(cute::make_stride(lda, cute::Int<1>{}, sa), cute::make_stride(ldb, cute::Int<1>{}, sb),
+                            a, b, d, m, n, k, batch, workspace, workspace_bytes, s);
+  }
+  return PO_EINVAL;
+}
+
+}  // extern "C"

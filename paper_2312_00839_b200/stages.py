@@ -232,6 +232,40 @@ def _splitk(rows: int, k: int, n: int) -> int:
     return s
 
 
+# fp32 stage GEMMs on the tensor cores (csrc/pipeoptim_gemm.cu: tcgen05 UMMA,
+# each fp32 operand split into three bf16 pieces — fp32-level accuracy) when
+# TF32 is off; set False to use cuBLAS's SIMT SGEMM instead.
+TC_FP32 = True
+
+
+def _tc_ok(*tensors) -> bool:
+    return (TC_FP32 and not torch.backends.cuda.matmul.allow_tf32
+            and all(t.is_cuda and t.dtype == torch.float32 and t.data_ptr() % 16 == 0 for t in tensors))
+
+
+def _splitk_tc(rows: int, k: int) -> int:
+    """K slices for the tensor-core GEMM of a small-M long-K shape: <= 8
+    slices of >= 128 (scripts/gemm_f32x3_check.py: 3072x1024 forward 14 us at
+    8 slices vs 19 us for the best SIMT split)."""
+    if rows > 512 or k < 256:
+        return 1
+    s = 1
+    while s < 8 and k % (s * 2) == 0 and k // (s * 2) >= 128:
+        s *= 2
+    return s
+
+
+def _gemm_tc(a, a_col: bool, lda: int, sa: int, b, b_col: bool, ldb: int, sb: int, m: int, n: int, k: int,
+             batch: int, out: torch.Tensor) -> torch.Tensor:
+    from . import _lib
+
+    rc = _lib.load().po_gemm_f32x3(int(a_col), int(b_col), a.data_ptr(), lda, sa, b.data_ptr(), ldb, sb,
+                                   out.data_ptr(), m, n, k, batch, None, 0,
+                                   torch.cuda.current_stream(out.device).cuda_stream)
+    _lib.check(rc, "po_gemm_f32x3")
+    return out
+
+
 def _splitk_reduce(part: torch.Tensor, bias, act: str, pre_out=None, flags=None, flag_index: int = 0):
     """act(sum_s part[s] + bias) in one launch (po_splitk_bias_act); with
     `flags`, flags[flag_index] is cleared if any output is non-finite."""
@@ -255,10 +289,15 @@ def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str, flags=N
     epilogue)."""
     rows, k = h.shape
     n = w.shape[1]
-    s = _splitk(rows, k, n)
-    if s > 1:
-        h = h if h.is_contiguous() else h.contiguous()
+    h = h if h.is_contiguous() else h.contiguous()
+    tc = n % 4 == 0 and k % 4 == 0 and _tc_ok(h, w)
+    s = _splitk_tc(rows, k) if tc else _splitk(rows, k, n)
+    if tc:  # tensor-core fp32 GEMM, batch = K slice, into the fused epilogue
+        part = _gemm_tc(h, False, k, k // s, w, False, n, (k // s) * n, rows, n, k // s, s,
+                        torch.empty((s, rows, n), dtype=torch.float32, device=h.device))
+    elif s > 1:
         part = torch.bmm(h.view(rows, s, k // s).transpose(0, 1), w.view(s, k // s, n))
+    if tc or s > 1:
         bias = b.view(-1)
         if act == "tanh":
             pre = torch.empty((rows, n), dtype=torch.float32, device=h.device)
@@ -278,11 +317,29 @@ def _input_grad_parts(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     split-K over the layer's output width (splits = 1: the product itself)."""
     rows, n = dpre.shape
     k = w.shape[0]
+    dpre = dpre if dpre.is_contiguous() else dpre.contiguous()
+    if n % 4 == 0 and k % 4 == 0 and _tc_ok(dpre, w):  # W^T read K-major straight from the flat buffer
+        s = _splitk_tc(rows, n)
+        return _gemm_tc(dpre, False, n, n // s, w, True, n, n // s, rows, k, n // s, s,
+                        torch.empty((s, rows, k), dtype=torch.float32, device=dpre.device))
     s = _splitk(rows, n, k)
     if s > 1:
-        dpre = dpre if dpre.is_contiguous() else dpre.contiguous()
         return torch.bmm(dpre.view(rows, s, n // s).transpose(0, 1), w.view(k, s, n // s).permute(1, 2, 0))
     return torch.mm(dpre, w.t()).unsqueeze(0)
+
+
+def _weight_grad(x: torch.Tensor, dpre: torch.Tensor, gw: torch.Tensor, accumulate: bool) -> None:
+    """gw (=|+=) x^T @ dpre: the tensor-core fp32 GEMM reads x^T M-major
+    straight from the stashed activation and writes the flat-gradient view."""
+    rows, k_in = x.shape
+    n = dpre.shape[1]
+    if (not accumulate and n % 4 == 0 and k_in % 4 == 0 and gw.is_contiguous() and x.is_contiguous()
+            and dpre.is_contiguous() and _tc_ok(x, dpre, gw)):
+        _gemm_tc(x, True, k_in, 0, dpre, False, n, 0, k_in, n, rows, 1, gw)
+    elif accumulate:
+        gw.addmm_(x.t(), dpre)
+    else:
+        torch.mm(x.t(), dpre, out=gw)
 
 
 def _input_grad(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
@@ -307,6 +364,16 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
     h = x
     fused = x.is_cuda
     checked = False
+    if fused and stage.rank == 0 and _tc_ok(x):
+        # the tensor-core fp32 GEMM saturates a non-finite INPUT (its bf16 split
+        # clamps +-inf) instead of propagating it to the output the reference
+        # checks (stages.py:182); the data entering stage 0 is therefore checked
+        # itself (later stages' inputs are earlier stages' checked outputs)
+        if check_finite:
+            if not bool(torch.isfinite(x).all()):
+                raise NumericError(f"non-finite value in stage {stage.rank} forward output (non-finite input)")
+        elif finite_flags is not None:
+            record_finite(x, finite_flags, flag_index)
     last = len(stage.layers) - 1
     for i, spec in enumerate(stage.layers):
         w, b = weights[2 * i], weights[2 * i + 1]
@@ -379,10 +446,7 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
             rc = lib.po_act_bwd_bias(int(relu), g.data_ptr(), splits, entry.pre_acts[i].data_ptr() if relu else None,
                                      rows, cols, dpre.data_ptr(), gb.data_ptr(), int(accumulate), stream)
             _lib.check(rc, "po_act_bwd_bias")
-            if accumulate:
-                gw.addmm_(x.t(), dpre)
-            else:
-                torch.mm(x.t(), dpre, out=gw)
+            _weight_grad(x, dpre, gw, accumulate)
         else:
             gfull = g[0] if g.shape[0] == 1 else _splitk_reduce(g, None, "linear")
             dpre = _activation_grad_mul(gfull, entry.pre_acts[i], spec.activation)
