@@ -440,6 +440,17 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         out["tf32"] = {k: t[k] for k in ("pred_on", "pred_off", "prediction_overhead", "serial_streams", "config")}
         progress("config 1 tf32")
         out["projected_8gpu"] = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
+        from paper_2312_00839_b200 import stages as _stages
+
+        _stages.TC_FP32 = False  # the same projection with cuBLAS's SIMT fp32 GEMMs, for reference
+        try:
+            simt = bp.projected_multi_gpu(torch, device, depth=8, n_batches=args.pipeline_batches)
+        finally:
+            _stages.TC_FP32 = True
+        out["projected_8gpu"]["simt_fp32_gemms"] = {
+            "prediction_overhead": simt["prediction_overhead"],
+            "pred_off_samples_per_s": simt["pred_off"]["multi_gpu_samples_per_s"],
+            "pred_on_samples_per_s": simt["pred_on"]["multi_gpu_samples_per_s"]}
         progress("projected 8-GPU")
         out["depth_sweep_1gpu"] = bp.depth_sweep(torch, device, n_batches=args.pipeline_batches)
         progress("depth sweep")

@@ -13,7 +13,9 @@ else:
           "serial", p["serial_streams"]["pred_off"]["samples_per_s"], p["serial_streams"]["pred_on"]["samples_per_s"],
           p["serial_streams"]["prediction_overhead"])
     print("tf32", p["tf32"]["pred_off"]["samples_per_s"], p["tf32"]["pred_on"]["samples_per_s"], p["tf32"]["prediction_overhead"])
-    print("proj8", p["projected_8gpu"]["prediction_overhead"], "multi-gpu roof ovh", p.get("multi_gpu_roofline_prediction_overhead"))
+    print("proj8", p["projected_8gpu"]["prediction_overhead"], p["projected_8gpu"]["pred_off"]["multi_gpu_samples_per_s"],
+          p["projected_8gpu"]["pred_on"]["multi_gpu_samples_per_s"], "simt", p["projected_8gpu"].get("simt_fp32_gemms"),
+          "multi-gpu roof ovh", p.get("multi_gpu_roofline_prediction_overhead"))
     print("cpu pipeline", p.get("cpu_baseline", {}).get("value"))
     for c, v in p.get("configs", {}).items():
         print(c, v.get("pred_off", {}).get("samples_per_s"), v.get("pred_on", {}).get("samples_per_s"),
