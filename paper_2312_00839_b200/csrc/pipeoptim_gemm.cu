@@ -34,7 +34,16 @@ using ElementAcc = float;
 using LayoutD = cutlass::layout::RowMajor;
 constexpr int kAlign = 4;  // 16-byte TMA alignment in floats
 
-using MmaTileShape = Shape<_128, _64, _32>;
+#ifndef PO_FASTF32_TILE_N
+#define PO_FASTF32_TILE_N 64
+#endif
+#ifndef PO_FASTF32_TILE_K
+#define PO_FASTF32_TILE_K 32
+#endif
+#ifndef PO_FASTF32_KMAJOR_A_SCHEDULE  // K-major A: bf16 pieces staged in shared memory (Smem) or TMEM
+#define PO_FASTF32_KMAJOR_A_SCHEDULE KernelTmaWarpSpecialized1SmFastFP32SmemSm100
+#endif
+using MmaTileShape = Shape<_128, Int<PO_FASTF32_TILE_N>, Int<PO_FASTF32_TILE_K>>;
 using ClusterShape = Shape<_1, _1, _1>;
 
 // The epilogue is layout-independent; one mainloop per operand-major pair.
@@ -46,12 +55,12 @@ using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBui
     kAlign, cutlass::epilogue::collective::EpilogueScheduleAuto>::CollectiveOp;
 constexpr int kEpiCarveout = static_cast<int>(sizeof(typename CollectiveEpilogue::SharedStorage));
 
-#define PO_FAST_F32_GEMM(NAME, LAYOUT_A, LAYOUT_B)                                                                 \
+#define PO_FAST_F32_GEMM(NAME, LAYOUT_A, LAYOUT_B, SCHEDULE)                                                       \
   namespace NAME {                                                                                                 \
   using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<                                         \
       cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, LAYOUT_A, kAlign, float, LAYOUT_B, kAlign,      \
       ElementAcc, MmaTileShape, ClusterShape, cutlass::gemm::collective::StageCountAutoCarveout<kEpiCarveout>,      \
-      cutlass::gemm::KernelTmaWarpSpecialized1SmFastFP32SmemSm100>::CollectiveOp;                                  \
+      cutlass::gemm::SCHEDULE>::CollectiveOp;                                                                      \
   using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, CollectiveEpilogue,    \
                                                       void>;                                                       \
   struct G {                                                                                                       \
@@ -59,9 +68,11 @@ constexpr int kEpiCarveout = static_cast<int>(sizeof(typename CollectiveEpilogue
   };                                                                                                               \
   }
 
-PO_FAST_F32_GEMM(row_row, cutlass::layout::RowMajor, cutlass::layout::RowMajor)     // x @ W
-PO_FAST_F32_GEMM(col_row, cutlass::layout::ColumnMajor, cutlass::layout::RowMajor)  // x^T @ dpre
-PO_FAST_F32_GEMM(row_col, cutlass::layout::RowMajor, cutlass::layout::ColumnMajor)  // dpre @ W^T
+PO_FAST_F32_GEMM(row_row, cutlass::layout::RowMajor, cutlass::layout::RowMajor, PO_FASTF32_KMAJOR_A_SCHEDULE)  // x@W
+PO_FAST_F32_GEMM(col_row, cutlass::layout::ColumnMajor, cutlass::layout::RowMajor,
+                 KernelTmaWarpSpecialized1SmFastFP32SmemSm100)  // x^T @ dpre (M-major A: shared-memory staging)
+PO_FAST_F32_GEMM(row_col, cutlass::layout::RowMajor, cutlass::layout::ColumnMajor,
+                 PO_FASTF32_KMAJOR_A_SCHEDULE)  // dpre @ W^T
 #undef PO_FAST_F32_GEMM
 
 template <class G>
