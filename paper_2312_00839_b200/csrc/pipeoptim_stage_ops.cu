@@ -133,13 +133,13 @@ __global__ void loss_grad_kernel(const float* __restrict__ pred, const float* __
 }
 
 // One CTA per 8 columns: thread t handles column t % 8 and rows t / 8,
-// t / 8 + 32, ... (a warp reads 4 rows x 32 contiguous bytes per load), keeps
-// its column partial in a register, then the 32 row-lanes' partials of each
+// t / 8 + 64, ... (a warp reads 4 rows x 32 contiguous bytes per load), keeps
+// its column partial in a register, then the 64 row-lanes' partials of each
 // column are summed in row-lane order through shared memory: a fixed
 // reduction order, so the bias gradient is deterministic. 8-column CTAs put
-// 128 CTAs on a 1024-wide layer (one CTA per 32 columns left 32 SMs busy and
-// took 12.5 us for 128 x 1024).
-constexpr int kReluCols = 8, kReluLanes = 32;
+// 128 CTAs on a 1024-wide layer; the up-to-8 split-K partials of an element
+// are loaded together (independent loads in flight), then summed in order.
+constexpr int kReluCols = 8, kReluLanes = 64;
 
 // g: `splits` partial products [splits x rows x cols], summed in order 0..S-1.
 // g and dpre may alias when splits == 1 (each element is read, then written,
@@ -152,21 +152,28 @@ __global__ void relu_bwd_bias_kernel(const float* g, int splits, const float* __
   const int64_t c = (int64_t)blockIdx.x * kReluCols + cl;
   float acc = 0.f;
   if (c < cols) {
-#pragma unroll 4
     for (int64_t r = lane; r < rows; r += kReluLanes) {
       const int64_t i = r * cols + c;
-      float gi = g[i];
-      for (int s = 1; s < splits; ++s) gi += g[(int64_t)s * n + i];
-      const float v = (!mask || h[i] > 0.f) ? gi : 0.f;  // g * (pre > 0): relu(pre) > 0 <=> pre > 0
-      dpre[i] = v;
-      acc += v;
+      float v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < splits) v[s] = g[(int64_t)s * n + i];
+      const bool keep = !mask || h[i] > 0.f;  // g * (pre > 0): relu(pre) > 0 <=> pre > 0
+      float gi = v[0];
+#pragma unroll
+      for (int s = 1; s < 8; ++s)
+        if (s < splits) gi += v[s];
+      for (int s = 8; s < splits; ++s) gi += g[(int64_t)s * n + i];
+      const float o = keep ? gi : 0.f;
+      dpre[i] = o;
+      acc += o;
     }
   }
   part[lane][cl] = acc;
   __syncthreads();
   if (lane == 0 && c < cols) {
     float s = 0.f;
-#pragma unroll
+#pragma unroll 8
     for (int k = 0; k < kReluLanes; ++k) s += part[k][cl];
     db[c] = accumulate ? db[c] + s : s;
   }
