@@ -130,7 +130,7 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
     return graph
 
 
-def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 20, trials: int = 5):
+def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 40, trials: int = 9):
     """Per-stage device time of one mini-batch's work — SURVEY.md §8d's
     t_f,k + t_b,k (+ t_u,k) — with prediction off (K2 update) and on (K3),
     each captured in a CUDA graph on THROWAWAY stages from `make()` ->

@@ -348,6 +348,18 @@ def _input_grad(dpre: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     return part[0] if part.shape[0] == 1 else _splitk_reduce(part, None, "linear")
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(device) -> "torch.cuda.Stream":
+    """One auxiliary stream per device per CURRENT stream (cached), for work
+    that only reads a tensor the main stream also reads."""
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
+
+
 def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int,
                   check_finite: bool = True, finite_flags: torch.Tensor | None = None,
                   flag_index: int = 0) -> torch.Tensor:
@@ -364,6 +376,7 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
     h = x
     fused = x.is_cuda
     checked = False
+    side_check = None
     if fused and stage.rank == 0 and _tc_ok(x):
         # the tensor-core fp32 GEMM saturates a non-finite INPUT (its bf16 split
         # clamps +-inf) instead of propagating it to the output the reference
@@ -373,7 +386,14 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
             if not bool(torch.isfinite(x).all()):
                 raise NumericError(f"non-finite value in stage {stage.rank} forward output (non-finite input)")
         elif finite_flags is not None:
-            record_finite(x, finite_flags, flag_index)
+            # off the critical path: the check only reads x, so it runs on a
+            # side stream beside the forward GEMMs and joins at the end
+            side_check = _side_stream(x.device)
+            fork = torch.cuda.Event()
+            fork.record()
+            side_check.wait_event(fork)
+            with torch.cuda.stream(side_check):
+                record_finite(x, finite_flags, flag_index)
     last = len(stage.layers) - 1
     for i, spec in enumerate(stage.layers):
         w, b = weights[2 * i], weights[2 * i + 1]
@@ -397,6 +417,8 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
             )
     elif finite_flags is not None and not checked:
         record_finite(h, finite_flags, flag_index)
+    if side_check is not None:
+        torch.cuda.current_stream(x.device).wait_stream(side_check)
     stage.stash.put(key, StashEntry(version, inputs, pres))
     return h
 
