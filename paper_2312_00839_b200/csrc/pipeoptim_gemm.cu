@@ -17,6 +17,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// The kernels are launched with programmatic dependent launch (PDL); with this
+// set, CUTLASS's producer waits on the preceding grid (griddepcontrol.wait)
+// before its first operand load — without it the wait compiles to nothing.
+#define CUTLASS_ENABLE_GDC_FOR_SM100 1
+
 #include "cute/tensor.hpp"
 #include "cutlass/cutlass.h"
 #include "cutlass/epilogue/collective/collective_builder.hpp"
@@ -99,7 +104,10 @@ int run_gemm(typename G::Gemm::GemmKernel::StrideA sa_, typename G::Gemm::GemmKe
   const size_t need = Gemm::get_workspace_size(args);
   if (need > 0 && (workspace == nullptr || static_cast<size_t>(workspace_bytes) < need)) return PO_EINVAL;
   if (gemm.initialize(args, workspace, stream) != cutlass::Status::kSuccess) return PO_EINVAL;
-  if (gemm.run(stream) != cutlass::Status::kSuccess) {
+  // programmatic dependent launch: the GEMM's CTAs are scheduled while the
+  // preceding kernel drains and wait (griddepcontrol.wait) before touching
+  // its operands, hiding the launch gap on the stage's critical path
+  if (gemm.run(stream, nullptr, /*launch_with_pdl=*/true) != cutlass::Status::kSuccess) {
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PO_EINVAL : (int)e;
   }
