@@ -450,7 +450,7 @@ DefaultShape default_shape(int kind, int mode, int64_t n) {
     case MODE_STEP: return sg ? DefaultShape{512, 1, 1, 1} : DefaultShape{512, 1, 2, 0};
     case MODE_STEP_PREDICT:
       if (sg) return DefaultShape{384, 1, 1, 1};
-      return kind == PO_ADAM ? DefaultShape{512, 1, 1, 1} : DefaultShape{256, 8, 2, 0};
+      return DefaultShape{512, 1, 1, 1};  // Adam and AdamW (2^30 re-tune: AdamW 6,549 GB/s vs 6,270 before)
     default: return DefaultShape{256, 4, 2, 1};
   }
 }
