@@ -478,9 +478,11 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         for name in bp.MODULE_CONFIGS:
             try:
                 if world == 1:
-                    configs[name] = bp.single_gpu_module_pipeline(torch, device, name, n_batches=16)
+                    # n >= 8 D mini-batches per measured run, fill and drain included
+                    n_mb = 8 * bp.MODULE_CONFIGS[name]["depth"]
+                    configs[name] = bp.single_gpu_module_pipeline(torch, device, name, n_batches=n_mb)
                     if bp.MODULE_CONFIGS[name].get("channels_last"):  # conv configs: bf16 stage compute too
-                        b = bp.single_gpu_module_pipeline(torch, device, name, n_batches=16, amp="bf16",
+                        b = bp.single_gpu_module_pipeline(torch, device, name, n_batches=n_mb, amp="bf16",
                                                           with_eager=False, with_roofline=False)
                         configs[name]["bf16"] = {k: b[k] for k in ("config", "pred_off", "pred_on",
                                                                    "prediction_overhead")}
