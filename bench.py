@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--no-pipeline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--pipeline-batches", type=int, default=64)
-    ap.add_argument("--pipeline-timeout", type=float, default=420.0)
+    ap.add_argument("--pipeline-timeout", type=float, default=None,
+                    help="watchdog on the pipeline leg (default 420 s on 1 GPU, 900 s with more ranks)")
     ap.add_argument("--no-configs", action="store_true", help="skip configs 2-4 in the pipeline leg")
     # test-only: exercise the multi-rank bench on ONE GPU (ranks share the
     # device, gloo transport with host staging); never used for numbers
@@ -531,6 +532,9 @@ def ours(args):
             os._exit(0)
 
         import faulthandler
+
+        if args.pipeline_timeout is None:
+            args.pipeline_timeout = 420.0 if world == 1 else 900.0
 
         faulthandler.dump_traceback_later(max(1.0, args.pipeline_timeout - 2.0), exit=False)  # where it hung
         dog = threading.Timer(args.pipeline_timeout, _expire)
