@@ -506,3 +506,46 @@ def test_empty_and_tiny_buffers(lib):
                                    2e-3, 2, None, None, stream()) == 0
         ew, _, _, ewh = F.step("sgdm", w, g, s1, s2, 1e-3, 2, c_pred=2e-3)
         assert np.array_equal(f32(dw), ew) and np.array_equal(f32(out), ewh)
+
+
+@pytest.mark.parametrize("variant", ["row_row", "col_row", "row_col"])
+@pytest.mark.parametrize("m,n,k,batch", [(128, 1024, 384, 8), (7, 20, 36, 1), (300, 64, 129, 3)])
+def test_fast_fp32_gemm_matches_float64(variant, m, n, k, batch):
+    """po_gemm_f32x3 (tcgen05, 3x bf16 split, fp32 accumulation) vs float64 on
+    every operand-major variant, batched: fp32-level accuracy (<= 2e-6
+    relative to the largest output, the SIMT SGEMM's level)."""
+    import torch
+
+    from paper_2312_00839_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(m * n + k)
+    a_col, b_col = {"row_row": (0, 0), "col_row": (1, 0), "row_col": (0, 1)}[variant]
+    # A stored (k x m) when column-major, B stored (n x k) when column-major
+    a = torch.randn(batch, *((k, m) if a_col else (m, k)), device="cuda", generator=g)
+    b = torch.randn(batch, *((n, k) if b_col else (k, n)), device="cuda", generator=g) / k ** 0.5
+    lda = m if a_col else k
+    ldb = k if b_col else n
+    if lda % 4 or ldb % 4 or n % 4:
+        pytest.skip("operand strides must be 16-byte aligned")
+    d = torch.empty(batch, m, n, device="cuda")
+    rc = _lib.load().po_gemm_f32x3(a_col, b_col, a.data_ptr(), lda, a[0].numel(), b.data_ptr(), ldb, b[0].numel(),
+                                   d.data_ptr(), m, n, k, batch, None, 0, torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    A = a.double().transpose(1, 2) if a_col else a.double()
+    B = b.double().transpose(1, 2) if b_col else b.double()
+    want = A @ B
+    assert float((d.double() - want).abs().max()) <= 2e-6 * float(want.abs().max())
+
+
+def test_fast_fp32_gemm_rejects_bad_arguments():
+    import torch
+
+    from paper_2312_00839_b200 import _lib
+
+    lib = _lib.load()
+    x = torch.zeros(64, 64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    p = x.data_ptr()
+    assert lib.po_gemm_f32x3(1, 1, p, 64, 0, p, 64, 0, p, 8, 8, 8, 1, None, 0, s) == _lib.PO_EINVAL  # both col-major
+    assert lib.po_gemm_f32x3(0, 0, p, 62, 0, p, 64, 0, p, 8, 8, 8, 1, None, 0, s) == _lib.PO_EINVAL  # lda % 4
+    assert lib.po_gemm_f32x3(0, 0, p, 64, 0, p, 64, 0, p, 0, 8, 8, 1, None, 0, s) == _lib.PO_EINVAL  # m = 0
