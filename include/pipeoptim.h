@@ -243,6 +243,13 @@ int po_gemm_f32x3(int32_t a_col_major, int32_t b_col_major, const float* a, int6
                   int64_t ldb, int64_t sb, float* d, int64_t m, int64_t n, int64_t k, int64_t batch, void* workspace,
                   int64_t workspace_bytes, void* stream);
 
+/* 1 if po_gemm_f32x3 was compiled (CUTLASS headers found at build time), 0 if
+ * the library was built without CUTLASS: po_gemm_f32x3 then returns
+ * PO_ENOSYS and the stage math uses cuBLAS. The optimizer kernels never
+ * depend on CUTLASS. */
+#define PO_ENOSYS (-38)
+int po_gemm_f32x3_available(void);
+
 /* ---- peer-memory boundary transport (pipeoptim_p2p.cu) ------------------
  * Replaces the simulated hand-off dicts of the reference executor
  * (runtime.py:390-391, 420-433): one direction of a pipeline boundary is a

@@ -14,6 +14,7 @@ from pathlib import Path
 from .build import LIB_PATH
 
 PO_EINVAL = -22
+PO_ENOSYS = -38
 PO_SGDM, PO_ADAM, PO_ADAMW = 0, 1, 2
 KIND_CODES = {"sgdm": PO_SGDM, "adam": PO_ADAM, "adamw": PO_ADAMW}
 
@@ -41,6 +42,7 @@ EXPORTS = (
     "po_dp_signal_dev",
     "po_step_predict_dp_dc",
     "po_gemm_f32x3",
+    "po_gemm_f32x3_available",
     "po_p2p_send",
     "po_p2p_recv",
     "po_ipc_alloc",
@@ -128,6 +130,7 @@ _SIGNATURES = {
                                           _I64, _P, _P]),
     "po_gemm_f32x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
                                      _I64, _I64, _P, _I64, _P]),
+    "po_gemm_f32x3_available": (ctypes.c_int, []),
     "po_p2p_send": (ctypes.c_int, [_P, _I64, _P, _I64, ctypes.c_int32, _P, _P, _P, _I64, _P, _P]),
     "po_p2p_recv": (ctypes.c_int, [_P, _I64, ctypes.c_int32, _P, _I64, _P, _P, _P, _I64, _P, _P]),
     "po_ipc_alloc": (ctypes.c_int, [_I64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p]),

@@ -123,6 +123,8 @@ using RowCol = row_col::G;
 
 extern "C" {
 
+int po_gemm_f32x3_available(void) { return 1; }
+
 int po_gemm_f32x3(int32_t a_col_major, int32_t b_col_major, const float* a, int64_t lda, int64_t sa, const float* b,
                   int64_t ldb, int64_t sb, float* d, int64_t m, int64_t n, int64_t k, int64_t batch, void* workspace,
                   int64_t workspace_bytes, void* stream) {

@@ -304,12 +304,12 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
         elem<KIND, MODE>(c, w[u].v[j], g[u].v[j], s1[u].v[j], s2[u].v[j], out[u].v[j], e);
         if (e && bad == INT64_MAX) bad = base + j;
       }
-      if constexpr (writes_w(MODE)) vstore<VEC, CACHE>(a.w + base, w[u]);
+      if constexpr (writes_w(MODE)) vstore<VEC, pol(CACHE, S_W)>(a.w + base, w[u]);
       if constexpr (writes_state(MODE)) {
-        vstore<VEC, CACHE>(a.s1 + base, s1[u]);
-        if constexpr (KIND != PO_SGDM) vstore<VEC, CACHE>(a.s2 + base, s2[u]);
+        vstore<VEC, pol(CACHE, S_STATE)>(a.s1 + base, s1[u]);
+        if constexpr (KIND != PO_SGDM) vstore<VEC, pol(CACHE, S_STATE)>(a.s2 + base, s2[u]);
       }
-      if constexpr (writes_out(MODE)) vstore<VEC, CACHE>(a.out + base, out[u]);
+      if constexpr (writes_out(MODE)) vstore<VEC, pol(CACHE, S_OUT)>(a.out + base, out[u]);
     }
   }
   for (; i < nv; i += stride) do_vec<KIND, MODE, VEC, CACHE>(a, c, i, bad);
@@ -579,7 +579,10 @@ __global__ void po_dp_wait_kernel(const long long* flags, int dp, long long epoc
   }
 }
 
-template <int KIND, int VEC>
+// DP is a template parameter so every replica's gradient load of an element
+// is issued before the first add (dp independent NVLink/HBM loads in flight
+// per vector, plus W and the state), then summed in rank order.
+template <int KIND, int VEC, int DP>
 __global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
   if (*(volatile int*)d.status != 0) return;  // a replica never signalled: update nothing
   const Args& a = d.a;
@@ -590,22 +593,21 @@ __global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
   int64_t bad = INT64_MAX;
   for (int64_t i = tid; i < nv; i += stride) {
     const int64_t base = i * VEC;
-    Vec<VEC> g = vload<VEC, 1, true>(d.grads[0] + base);
+    Vec<VEC> gr[DP];
+#pragma unroll
+    for (int r = 0; r < DP; ++r) gr[r] = vload<VEC, 1, true>(d.grads[r] + base);
     Vec<VEC> w = vload<VEC, 1, false>(a.w + base);
     Vec<VEC> s1 = vload<VEC, 1, false>(a.s1 + base);
     Vec<VEC> s2{};
     if constexpr (KIND != PO_SGDM) s2 = vload<VEC, 1, false>(a.s2 + base);
-#pragma unroll 1
-    for (int r = 1; r < d.dp; ++r) {
-      const Vec<VEC> gr = vload<VEC, 1, true>(d.grads[r] + base);
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) g.v[j] = __fadd_rn(g.v[j], gr.v[j]);
-    }
     Vec<VEC> out;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
+      float g = gr[0].v[j];
+#pragma unroll
+      for (int r = 1; r < DP; ++r) g = __fadd_rn(g, gr[r].v[j]);  // rank order
       bool e = false;
-      elem<KIND, MODE_STEP_PREDICT>(c, w.v[j], __fmul_rn(g.v[j], d.inv_dp), s1.v[j], s2.v[j], out.v[j], e);
+      elem<KIND, MODE_STEP_PREDICT>(c, w.v[j], DP == 1 ? g : __fmul_rn(g, d.inv_dp), s1.v[j], s2.v[j], out.v[j], e);
       if (e && bad == INT64_MAX) bad = base + j;
     }
     vstore<VEC, 1>(a.w + base, w);
@@ -616,10 +618,11 @@ __global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
   const int64_t t = nv * VEC + tid;  // scalar tail
   if (t < a.n) {
     float g = d.grads[0][t];
-    for (int r = 1; r < d.dp; ++r) g = __fadd_rn(g, d.grads[r][t]);
+#pragma unroll
+    for (int r = 1; r < DP; ++r) g = __fadd_rn(g, d.grads[r][t]);
     float w = a.w[t], s1 = a.s1[t], s2 = (KIND != PO_SGDM) ? a.s2[t] : 0.f, out = 0.f;
     bool e = false;
-    elem<KIND, MODE_STEP_PREDICT>(c, w, __fmul_rn(g, d.inv_dp), s1, s2, out, e);
+    elem<KIND, MODE_STEP_PREDICT>(c, w, DP == 1 ? g : __fmul_rn(g, d.inv_dp), s1, s2, out, e);
     if (e && bad == INT64_MAX) bad = t;
     a.w[t] = w;
     a.s1[t] = s1;
@@ -641,15 +644,26 @@ __global__ void po_dp_signal_kernel(long long* const* slots, int dp, long long e
   }
 }
 
+template <int KIND, int VEC>
+cudaError_t launch_dp_vec(const DpArgs& d, dim3 grid, dim3 block, cudaStream_t s) {
+  switch (d.dp) {
+    case 1: po_dp_kernel<KIND, VEC, 1><<<grid, block, 0, s>>>(d); break;
+    case 2: po_dp_kernel<KIND, VEC, 2><<<grid, block, 0, s>>>(d); break;
+    case 3: po_dp_kernel<KIND, VEC, 3><<<grid, block, 0, s>>>(d); break;
+    case 4: po_dp_kernel<KIND, VEC, 4><<<grid, block, 0, s>>>(d); break;
+    case 5: po_dp_kernel<KIND, VEC, 5><<<grid, block, 0, s>>>(d); break;
+    case 6: po_dp_kernel<KIND, VEC, 6><<<grid, block, 0, s>>>(d); break;
+    case 7: po_dp_kernel<KIND, VEC, 7><<<grid, block, 0, s>>>(d); break;
+    default: po_dp_kernel<KIND, VEC, 8><<<grid, block, 0, s>>>(d); break;
+  }
+  return cudaGetLastError();
+}
+
 template <int KIND>
 cudaError_t launch_dp(const DpArgs& d, int vec, dim3 grid, dim3 block, cudaStream_t s) {
-  if (vec == 8)
-    po_dp_kernel<KIND, 8><<<grid, block, 0, s>>>(d);
-  else if (vec == 4)
-    po_dp_kernel<KIND, 4><<<grid, block, 0, s>>>(d);
-  else
-    po_dp_kernel<KIND, 1><<<grid, block, 0, s>>>(d);
-  return cudaGetLastError();
+  if (vec == 8) return launch_dp_vec<KIND, 8>(d, grid, block, s);
+  if (vec == 4) return launch_dp_vec<KIND, 4>(d, grid, block, s);
+  return launch_dp_vec<KIND, 1>(d, grid, block, s);
 }
 
 }  // namespace
@@ -860,11 +874,14 @@ static int step_predict_dp_impl(const po_hparams* hp, float* w, const float* con
     return true;
   };
   while (vec > 1 && !all_aligned(vec * 4)) vec = vec == 8 ? 4 : 1;
-  const int block = 256;
+  // K3's launch shape for this size (block x CTAs/SM); one vector per stream
+  // in flight, dp of them for the gradient
+  const DefaultShape ds = default_shape(hp->kind, MODE_STEP_PREDICT, n);
+  const int block = ds.block;
   const int64_t nv = n / vec;
   int64_t want = (nv + block - 1) / block;
   if (want < 1) want = 1;
-  int64_t cap = (int64_t)sm_count() * 8;
+  int64_t cap = (int64_t)sm_count() * ds.ctas_per_sm;
   const int64_t grid = want < cap ? want : cap;
   po_dp_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d.flags, dp, d.epoch, d.timeout_cycles, status,
                                                         reinterpret_cast<const long long*>(epoch_dev));

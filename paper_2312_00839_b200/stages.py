@@ -238,9 +238,23 @@ def _splitk(rows: int, k: int, n: int) -> int:
 TC_FP32 = True
 
 
+_TC_BUILT: bool | None = None
+
+
+def _tc_built() -> bool:
+    """po_gemm_f32x3 was compiled (the library found CUTLASS at build time)."""
+    global _TC_BUILT
+    if _TC_BUILT is None:
+        from . import _lib
+
+        _TC_BUILT = bool(_lib.load().po_gemm_f32x3_available())
+    return _TC_BUILT
+
+
 def _tc_ok(*tensors) -> bool:
     return (TC_FP32 and not torch.backends.cuda.matmul.allow_tf32
-            and all(t.is_cuda and t.dtype == torch.float32 and t.data_ptr() % 16 == 0 for t in tensors))
+            and all(t.is_cuda and t.dtype == torch.float32 and t.data_ptr() % 16 == 0 for t in tensors)
+            and _tc_built())
 
 
 def _splitk_tc(rows: int, k: int) -> int:
