@@ -487,6 +487,9 @@ def pipeline_leg(args, torch, dist, rank, world, device):
                                                           with_eager=False, with_roofline=False)
                         configs[name]["bf16"] = {k: b[k] for k in ("config", "pred_off", "pred_on",
                                                                    "prediction_overhead")}
+                        configs[name]["bf16"]["semantics"] = (
+                            "throughput only: autocast's bf16 weight copies make conv input gradients use the "
+                            "forward (predicted) weights, not the live ones (S9); no parity claim")
                 else:
                     configs[name] = bench_module_pipeline(torch, dist, rank, world, device, name, n_batches=16,
                                                           host_staging=args.dist_backend != "nccl")

@@ -45,6 +45,7 @@ class FusedDPGroup:
         self.bufs = [self._ipc[0].tensor, self._ipc[1].tensor]
         self.flags = self._ipc[2].tensor
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.poisoned = False
         torch.cuda.synchronize(self.device)
         mine = [b.export() for b in self._ipc]
         handles = [None] * dp_size
@@ -78,6 +79,7 @@ class FusedDPGroup:
 
     def step_predict(self, opt, flat, lr: float, lr_pred: float, steps_ahead: int, out: torch.Tensor) -> None:
         """Signal this epoch's gradient, then the fused mean-over-replicas K3."""
+        self._live()
         if steps_ahead < 0:
             raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
         if flat.layout.numel != self.numel:
@@ -104,6 +106,7 @@ class FusedDPGroup:
         a device po_coef filled here). The grad-buffer parity alternates per
         call as in step_predict, so a captured run must hold an even number
         of updates to replay consistently."""
+        self._live()
         if steps_ahead < 0:
             raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
         if flat.layout.numel != self.numel:
@@ -133,6 +136,14 @@ class FusedDPGroup:
         self.parity ^= 1
 
     def check(self) -> None:
-        """Raise if a fused update timed out waiting for a replica (syncs)."""
-        if int(self.status.item()) != 0:
+        """Raise if a fused update timed out waiting for a replica (syncs).
+        The group is then poisoned: the kernel skipped that update (and would
+        skip every later one), so further updates raise instead of silently
+        advancing step counts over unchanged weights."""
+        if self.poisoned or int(self.status.item()) != 0:
+            self.poisoned = True
             raise RuntimeError("fused DP update timed out waiting for a replica's gradient signal")
+
+    def _live(self) -> None:
+        if self.poisoned:
+            raise RuntimeError("fused DP group is poisoned: an earlier update timed out waiting for a replica")

@@ -37,6 +37,14 @@ OPTIMIZER_KINDS = ("sgdm", "adam", "adamw")
 
 _INT64_MAX = (1 << 63) - 1
 
+# Test-only launch audit (tests/parity_audit.py). When set, every eager K1 /
+# K2 / K3 launch of an OptimizerState is bracketed by AUDIT.before(opt, op,
+# flat, out) -> token and AUDIT.after(token, lr, lr_pred, steps_ahead), and
+# runtime.execute reports each forward's weights (AUDIT.forward), so a test
+# can replay every update and prediction of a real run through the oracle.
+# None in production: one attribute test per launch.
+AUDIT = None
+
 
 @dataclass(frozen=True)
 class OptimizerConfig:
@@ -348,12 +356,15 @@ class OptimizerState:
             _lib.check(rc, "po_step_dc")
             self.step_count += 1
             return
+        tok = AUDIT.before(self, "step", flat, None) if AUDIT is not None else None
         rc = self._lib.po_step(
             ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1),
             _ptr(self._s2), None, flat.layout.numel, float(lr), self.step_count,
             _ptr(self._bad), self._launch_ref(), _stream(flat.data.device),
         )
         _lib.check(rc, "po_step")
+        if tok is not None:
+            AUDIT.after(tok, lr, None, None)
         self._after_step()
         self.step_count += 1
 
@@ -372,12 +383,15 @@ class OptimizerState:
             )
             _lib.check(rc, "po_predict_dc")
             return
+        tok = AUDIT.before(self, "predict", flat, out) if AUDIT is not None else None
         rc = self._lib.po_predict(
             ctypes.byref(self._hp), _ptr(flat.data), _ptr(self._s1), _ptr(self._s2), _ptr(out),
             flat.layout.numel, float(lr) * steps_ahead, self.step_count, self._launch_ref(),
             _stream(flat.data.device),
         )
         _lib.check(rc, "po_predict")
+        if tok is not None:
+            AUDIT.after(tok, None, lr, steps_ahead)
 
     def step_predict_(
         self, flat: FlatParams, lr: float, lr_pred: float, steps_ahead: int, out: torch.Tensor
@@ -397,12 +411,15 @@ class OptimizerState:
             _lib.check(rc, "po_step_predict_dc")
             self.step_count += 1
             return
+        tok = AUDIT.before(self, "step_predict", flat, out) if AUDIT is not None else None
         rc = self._lib.po_step_predict(
             ctypes.byref(self._hp), _ptr(flat.data), _ptr(flat.grad), _ptr(self._s1),
             _ptr(self._s2), _ptr(out), flat.layout.numel, float(lr), float(lr_pred) * steps_ahead,
             self.step_count, _ptr(self._bad), self._launch_ref(), _stream(flat.data.device),
         )
         _lib.check(rc, "po_step_predict")
+        if tok is not None:
+            AUDIT.after(tok, lr, lr_pred, steps_ahead)
         self._after_step()
         self.step_count += 1
 
@@ -667,6 +684,7 @@ class HostStreamer:
             ev.record(self.s_comp)
             self.ev_free[k] = ev
         cur.wait_stream(self.s_comp)
+        opt._after_step()  # eager_checks: raise NumericError now, like step_predict
         opt.step_count += 1
         return n_chunks
 

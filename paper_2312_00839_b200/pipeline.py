@@ -258,7 +258,10 @@ class _OpGraphs:
                                            need_input_grad=r.rank > 0)
             return g_in
 
-        return self._run(("B", slot), fn)
+        # keyed on the weights' address like the forward: under weight stashing
+        # / 2BW the backward reads a per-version snapshot whose address the
+        # captured graph bakes in
+        return self._run(("B", slot, weights[0].data_ptr()), fn)
 
     def update(self, op):
         from . import _lib

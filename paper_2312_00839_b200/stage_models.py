@@ -20,6 +20,13 @@ weight explicitly; LSTM layers use `LiveLSTM` (cuBLAS GEMMs + the
 po_lstm_cell_fwd/bwd kernels), whose backward propagates through the live
 weights (cuDNN's LSTM would keep its own packed forward-time copy).
 
+Exception — the bf16-autocast variant (`amp_dtype`, a throughput-only arm of
+the bench): autocast casts each conv weight to a fresh bf16 tensor, and the
+convolution's autograd node saves THAT copy, so conv input gradients go
+through the forward-time (predicted) weights, not the live ones. Linear
+layers keep the live-weight rule. The amp arm therefore does not carry the
+S9 semantics and is excluded from every parity claim; the fp32 path does.
+
 Image stages can run NHWC inside the stage (`channels_last=True`; boundary
 tensors stay NCHW), and their batch norms run on PyTorch's native kernels:
 cuDNN's training batch-norm kernels synchronise across their grid and can

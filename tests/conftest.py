@@ -6,6 +6,9 @@ import pytest
 ROOT = Path(__file__).resolve().parent.parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+TESTS = Path(__file__).resolve().parent
+if str(TESTS) not in sys.path:  # test helpers (parity_audit)
+    sys.path.insert(0, str(TESTS))
 
 REFERENCE_SRC = Path("/root/reference/pkg/src")
 
