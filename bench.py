@@ -512,6 +512,10 @@ def ours(args):
     torch.cuda.set_device(device)
     if world > 1:
         if args.dist_backend == "nccl":
+            # keep NCCL's communicator-init lines (rank counts, NVLS/P2P
+            # transports) in stderr so a multi-GPU run can be audited
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group("gloo")

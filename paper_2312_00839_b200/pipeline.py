@@ -50,6 +50,49 @@ class StageReport:
     executed: list
 
 
+def input_link(kind, stage: int, depth: int):
+    """The boundary message a work op of `stage` consumes: ("act", k) is the
+    activation k -> k+1, ("grad", k) the input gradient k+1 -> k; None for
+    stage 0's forwards and the last stage's backwards (local inputs)."""
+    if kind == FORWARD and stage > 0:
+        return ("act", stage - 1)
+    if kind == BACKWARD and stage < depth - 1:
+        return ("grad", stage)
+    return None
+
+
+def output_link(kind, stage: int, depth: int):
+    """The boundary message a work op of `stage` produces (None: kept local)."""
+    if kind == FORWARD and stage < depth - 1:
+        return ("act", stage)
+    if kind == BACKWARD and stage > 0:
+        return ("grad", stage - 1)
+    return None
+
+
+def exchange_plan(program, stage: int, depth: int) -> list[list[tuple[str, tuple, int]]]:
+    """The grouped exchanges PipelineStageRunner.run posts, in posting order:
+    group 0 = {recv work[0]'s input}; group i+1 = {send work[i]'s output,
+    recv work[i+1]'s input} — entries ("send" | "recv", link, mb). Every group
+    is one batch_isend_irecv (ncclGroupStart/End); tests/test_nccl_groups.py
+    checks that these plans cannot deadlock under NCCL's group semantics."""
+    work = [op for op in program if op.kind != UPDATE]
+    groups = []
+    first = input_link(work[0].kind, stage, depth) if work else None
+    groups.append([("recv", first, work[0].mb)] if first else [])
+    for i, op in enumerate(work):
+        g = []
+        out = output_link(op.kind, stage, depth)
+        if out:
+            g.append(("send", out, op.mb))
+        if i + 1 < len(work):
+            nxt = input_link(work[i + 1].kind, stage, depth)
+            if nxt:
+                g.append(("recv", nxt, work[i + 1].mb))
+        groups.append(g)
+    return groups
+
+
 class _Req:
     """A communication request whose wait() may be called more than once: a
     gloo send's wait consumes its completion, so a second wait (the run loop
@@ -368,11 +411,12 @@ class PipelineStageRunner:
     # -- what each op consumes / produces -------------------------------------------------
 
     def _input_spec(self, op):
-        if op.kind == FORWARD and self.rank > 0:
+        link = input_link(op.kind, self.rank, self.depth)
+        if link is None:
+            return None
+        if link[0] == "act":
             return (self.rows, *self.stage.in_shape), self.stage_ranks[self.rank - 1]
-        if op.kind == BACKWARD and self.rank < self.depth - 1:
-            return (self.rows, *self.stage.out_shape), self.stage_ranks[self.rank + 1]
-        return None
+        return (self.rows, *self.stage.out_shape), self.stage_ranks[self.rank + 1]
 
     def run(self) -> StageReport:
         work = [op for op in self.program if op.kind != UPDATE]
@@ -440,7 +484,7 @@ class PipelineStageRunner:
                 rec = VersionRecord(op.mb, 0, self.rank, fv, predicted, target)
                 records[op.mb] = rec
                 order.append(rec)
-                if not last:
+                if output_link(op.kind, self.rank, self.depth):
                     out_msg = (out if out.is_contiguous() else out.contiguous(), self.stage_ranks[self.rank + 1])
                 else:
                     if self.eager and not bool(torch.isfinite(loss)):
@@ -460,7 +504,7 @@ class PipelineStageRunner:
                 self.rt.pending_count = 1
                 rec.backward_version = bv
                 rec.live_backward_version = self.stage.version
-                if self.rank > 0:
+                if output_link(op.kind, self.rank, self.depth):
                     out_msg = (g_in if g_in.is_contiguous() else g_in.contiguous(), self.stage_ranks[self.rank - 1])
             snapshot_peak = max(snapshot_peak, self.policy.snapshot_count(self.rt))
             wi += 1

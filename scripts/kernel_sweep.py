@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import itertools
 import json
 import statistics
 import sys
@@ -132,19 +133,23 @@ def main():
     rows = []
     print(f"# device {torch.cuda.get_device_name()}  measured copy peak {peak} GB/s", flush=True)
     if args.tune_small:
-        shapes = [(512, 1, 1), (512, 2, 1), (512, 4, 1), (256, 8, 1), (256, 4, 2), (128, 16, 1), (1024 // 2, 2, 2),
-                  (256, 8, 2), (128, 16, 2), (256, 6, 1)]
+        shapes = [(512, 1, 1), (512, 2, 1), (512, 4, 1), (256, 8, 1), (256, 4, 2), (128, 16, 1), (512, 2, 2),
+                  (256, 8, 2), (128, 16, 2), (256, 6, 1), (128, 8, 1), (128, 8, 2), (128, 8, 4), (256, 4, 4),
+                  (512, 2, 4), (512, 1, 4), (256, 2, 4)]
         for lg in (20, 22, 24):
             n = 1 << lg
             b = Buffers(n)
             for kernel in args.kernels.split(","):
                 for kind in args.kinds.split(","):
-                    for block, cps, unroll in shapes:
-                        la = _lib.make_launch(block, cps, 8, 1, unroll)
+                    for (block, cps, unroll), cache in itertools.product([(None, None, None)] + shapes, (1, 4)):
+                        if block is None and cache == 4:
+                            continue
+                        la = None if block is None else _lib.make_launch(block, cps, 8, cache, unroll)
                         med, best = time_kernel(lib, kernel, kind, b, la, reps=20, warmup=3)
                         gbs = BYTES[(kernel, kind)] * n / med / 1e9
-                        row = dict(n=n, kernel=kernel, kind=kind, block=block, cps=cps, unroll=unroll,
-                                   us=round(med * 1e6, 2), gbs=round(gbs, 1), flush=FLUSH)
+                        row = dict(n=n, kernel=kernel, kind=kind, block=block, cps=cps, unroll=unroll, cache=cache,
+                                   us=round(med * 1e6, 2), gbs=round(gbs, 1), frac=round(gbs / peak, 4),
+                                   flush=FLUSH)
                         rows.append(row)
                         print(json.dumps(row), flush=True)
     elif args.tune_all:
