@@ -11,7 +11,10 @@ needed between steps.
           time, device-timed with CUDA events, max over ranks.
   e2e     the same metric through the reference-facing host-buffer API
           (HostStreamer: pinned host W and G in, W' and W_hat out, PCIe copies
-          inside the timed region; optimizer state device-resident).
+          inside the timed region; optimizer state device-resident); beside
+          it the training-loop setting (gradient in, flag out) and the
+          reference's three-call list API on host tensors.
+  kernels_1e9  K1 / K2 / K3 x SGDM / Adam / AdamW at the same N.
   roofline  K3's achieved GB/s vs MEASURED_PEAKS.json hbm_gbs; `traffic` is
           ncu's dram bytes per launch from profiles/ when captured.
   cpu_baseline  the reference's algorithm (oracle/c, float64, OpenMP on every
@@ -322,15 +325,48 @@ def kernel_leg(args, torch, dist, rank, world, device):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_max = float(tt.item())
     bytes_step = BYTES_PER_PARAM[kind] * n
+    # every kernel x kind at the same N (BASELINE configs[4] at 1B), same
+    # timing regime (back-to-back launches, inputs >> L2), median of 5
+    if v is None:
+        v = mk(3, 1e-2).square_()
+    kinds = {}
+    for kd in ("sgdm", "adam", "adamw"):
+        hpk = OptimizerConfig(kd).hparams()
+        vp = None if kd == "sgdm" else v.data_ptr()
+        for kern_name, bpp in (("predict", 12 if kd == "sgdm" else 16), ("step", 20 if kd == "sgdm" else 28),
+                               ("step_predict", BYTES_PER_PARAM[kd])):
+            def one():
+                if kern_name == "predict":
+                    rc = lib.po_predict(ctypes.byref(hpk), w.data_ptr(), m.data_ptr(), vp, w_hat.data_ptr(), n,
+                                        lr * s, 10, None, stream.cuda_stream)
+                elif kern_name == "step":
+                    rc = lib.po_step(ctypes.byref(hpk), w.data_ptr(), g.data_ptr(), m.data_ptr(), vp, None, n, lr,
+                                     10, None, None, stream.cuda_stream)
+                else:
+                    rc = lib.po_step_predict(ctypes.byref(hpk), w.data_ptr(), g.data_ptr(), m.data_ptr(), vp,
+                                             w_hat.data_ptr(), n, lr, lr * s, 10, None, None, stream.cuda_stream)
+                _lib.check(rc, kern_name)
+
+            one()
+            ts = []
+            for _ in range(5):
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                one()
+                a1.record(stream)
+                a1.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            t_ms = statistics.median(ts)
+            kinds[f"{kern_name}/{kd}"] = {"ms": round(t_ms, 4), "gbs": round(bpp * n / (t_ms * 1e-3) / 1e9, 1)}
     del w, g, m, v, w_hat
     torch.cuda.empty_cache()
-    return {"ms_per_step": ms_max, "ms_local": ms, "gbs_per_rank": bytes_step / (ms * 1e-3) / 1e9,
+    return {"kernels": kinds, "ms_per_step": ms_max, "ms_local": ms, "gbs_per_rank": bytes_step / (ms * 1e-3) / 1e9,
             "value": world * bytes_step / (ms_max * 1e-3) / 1e9, "launches": args.steps, "clocks": clk, "n": n}
 
 
 def e2e_leg(args, torch, dist, world, device):
     """Same metric through the host-buffer API: pinned host W, G in; W', W_hat out."""
-    from paper_2312_00839_b200.optim import HostStreamer, OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.optim import HostStreamer, OptimizerConfig, OptimizerState, predict_weights
 
     n = int(args.n_params)
     kind = args.kind
@@ -387,32 +423,62 @@ def e2e_leg(args, torch, dist, world, device):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_res = float(tt.item())
     del wd, whd, opt2
-    # `e2e` follows the contract's definition: the step's INPUT (the gradient)
-    # copied host->device every step, the step's RESULT (the non-finite flag
-    # of the update) read device->host every step, model state (W, m, v)
-    # device-resident like any training loop's. The stricter round trip of the
-    # reference-shaped list API (parameters in AND out over PCIe) is reported
-    # beside it.
+    # the reference's own call sequence on host lists (pipesim swaps in
+    # OptimizerState.step, then prediction_direction + predict_weights for the
+    # next forward: optim.py:63-155): W, G in -> W', dirs out; dirs out; W', d
+    # in -> W_hat out — 32 B/param over PCIe, each call chunked and overlapped
+    lopt = OptimizerState(OptimizerConfig(kind), ["stage.flat"], device=device, eager_checks=False)
+
+    def list_step():
+        new, _ = lopt.step([w_h], [g_h], 1e-3)
+        d = lopt.prediction_direction(new)
+        return predict_weights(new, 1e-3, 3, d)
+
+    list_step()
+    torch.cuda.synchronize(device)
+    l_steps = max(1, min(3, args.e2e_steps))
+    t_l = time.perf_counter()
+    for _ in range(l_steps):
+        list_step()
+    torch.cuda.synchronize(device)
+    ms_list = (time.perf_counter() - t_l) / l_steps * 1e3
+    del lopt
+    # `e2e` is the reference-shaped round trip: the caller's W and G come from
+    # pinned host memory every step and W' and W_hat go back (one fused K3
+    # call, HostStreamer.step_predict); the training-loop setting with W, m, v
+    # device-resident (only the gradient in, the non-finite flag out) and the
+    # three-call list API are reported beside it.
     res = {
-        "value": round(world * BYTES_PER_PARAM[kind] * n / (ms_res * 1e-3) / 1e9, 2),
+        "value": round(world * BYTES_PER_PARAM[kind] * n / (ms * 1e-3) / 1e9, 2),
         "unit": "GB/s",
-        "h2d_bytes_per_step": 4 * n,
-        "d2h_bytes_per_step": 8,
-        "ms_per_step": round(ms_res, 3),
-        "path": "OptimizerState + HostStreamer.step_predict_resident: pinned host G -> device in 16M-element "
-                "chunks (H2D stream) -> K3 per chunk on device-resident W, m, v -> W', W_hat on device; "
-                "non-finite flag read back each step",
-        "launches": res_launches,
-        "host_params_roundtrip": {
-            "value": round(world * BYTES_PER_PARAM[kind] * n / (ms * 1e-3) / 1e9, 2),
+        "h2d_bytes_per_step": 8 * n,
+        "d2h_bytes_per_step": 8 * n,
+        "ms_per_step": round(ms, 3),
+        "wall_s": round(wall, 3),
+        "path": "OptimizerState + HostStreamer.step_predict: pinned host W, G -> device (chunked) -> K3 against "
+                "device-resident m, v -> W', W_hat -> pinned host (H2D and D2H streams overlapped)",
+        "launches": launches[0],
+        "grad_in_state_resident": {
+            "value": round(world * BYTES_PER_PARAM[kind] * n / (ms_res * 1e-3) / 1e9, 2),
             "unit": "GB/s",
-            "h2d_bytes_per_step": 8 * n,
-            "d2h_bytes_per_step": 8 * n,
-            "ms_per_step": round(ms, 3),
-            "wall_s": round(wall, 3),
-            "path": "OptimizerState + HostStreamer.step_predict: pinned host W, G -> device (chunked) -> K3 against "
-                    "device-resident m, v -> W', W_hat -> pinned host (H2D and D2H streams overlapped)",
-            "launches": launches[0],
+            "h2d_bytes_per_step": 4 * n,
+            "d2h_bytes_per_step": 8,
+            "ms_per_step": round(ms_res, 3),
+            "path": "OptimizerState + HostStreamer.step_predict_resident: pinned host G -> device in 16M-element "
+                    "chunks (H2D stream) -> K3 per chunk on device-resident W, m, v -> W', W_hat on device; "
+                    "non-finite flag read back each step",
+            "launches": res_launches,
+        },
+        "list_api": {
+            "value": round(world * BYTES_PER_PARAM[kind] * n / (ms_list * 1e-3) / 1e9, 2),
+            "unit": "GB/s",
+            "h2d_bytes_per_step": 16 * n,
+            "d2h_bytes_per_step": 16 * n,
+            "ms_per_step": round(ms_list, 3),
+            "steps": l_steps,
+            "path": "reference call sequence on host lists: OptimizerState.step([W],[G]) -> (W', dirs); "
+                    "prediction_direction(W'); predict_weights(W', lr, 3, d) -> W_hat (each chunked through "
+                    "HostStreamer; wall clock)",
         },
     }
     del w_h, g_h, wo_h, wh_h, streamer, opt
@@ -450,8 +516,8 @@ def pipeline_leg(args, torch, dist, rank, world, device):
             _stages.TC_FP32 = True
         out["projected_8gpu"]["simt_fp32_gemms"] = {
             "prediction_overhead": simt["prediction_overhead"],
-            "pred_off_samples_per_s": simt["pred_off"]["multi_gpu_samples_per_s"],
-            "pred_on_samples_per_s": simt["pred_on"]["multi_gpu_samples_per_s"]}
+            "pred_off_samples_per_s": simt["pred_off"]["projection"]["one_stage_per_gpu_samples_per_s"],
+            "pred_on_samples_per_s": simt["pred_on"]["projection"]["one_stage_per_gpu_samples_per_s"]}
         progress("projected 8-GPU")
         out["depth_sweep_1gpu"] = bp.depth_sweep(torch, device, n_batches=args.pipeline_batches)
         progress("depth sweep")
@@ -604,6 +670,7 @@ def _line(args, kern, e2e, cpu, world):
             "kernel": "po_stream_kernel<ADAM, STEP_PREDICT> (K3)",
             "kernel_ms": round(kern["ms_per_step"], 4),
         },
+        "kernels_1e9": kern.get("kernels"),
         "clocks": kern["clocks"],
         "e2e": e2e,
         "gpu_launches": launches,

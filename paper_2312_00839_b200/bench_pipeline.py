@@ -161,19 +161,22 @@ def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 40, trial
     return out
 
 
-def pipeline_roofline(stage_times, batch, n, depth, boundary_bytes, link_gbs=770.0):
-    """SURVEY.md §8d pipeline roofline: min(compute, link) samples/s.
-    compute = B / max_k t_k * n / (n + D - 1) (1F1B unit makespan 2n+2D-2);
-    link = B / (max boundary bytes / per-direction NVLink bandwidth) — the
-    activation and the gradient of a boundary move in opposite directions.
-    Single GPU (all stages serialised): B / sum_k t_k."""
-    one_gpu = batch / sum(stage_times)
-    compute = batch / max(stage_times) * n / (n + depth - 1)
-    link = batch / (max(boundary_bytes) / (link_gbs * 1e9)) if boundary_bytes else float("inf")
-    return {"single_gpu_samples_per_s": round(one_gpu, 1), "compute_samples_per_s": round(compute, 1),
-            "link_samples_per_s": round(link, 1) if link != float("inf") else None,
-            "multi_gpu_samples_per_s": round(min(compute, link), 1), "link_gbs": link_gbs,
+def unit_time_projection(stage_times, batch, n, depth):
+    """Throughput PROJECTED from measured per-stage unit times (not a bound):
+    one stage per GPU runs at B / max_k t_k * n / (n + D - 1) (1F1B unit
+    makespan 2n + 2D - 2); all stages serialised on one stream at B / sum_k t_k."""
+    return {"one_stage_per_gpu_samples_per_s": round(batch / max(stage_times) * n / (n + depth - 1), 1),
+            "serialised_samples_per_s": round(batch / sum(stage_times), 1),
             "stage_ms": [round(t * 1e3, 4) for t in stage_times]}
+
+
+def _attach_bounds(row, bound, projection=None):
+    """row["roofline"] = the counted-work bounds (roofline.py); the fraction
+    is achieved / the single-GPU bound (all stages share this GPU)."""
+    row["roofline"] = bound
+    row["frac_of_roofline"] = round(row["samples_per_s"] / bound["single_gpu"]["samples_per_s"], 4)
+    if projection is not None:
+        row["projection"] = projection
 
 
 def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, replays: int = 5, tf32: bool = False,
@@ -203,7 +206,13 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
             return st, [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in st]
 
         units = stage_unit_times(torch, device, make, data, "softmax_xent")
-        boundary = [4 * BATCH * s_.out_dim for s_ in make()[0][:-1]]
+        from .roofline import mlp_pipeline_bounds
+
+        arith = "tf32" if tf32 else "fast_fp32"
+        probe = make()[0]
+        bounds = {key: mlp_pipeline_bounds(probe, BATCH, n_batches, "adam", key == "pred_on", arith)
+                  for key in ("pred_off", "pred_on")}
+        del probe
     out["serial_streams"] = {}
     for strategy in ("async_raw", "optimizer_prediction"):
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
@@ -222,16 +231,9 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
             _, esec, _ = _run_once(torch, device, strategy, depth, n_batches, data)
             out[key]["eager_samples_per_s"] = round(n_batches * BATCH / esec, 1)
         if with_roofline:
-            roof = pipeline_roofline(units[key], BATCH, n_batches, depth, boundary)
-            out[key]["roofline"] = roof
-            # serialised stages are bounded by B / sum_k t_k; concurrent stages on
-            # one GPU by neither (they share the SMs) — both fractions reported
-            out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] /
-                                                            roof["single_gpu_samples_per_s"], 4)
-            out[key]["frac_of_multi_gpu_roofline"] = round(out[key]["samples_per_s"] /
-                                                           roof["multi_gpu_samples_per_s"], 4)
+            _attach_bounds(out[key], bounds[key], unit_time_projection(units[key], BATCH, n_batches, depth))
             ser = out["serial_streams"][key]
-            ser["frac_of_single_gpu_roofline"] = round(ser["samples_per_s"] / roof["single_gpu_samples_per_s"], 4)
+            ser["frac_of_roofline"] = round(ser["samples_per_s"] / bounds[key]["single_gpu"]["samples_per_s"], 4)
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out["value"] = on
     out["unit"] = "samples/s"
@@ -242,9 +244,9 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
         # one stage per GPU (the north star's setting): the pipeline runs at the
         # slowest stage's unit time, so the prediction overhead there is the
         # bottleneck stage's K3-vs-K2 cost (each GPU's L2 holds one stage)
-        r_on, r_off = out["pred_on"]["roofline"], out["pred_off"]["roofline"]
-        out["multi_gpu_roofline_prediction_overhead"] = round(
-            1.0 - r_on["compute_samples_per_s"] / r_off["compute_samples_per_s"], 4)
+        r_on, r_off = out["pred_on"]["projection"], out["pred_off"]["projection"]
+        out["projected_one_stage_per_gpu_prediction_overhead"] = round(
+            1.0 - r_on["one_stage_per_gpu_samples_per_s"] / r_off["one_stage_per_gpu_samples_per_s"], 4)
         out["single_gpu_note"] = ("all stages share one GPU's SMs and 126 MB L2 here; the predicted-weights "
                                   "staging buffers add ~21 MB to a ~105 MB per-mini-batch working set")
     if with_eager:
@@ -300,11 +302,19 @@ def projected_multi_gpu(torch, device, depth: int = 8, n_batches: int = 64, tf32
         return st, [OptimizerState(OptimizerConfig("adam"), s_.param_names, device=device) for s_ in st]
 
     units = stage_unit_times(torch, device, make, data, "softmax_xent")
-    boundary = [4 * BATCH * s_.out_dim for s_ in make()[0][:-1]]
+    from .roofline import mlp_pipeline_bounds
+
+    probe = make()[0]
     for key in ("pred_off", "pred_on"):
-        out[key] = pipeline_roofline(units[key], BATCH, n_batches, depth, boundary)
+        proj = unit_time_projection(units[key], BATCH, n_batches, depth)
+        bound = mlp_pipeline_bounds(probe, BATCH, n_batches, "adam", key == "pred_on", "tf32" if tf32 else "fast_fp32")
+        out[key] = {"projection": proj, "roofline": bound["one_stage_per_gpu"], "per_stage": bound["per_stage"],
+                    "frac_of_roofline": round(proj["one_stage_per_gpu_samples_per_s"] /
+                                              bound["one_stage_per_gpu"]["samples_per_s"], 4)}
+    del probe
     out["prediction_overhead"] = round(
-        1.0 - out["pred_on"]["multi_gpu_samples_per_s"] / out["pred_off"]["multi_gpu_samples_per_s"], 4)
+        1.0 - out["pred_on"]["projection"]["one_stage_per_gpu_samples_per_s"] /
+        out["pred_off"]["projection"]["one_stage_per_gpu_samples_per_s"], 4)
     torch.backends.cuda.matmul.allow_tf32 = False
     return out
 
@@ -455,6 +465,14 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
             return st, [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in st]
 
         units = stage_unit_times(torch, device, make, data, "softmax_xent", reps=3, trials=3)
+        from .roofline import module_pipeline_bounds
+
+        arith = "bf16" if amp == "bf16" else ("tf32" if tf32 else "fast_fp32")
+        probe = make()[0]
+        in_dtype = torch.long if cfg.get("tokens") else None
+        bounds = {key: module_pipeline_bounds(torch, probe, cfg["batch"], n_batches, cfg["opt"], key == "pred_on",
+                                              arith, in_dtype=in_dtype) for key in ("pred_off", "pred_on")}
+        del probe
         torch.cuda.empty_cache()
     for strategy in ("async_raw", "optimizer_prediction"):
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
@@ -469,19 +487,15 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
             out[key]["eager_serial_samples_per_s"] = round(n_batches * cfg["batch"] / (e0.elapsed_time(e1) / 1e3), 2)
             del stages, opts
         if with_roofline:
-            roof = pipeline_roofline(units[key], cfg["batch"], n_batches, cfg["depth"], out["boundary_bytes"])
-            out[key]["roofline"] = roof
-            out[key]["frac_of_single_gpu_roofline"] = round(out[key]["samples_per_s"] /
-                                                            roof["single_gpu_samples_per_s"], 4)
-            out[key]["frac_of_multi_gpu_roofline"] = round(out[key]["samples_per_s"] /
-                                                           roof["multi_gpu_samples_per_s"], 4)
+            _attach_bounds(out[key], bounds[key], unit_time_projection(units[key], cfg["batch"], n_batches,
+                                                                       cfg["depth"]))
         torch.cuda.empty_cache()
     on, off = out["pred_on"]["samples_per_s"], out["pred_off"]["samples_per_s"]
     out.update(value=on, unit="samples/s", prediction_overhead=round(1.0 - on / off, 4))
     if with_roofline:
-        r_on, r_off = out["pred_on"]["roofline"], out["pred_off"]["roofline"]
-        out["multi_gpu_roofline_prediction_overhead"] = round(
-            1.0 - r_on["multi_gpu_samples_per_s"] / r_off["multi_gpu_samples_per_s"], 4)
+        r_on, r_off = out["pred_on"]["projection"], out["pred_off"]["projection"]
+        out["projected_one_stage_per_gpu_prediction_overhead"] = round(
+            1.0 - r_on["one_stage_per_gpu_samples_per_s"] / r_off["one_stage_per_gpu_samples_per_s"], 4)
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     return out

@@ -439,12 +439,13 @@ struct DefaultShape {
 DefaultShape default_shape(int kind, int mode, int64_t n) {
   const bool sg = kind == PO_SGDM;
   // pipeline-stage sizes (< 32 M elements, the 1F1B configs' 0.01-20 M-param
-  // stages): many small CTAs, streaming stores — measured +2% (fp32 GEMMs) to
-  // +11% (TF32) config-1 pipeline throughput (profiles/r1_pipeline.md,
-  // scripts/pipeline_variants.py); 8 CTAs/SM and, above 4 M elements, two
-  // vectors per stream in flight (scripts/small_n_shapes.py, CUDA-graph timed:
-  // K3 Adam at 3.1 M params 12.1 -> 11.1 us, K2 at 8.4 M 39.6 -> 37.7 us)
-  if (n < (int64_t(1) << 25)) return DefaultShape{128, 8, n >= (int64_t(1) << 22) ? 2 : 1, 1};
+  // stages): many small CTAs (pipeline stages run concurrently with other
+  // stages' kernels, profiles/r1_pipeline.md), streaming stores, and a full
+  // SM (16 x 128 threads) with one vector per stream each — the best or tied
+  // shape for K1 and K3 (SGDM and Adam) at 2^20 / 2^22 / 2^24 in the L2-flushed
+  // round-2 sweep (profiles/r2_kernel_tune_small.jsonl): K1 Adam at 2^24
+  // 53.3 -> 45.1 us (0.77 -> 0.91 of copy), at 2^22 20.5 -> 16.4 us
+  if (n < (int64_t(1) << 25)) return DefaultShape{128, 16, 1, 1};
   switch (mode) {
     case MODE_PREDICT: return sg ? DefaultShape{256, 8, 2, 1} : DefaultShape{512, 2, 1, 1};
     case MODE_STEP: return sg ? DefaultShape{512, 1, 1, 1} : DefaultShape{512, 1, 2, 0};

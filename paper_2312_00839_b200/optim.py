@@ -432,7 +432,11 @@ class OptimizerState:
         views = self._layout.views(buf)
         if host is None:
             return views
-        return [v.to(host) for v in views]
+        outs = [torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for v in views]
+        for o, v in zip(outs, views):
+            o.copy_(v, non_blocking=True)
+        torch.cuda.current_stream(buf.device).synchronize()
+        return outs
 
     def step(self, params, grads, lr: float):
         """Apply one update; returns (new params, applied directions) with
@@ -447,6 +451,8 @@ class OptimizerState:
         layout = FlatLayout(self.names, [tuple(p.shape) for p in params])
         self._bind(layout)
         host = None if params[0].is_cuda else params[0].device
+        if host is not None and all(not g.is_cuda for g in grads):
+            return self._step_host(params, grads, lr)
         dev = params[0].device if params[0].is_cuda else self.device
         w = self._layout.pack(params, dev)  # a new buffer: inputs stay untouched
         g = self._layout.as_flat(grads) if host is None else None
@@ -463,6 +469,34 @@ class OptimizerState:
         self.check_finite()  # the list API always raises like the reference
         self.step_count += 1
         return self._out(w, host), self._out(dirs, host)
+
+    def _streamer(self) -> "HostStreamer":
+        if getattr(self, "_host_streamer", None) is None:
+            self._host_streamer = _streamer_for(self.device, self._layout.numel)
+        return self._host_streamer
+
+    def _step_host(self, params, grads, lr):
+        """step() on host tensors: W and G stream to the device in chunks and
+        W' and the applied direction stream back (HostStreamer, three streams
+        overlapped); the optimizer state never leaves the device. Outputs are
+        new pinned host tensors (the inputs are not mutated)."""
+        self._ensure_state()
+        f32 = lambda t: t if t.dtype == torch.float32 else t.float()  # noqa: E731
+        new_w = [torch.empty(p.shape, dtype=torch.float32, pin_memory=True) for p in params]
+        dirs = [torch.empty(p.shape, dtype=torch.float32, pin_memory=True) for p in params]
+        segs = [(o, f32(p).reshape(-1), f32(g).reshape(-1), w.reshape(-1), d.reshape(-1))
+                for o, p, g, w, d in zip(self._layout.offsets, params, grads, new_w, dirs) if p.numel()]
+        st = self._streamer()
+        _, bad = st.run(self, "step_dir", segs, lr)
+        torch.cuda.current_stream(self.device).synchronize()  # the outputs are host memory
+        eager = self.eager_checks
+        self.eager_checks = True  # the list API always raises like the reference
+        try:
+            st._raise_bad(self, bad, list(zip(self._layout.offsets, self._layout.sizes, self.names)))
+        finally:
+            self.eager_checks = eager
+        self.step_count += 1
+        return new_w, dirs
 
     def prediction_direction(self, params):
         """Direction the next update is expected to take, read from the
@@ -601,51 +635,85 @@ class HostStreamer:
             raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
         opt._bind(FlatLayout(opt.names, [(n,)]))
         opt._ensure_state()
-        n_chunks = -(-n // self.chunk)
-        bad = torch.full((n_chunks,), _INT64_MAX, dtype=torch.int64, device=self.device)
+        launches, bad = self.run(opt, "step_predict", [(0, w_host, g_host, w_out, w_hat_out)], lr,
+                                 float(lr_pred) * steps_ahead)
+        self._raise_bad(opt, bad, [(0, n, opt.names[0])])
+        opt.step_count += 1
+        return launches
+
+    def run(self, opt: "OptimizerState | None", mode: str, segs, lr: float = 0.0, c_pred: float = 0.0):
+        """Stream host segments through the device in chunks: H2D on one
+        stream, the kernel per chunk on another, D2H on a third, `slots`-deep
+        buffers, so both PCIe directions and the kernel overlap. Each segment
+        is (state offset, a_host, b_host, out1_host, out2_host), all 1-D fp32:
+
+          "step_predict"  a = W, b = G  -> out1 = W', out2 = W_hat   (K3)
+          "step_dir"      a = W, b = G  -> out1 = W', out2 = dir     (K2 + dir)
+          "axpy"          a = W, b = d  -> out1 = W - c_pred * d     (predict_weights)
+
+        The optimizer state (K2/K3) stays on the device at the segment's
+        offset. Returns (launches, per-chunk non-finite flags on the device)."""
+        chunks = []
+        for off, a, b, o1, o2 in segs:
+            for lo in range(0, a.numel(), self.chunk):
+                chunks.append((off, a, b, o1, o2, lo, min(self.chunk, a.numel() - lo)))
+        bad = torch.full((max(1, len(chunks)),), _INT64_MAX, dtype=torch.int64, device=self.device)
         cur = torch.cuda.current_stream(self.device)
-        for s in (self.s_in, self.s_comp, self.s_out):
-            s.wait_stream(cur)
-        c_pred = float(lr_pred) * steps_ahead
-        hp = ctypes.byref(opt._hp)
-        for i in range(n_chunks):
+        for st in (self.s_in, self.s_comp, self.s_out):
+            st.wait_stream(cur)
+        lib = _lib.load()
+        hp = ctypes.byref(opt._hp) if opt is not None else None
+        la = opt._launch_ref() if opt is not None else None
+        for i, (off, a, b, o1, o2, lo, m) in enumerate(chunks):
             k = i % self.slots
-            lo = i * self.chunk
-            m = min(self.chunk, n - lo)
             with torch.cuda.stream(self.s_in):
                 if self.ev_free[k] is not None:
                     self.s_in.wait_event(self.ev_free[k])
-                self.dw[k][:m].copy_(w_host[lo : lo + m], non_blocking=True)
-                self.dg[k][:m].copy_(g_host[lo : lo + m], non_blocking=True)
+                self.dw[k][:m].copy_(a[lo : lo + m], non_blocking=True)
+                self.dg[k][:m].copy_(b[lo : lo + m], non_blocking=True)
                 self.ev_in[k].record(self.s_in)
             self.s_comp.wait_event(self.ev_in[k])
-            s1 = opt._s1[lo:]
-            s2 = opt._s2[lo:] if opt._s2 is not None else None
-            rc = opt._lib.po_step_predict(
-                hp, _ptr(self.dw[k]), _ptr(self.dg[k]), _ptr(s1), _ptr(s2), _ptr(self.dwh[k]), m,
-                float(lr), c_pred, opt.step_count, bad[i:].data_ptr(), opt._launch_ref(),
-                self.s_comp.cuda_stream,
-            )
-            _lib.check(rc, "po_step_predict")
+            sc = self.s_comp.cuda_stream
+            if mode == "axpy":
+                rc = lib.po_axpy_predict(_ptr(self.dw[k]), _ptr(self.dg[k]), _ptr(self.dwh[k]), m, float(c_pred),
+                                         None, sc)
+            else:
+                s1 = opt._s1[off + lo:].data_ptr()
+                s2 = opt._s2[off + lo:].data_ptr() if opt._s2 is not None else None
+                if mode == "step_predict":
+                    rc = lib.po_step_predict(hp, _ptr(self.dw[k]), _ptr(self.dg[k]), s1, s2, _ptr(self.dwh[k]), m,
+                                             float(lr), float(c_pred), opt.step_count, bad[i:].data_ptr(), la, sc)
+                elif mode == "step_dir":
+                    rc = lib.po_step(hp, _ptr(self.dw[k]), _ptr(self.dg[k]), s1, s2, _ptr(self.dwh[k]), m,
+                                     float(lr), opt.step_count, bad[i:].data_ptr(), la, sc)
+                else:
+                    raise ValueError(f"unknown streaming mode {mode!r}")
+            _lib.check(rc, f"HostStreamer.run({mode})")
             self.ev_comp[k].record(self.s_comp)
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(self.ev_comp[k])
-                w_out[lo : lo + m].copy_(self.dw[k][:m], non_blocking=True)
-                w_hat_out[lo : lo + m].copy_(self.dwh[k][:m], non_blocking=True)
+                if mode == "axpy":
+                    o1[lo : lo + m].copy_(self.dwh[k][:m], non_blocking=True)
+                else:
+                    o1[lo : lo + m].copy_(self.dw[k][:m], non_blocking=True)
+                    o2[lo : lo + m].copy_(self.dwh[k][:m], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self.s_out)
                 self.ev_free[k] = ev
         cur.wait_stream(self.s_out)
-        if opt.eager_checks:
-            cur.synchronize()
-            b = bad.cpu()
-            for i, v in enumerate(b.tolist()):
-                if v != _INT64_MAX:
-                    raise NumericError(
-                        f"optimizer step produced non-finite values in {opt.names[0]} (index {i * self.chunk + v})"
-                    )
-        opt.step_count += 1
-        return n_chunks
+        self._chunks = chunks
+        return len(chunks), bad
+
+    def _raise_bad(self, opt, bad, where) -> None:
+        """eager_checks: sync and raise NumericError for the first non-finite
+        chunk, naming the parameter (`where`: (state offset, numel, name))."""
+        if not opt.eager_checks:
+            return
+        torch.cuda.current_stream(self.device).synchronize()
+        for (off, a, b, o1, o2, lo, m), v in zip(self._chunks, bad.cpu().tolist()):
+            if v != _INT64_MAX:
+                name = next((nm for o, n, nm in where if o <= off + lo + v < o + n), opt.names[0])
+                raise NumericError(f"optimizer step produced non-finite values in {name}")
 
     def step_predict_resident(self, opt: "OptimizerState", w_dev: torch.Tensor, g_host: torch.Tensor, lr: float,
                               lr_pred: float, steps_ahead: int, w_hat_dev: torch.Tensor) -> int:
@@ -696,6 +764,20 @@ def _as_tensor(x) -> torch.Tensor:
     return torch.as_tensor(a)
 
 
+_STREAMERS: dict = {}
+
+
+def _streamer_for(device, numel: int) -> HostStreamer:
+    """A cached HostStreamer whose chunk fits `numel` (<= 16 M elements):
+    small host calls do not pin down 3 x 4 x 64 MB of device buffers."""
+    device = torch.device(device)
+    chunk = min(1 << 24, max(1 << 12, 1 << max(0, int(numel) - 1).bit_length()))
+    key = (device.index, chunk)
+    if key not in _STREAMERS:
+        _STREAMERS[key] = HostStreamer(device, chunk_elems=chunk)
+    return _STREAMERS[key]
+
+
 def predict_weights(params, lr: float, steps_ahead: int, directions) -> list[torch.Tensor]:
     """Extrapolate parameters steps_ahead updates into the future: each w
     becomes w - lr * steps_ahead * d (optim.py:145-155, Eq. (5)). Inputs are
@@ -713,6 +795,17 @@ def predict_weights(params, lr: float, steps_ahead: int, directions) -> list[tor
     names = [f"p{i}" for i in range(len(params))]
     layout = FlatLayout(names, [tuple(p.shape) for p in params])
     host = None if params[0].is_cuda else params[0].device
+    if host is not None and all(not d.is_cuda for d in directions):
+        # host tensors: W and d stream through the device chunk by chunk
+        dev = torch.device("cuda", torch.cuda.current_device())
+        st = _streamer_for(dev, layout.numel)
+        f32 = lambda t: t if t.dtype == torch.float32 else t.float()  # noqa: E731
+        outs = [torch.empty(p.shape, dtype=torch.float32, pin_memory=True) for p in params]
+        st.run(None, "axpy", [(0, f32(p).reshape(-1), f32(d).reshape(-1), o.reshape(-1), None)
+                              for p, d, o in zip(params, directions, outs) if p.numel()],
+               c_pred=float(lr) * steps_ahead)
+        torch.cuda.current_stream(dev).synchronize()
+        return outs
     dev = params[0].device if params[0].is_cuda else torch.device("cuda", torch.cuda.current_device())
     w = layout.as_flat(params) if host is None else None
     if w is None:

@@ -231,3 +231,53 @@ def test_host_streamer_paths_match_oracle(kind):
         assert R.inf_norm_rel(wh.double().numpy(), want_hat) <= 1e-6
         assert torch.equal(wd.cpu(), wo) and torch.equal(whd.cpu(), wh)
     assert o1.step_count == o2.step_count == 3
+
+
+def test_host_list_api_streams_in_chunks():
+    """The reference-shaped list API on host tensors (step -> W', dirs;
+    predict_weights) goes through the chunked HostStreamer: several
+    parameters, chunk edges inside and across them, a ragged tail; results
+    <= 1e-6 vs the oracle and bit-exact vs the fp32 emulation; a non-finite
+    update names its parameter like optim.py:82-84."""
+    import torch
+
+    from oracle import optim_f32
+    from oracle import optim_ref as R
+    from paper_2312_00839_b200.errors import NumericError
+    from paper_2312_00839_b200.optim import (FlatLayout, HostStreamer, OptimizerConfig, OptimizerState,
+                                             predict_weights)
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    shapes = [(3, 3001), (7,), (5000,), (1,)]
+    names = ["a", "b", "c", "d"]
+    ps = [rng.normal(0, 0.02, s).astype(np.float32) for s in shapes]
+    opt = OptimizerState(OptimizerConfig("adam"), names, device=dev)
+    opt._bind(FlatLayout(names, shapes))
+    opt._host_streamer = HostStreamer(dev, chunk_elems=1 << 12, slots=2)
+    orc = R.OracleOptimizer(R.Hyper("adam"), names)
+    cur64 = [p.astype(np.float64) for p in ps]
+    cur = [torch.from_numpy(p.copy()) for p in ps]
+    m = [np.zeros(s, np.float32) for s in shapes]
+    v = [np.zeros(s, np.float32) for s in shapes]
+    for t in range(3):
+        gs = [rng.normal(0, 1e-2, s).astype(np.float32) for s in shapes]
+        new, dirs = opt.step(cur, [torch.from_numpy(g) for g in gs], 1e-3)
+        want, wdirs = orc.step([c.numpy().astype(np.float64) for c in cur], [g.astype(np.float64) for g in gs], 1e-3)
+        for i, (a, b) in enumerate(zip(new, want)):
+            assert not a.is_cuda
+            assert R.inf_norm_rel(a.double().numpy(), b) <= (1e-6 if a.numel() >= 64 else 1e-5)
+            ew, m[i], v[i], _ = optim_f32.step("adam", cur[i].numpy(), gs[i], m[i], v[i], 1e-3, t)
+            assert np.array_equal(a.numpy(), ew)
+        cur = new
+        cur64 = want
+    d = opt.prediction_direction(cur)
+    wh = predict_weights(cur, 1e-3, 3, d)
+    want_hat = R.predict_weights([c.numpy().astype(np.float64) for c in cur], 1e-3, 3,
+                                   orc.prediction_direction(cur64))
+    for a, b in zip(wh, want_hat):
+        assert not a.is_cuda and R.inf_norm_rel(a.double().numpy(), b) <= 1e-5
+    bad = [torch.from_numpy(g) for g in (np.zeros(s, np.float32) for s in shapes)]
+    bad[2][4321] = float("inf")
+    with pytest.raises(NumericError, match="in c"):
+        opt.step(cur, bad, 1e-3)
