@@ -349,13 +349,14 @@ def kernel_leg(args, torch, dist, rank, world, device):
 
             one()
             ts = []
-            for _ in range(5):
+            for _ in range(3):  # 3 samples of 4 back-to-back launches, median
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
-                one()
+                for _ in range(4):
+                    one()
                 a1.record(stream)
                 a1.synchronize()
-                ts.append(a0.elapsed_time(a1))
+                ts.append(a0.elapsed_time(a1) / 4)
             t_ms = statistics.median(ts)
             kinds[f"{kern_name}/{kd}"] = {"ms": round(t_ms, 4), "gbs": round(bpp * n / (t_ms * 1e-3) / 1e9, 1)}
     del w, g, m, v, w_hat
@@ -521,6 +522,13 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         progress("projected 8-GPU")
         out["depth_sweep_1gpu"] = bp.depth_sweep(torch, device, n_batches=args.pipeline_batches)
         progress("depth sweep")
+        out["gpipe"] = {}
+        for name, nb in (("config1", args.pipeline_batches), ("config2_vgg16", 32), ("config3_resnet101", 16)):
+            try:
+                out["gpipe"][name] = bp.gpipe_comparison(torch, device, name, n_batches=nb)
+            except Exception as exc:
+                out["gpipe"][name] = {"error": f"{type(exc).__name__}: {exc}"}
+            progress(f"gpipe vs pipeoptim {name}")
         if not args.no_cpu:
             try:
                 out["cpu_baseline"] = cpu_pipeline_baseline()

@@ -506,3 +506,72 @@ def multi_gpu_pipeline(torch, dist, rank, world, device, n_batches: int = 64, ho
     from .pipeline import bench_config1_pipeline
 
     return bench_config1_pipeline(torch, dist, rank, world, device, n_batches=n_batches, host_staging=host_staging)
+
+
+def gpipe_comparison(torch, device, name: str = "config1", n_batches: int = 64, micros: int = 4, trials: int = 5,
+                     tf32: bool | None = None):
+    """The paper's throughput comparison: GPipe (T
+    micro-batches per mini-batch, gradients averaged over them before one
+    synchronous update per stage; schedule.py:114-147, runtime.py:441-454)
+    vs PipeOptim (1F1B with prediction) on the same stages, batch and GPU.
+    Both are whole-run CUDA graphs on the stage-concurrent single-GPU runner,
+    replayed in alternation (median of `trials`)."""
+    import statistics
+
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import GraphedExecute, build_timeline
+    from .stages import build_layers, build_stages, torch_init
+
+    if name == "config1":
+        tf32 = False if tf32 is None else tf32
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+        data, batch, depth, lr, loss = DeviceBatches(torch, device), BATCH, 4, 1e-4, "softmax_xent"
+
+        def setup(strategy):
+            st = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), depth, torch_init(0, device), device=device)
+            return st, [OptimizerState(OptimizerConfig("adam"), s.param_names, device=device) for s in st]
+        streams = "stage"
+    else:
+        cfg = MODULE_CONFIGS[name]
+        tf32 = True if tf32 is None else tf32
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+        torch.backends.cudnn.allow_tf32 = tf32
+        data, batch, depth, lr, loss = ModuleBatches(torch, device, cfg), cfg["batch"], cfg["depth"], cfg["lr"], \
+            "softmax_xent"
+
+        def setup(strategy):
+            st, opts, _ = _module_setup(torch, device, name, strategy, n_batches)
+            return st, opts
+        streams = cfg.get("single_gpu_streams", "stage")
+    graphs = {}
+    try:
+        for strategy, t in (("gpipe", micros), ("optimizer_prediction", 1)):
+            st, opts = setup(strategy)
+            if streams == "serial" and name != "config1":
+                from .stage_models import use_cudnn_bn
+
+                use_cudnn_bn(st)
+            tl = build_timeline(strategy, depth, n_batches, t)
+            g = GraphedExecute(tl, st, opts, strategy, data, loss, lambda mb: lr, warmup_runs=1, streams=streams)
+            g.replay()
+            torch.cuda.synchronize(device)
+            graphs[strategy] = g
+        times = {s: [] for s in graphs}
+        for _ in range(trials):
+            for s, g in graphs.items():
+                times[s].append(_time_replays(torch, device, g, 1))
+        sps = {s: n_batches * batch / statistics.median(v) for s, v in times.items()}
+        out = {"config": f"{name}: D={depth}, batch {batch}, {n_batches} mini-batches per run, GPipe T={micros} "
+                         f"micro-batches of {batch // micros}; {'TF32' if tf32 else 'fp32'}; one GPU, "
+                         f"{'one stream per stage' if streams == 'stage' else 'stages on one stream'}",
+               "gpipe_samples_per_s": round(sps["gpipe"], 1),
+               "pipeoptim_samples_per_s": round(sps["optimizer_prediction"], 1),
+               "pipeoptim_over_gpipe": round(sps["optimizer_prediction"] / sps["gpipe"], 4),
+               "gpipe_final_loss": graphs["gpipe"].report().losses[-1],
+               "pipeoptim_final_loss": graphs["optimizer_prediction"].report().losses[-1]}
+    finally:
+        graphs = g = st = opts = None  # noqa: F841
+        torch.cuda.empty_cache()
+        torch.backends.cuda.matmul.allow_tf32 = False
+        torch.backends.cudnn.allow_tf32 = False
+    return out

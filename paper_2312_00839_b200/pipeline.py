@@ -73,22 +73,22 @@ def output_link(kind, stage: int, depth: int):
 def exchange_plan(program, stage: int, depth: int) -> list[list[tuple[str, tuple, int]]]:
     """The grouped exchanges PipelineStageRunner.run posts, in posting order:
     group 0 = {recv work[0]'s input}; group i+1 = {send work[i]'s output,
-    recv work[i+1]'s input} — entries ("send" | "recv", link, mb). Every group
+    recv work[i+1]'s input} — entries ("send" | "recv", link, (mb, micro)). Every group
     is one batch_isend_irecv (ncclGroupStart/End); tests/test_nccl_groups.py
     checks that these plans cannot deadlock under NCCL's group semantics."""
     work = [op for op in program if op.kind != UPDATE]
     groups = []
     first = input_link(work[0].kind, stage, depth) if work else None
-    groups.append([("recv", first, work[0].mb)] if first else [])
+    groups.append([("recv", first, (work[0].mb, work[0].micro))] if first else [])
     for i, op in enumerate(work):
         g = []
         out = output_link(op.kind, stage, depth)
         if out:
-            g.append(("send", out, op.mb))
+            g.append(("send", out, (op.mb, op.micro)))
         if i + 1 < len(work):
             nxt = input_link(work[i + 1].kind, stage, depth)
             if nxt:
-                g.append(("recv", nxt, work[i + 1].mb))
+                g.append(("recv", nxt, (work[i + 1].mb, work[i + 1].micro)))
         groups.append(g)
     return groups
 
@@ -356,7 +356,7 @@ class _OpGraphs:
 
 
 class PipelineStageRunner:
-    """Runs one stage's 1F1B program on this rank."""
+    """Runs one stage's 1F1B (or GPipe) program on this rank."""
 
     def __init__(self, dist, tl: Timeline, stage: StageModel, opt, strategy: str, data, loss_kind: str,
                  lr_for_mb, rows: int, *, checks: str = "deferred", fuse: bool = True, group=None,
@@ -367,8 +367,12 @@ class PipelineStageRunner:
         `dp_rank` trains on rows [dp_rank*rows, (dp_rank+1)*rows) of every
         batch and the stage gradient is averaged over `dp_group` before each
         update, so the replicas stay identical."""
-        if STRATEGY_SCHEDULE.get(strategy) != "1f1b" or tl.kind != "1f1b":
-            raise ValueError(f"the distributed runner executes 1f1b strategies, got {strategy!r} on {tl.kind!r}")
+        kind = STRATEGY_SCHEDULE.get(strategy)
+        if kind not in ("1f1b", "gpipe") or tl.kind != kind:
+            raise ValueError(f"the distributed runner executes 1f1b and gpipe strategies, got {strategy!r} "
+                             f"on {tl.kind!r}")
+        if rows % tl.micro_per_mini:
+            raise ValueError(f"{rows} rows do not split into {tl.micro_per_mini} micro-batches")
         if strategy == "spectrain" and opt.config.kind != "sgdm":
             raise ValueError("spectrain requires the sgdm optimizer")
         validate_timeline(tl)
@@ -383,6 +387,10 @@ class PipelineStageRunner:
         self.loss_kind = loss_kind
         self.lr_for_mb = lr_for_mb
         self.rows = rows
+        # GPipe: T micro-batches of rows / T per mini-batch, gradients summed
+        # over them and averaged before the update (runtime.py:441-454)
+        self.micros = tl.micro_per_mini
+        self.mrows = rows // self.micros
         self.eager = checks == "eager"
         self.fuse = fuse
         self.predictive = strategy in PREDICTIVE_STRATEGIES
@@ -405,7 +413,7 @@ class PipelineStageRunner:
         # cost dominates small stages); needs deferred checks, an MLP stage
         # and no data parallelism (those paths run eagerly)
         use_graphs = (graphed and not self.eager and dp_size == 1 and isinstance(stage, StageModel)
-                      and self.device.type == "cuda")
+                      and self.device.type == "cuda" and self.micros == 1)
         self._graphs = _OpGraphs(self) if use_graphs else None
 
     # -- what each op consumes / produces -------------------------------------------------
@@ -415,15 +423,15 @@ class PipelineStageRunner:
         if link is None:
             return None
         if link[0] == "act":
-            return (self.rows, *self.stage.in_shape), self.stage_ranks[self.rank - 1]
-        return (self.rows, *self.stage.out_shape), self.stage_ranks[self.rank + 1]
+            return (self.mrows, *self.stage.in_shape), self.stage_ranks[self.rank - 1]
+        return (self.mrows, *self.stage.out_shape), self.stage_ranks[self.rank + 1]
 
     def run(self) -> StageReport:
         work = [op for op in self.program if op.kind != UPDATE]
         records: dict[int, VersionRecord] = {}
         order: list[VersionRecord] = []
         losses = {} if self.rank == self.depth - 1 else None
-        grads_local: dict[int, torch.Tensor] = {}
+        grads_local: dict[tuple[int, int], torch.Tensor] = {}
         snapshot_peak = 1
         executed = []
         g = self._graphs
@@ -447,7 +455,7 @@ class PipelineStageRunner:
         while i < len(self.program):
             op = self.program[i]
             i += 1
-            executed.append((op.kind, op.mb))
+            executed.append((op.kind, op.mb) if self.micros == 1 else (op.kind, op.mb, op.micro))
             if op.kind == UPDATE:
                 if g is not None:
                     g.update(op)
@@ -464,15 +472,16 @@ class PipelineStageRunner:
                 y = None
                 last = self.rank == self.depth - 1
                 if self.rank == 0:
-                    x = self._shard(_to_device(self.data.batch(op.mb)[0], self.device))
+                    x = self._micro(self._shard(_to_device(self.data.batch(op.mb)[0], self.device)), op.micro)
                 if last:
-                    y = self._shard(_to_device(self.data.batch(op.mb)[1], self.device))
-                weights, fv, predicted, target = self.policy.forward_view(self.rt, op.mb, 0, self.lr_for_mb(op.mb))
+                    y = self._micro(self._shard(_to_device(self.data.batch(op.mb)[1], self.device)), op.micro)
+                weights, fv, predicted, target = self.policy.forward_view(self.rt, op.mb, op.micro,
+                                                                          self.lr_for_mb(op.mb))
                 try:
                     if g is not None:
                         out, loss, grad = g.forward(op, weights, x, y, fv, flags, len(work))
                     else:
-                        out = self.stage.run_forward(weights, (op.mb, 0), x, fv, check_finite=self.eager,
+                        out = self.stage.run_forward(weights, (op.mb, op.micro), x, fv, check_finite=self.eager,
                                                      finite_flags=flags, flag_index=wi)
                         loss = grad = None
                         if last:
@@ -481,27 +490,28 @@ class PipelineStageRunner:
                     raise NumericError(f"mb {op.mb} stage {self.rank}: {err}") from err
                 in_flight += 1
                 peak_in_flight = max(peak_in_flight, in_flight)
-                rec = VersionRecord(op.mb, 0, self.rank, fv, predicted, target)
-                records[op.mb] = rec
+                rec = VersionRecord(op.mb, op.micro, self.rank, fv, predicted, target)
+                records[(op.mb, op.micro)] = rec
                 order.append(rec)
                 if output_link(op.kind, self.rank, self.depth):
                     out_msg = (out if out.is_contiguous() else out.contiguous(), self.stage_ranks[self.rank + 1])
                 else:
                     if self.eager and not bool(torch.isfinite(loss)):
                         raise NumericError(f"mb {op.mb} stage {self.rank}: non-finite loss under {self.loss_kind}")
-                    losses[op.mb] = loss.detach().clone() if g is not None else loss.detach()
-                    grads_local[op.mb] = grad
+                    losses.setdefault(op.mb, []).append(loss.detach().clone() if g is not None else loss.detach())
+                    grads_local[(op.mb, op.micro)] = grad
             else:
-                g_out = grads_local.pop(op.mb) if self.rank == self.depth - 1 else inp
-                rec = records[op.mb]
-                weights, bv = self.policy.backward_view(self.rt, op.mb, 0, rec.forward_version)
+                g_out = grads_local.pop((op.mb, op.micro)) if self.rank == self.depth - 1 else inp
+                rec = records[(op.mb, op.micro)]
+                weights, bv = self.policy.backward_view(self.rt, op.mb, op.micro, rec.forward_version)
                 if g is not None:
                     g_in = g.backward(op, weights, g_out)
                 else:
-                    g_in, _ = self.stage.run_backward(weights, (op.mb, 0), g_out, accumulate=False,
+                    g_in, _ = self.stage.run_backward(weights, (op.mb, op.micro), g_out,
+                                                      accumulate=self.rt.pending_count > 0,
                                                       need_input_grad=self.rank > 0)
                 in_flight -= 1
-                self.rt.pending_count = 1
+                self.rt.pending_count += 1
                 rec.backward_version = bv
                 rec.live_backward_version = self.stage.version
                 if output_link(op.kind, self.rank, self.depth):
@@ -527,7 +537,8 @@ class PipelineStageRunner:
             self.opt.check_finite()
         host_losses = None
         if losses is not None:
-            vals = torch.stack([losses[m] for m in sorted(losses)]).cpu().tolist()
+            vals = torch.stack([torch.stack(losses[m]).mean() if len(losses[m]) > 1 else losses[m][0]
+                                for m in sorted(losses)]).cpu().tolist()
             host_losses = vals
             if not all(v == v and abs(v) != float("inf") for v in vals):
                 raise NumericError(f"stage {self.rank}: non-finite loss under {self.loss_kind}")
@@ -537,12 +548,19 @@ class PipelineStageRunner:
         return StageReport(self.rank, order, host_losses, self.stage.version, stash_peak,
                            snapshot_peak, time.perf_counter() - t0, executed)
 
+    def _micro(self, t, micro: int):
+        if self.micros == 1:
+            return t
+        return t[micro * self.mrows : (micro + 1) * self.mrows]
+
     def _shard(self, t):
         if self.dp_size == 1:
             return t
         return t[self.dp_rank * self.rows : (self.dp_rank + 1) * self.rows]
 
     def _update(self, op):
+        if self.rt.pending_count > 1:  # GPipe: mean over the micro-batches (runtime.py:441-454)
+            self.stage.flat.grad.div_(self.rt.pending_count)
         if self.fused_dp is not None:
             lr = self.lr_for_mb(op.mb)
             if self.fuse and op.fuse_predict:
@@ -637,6 +655,39 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
     gon, goff = out["graphed_pred_on"]["samples_per_s"], out["graphed_pred_off"]["samples_per_s"]
     out.update(value=max(on, gon), unit="samples/s", prediction_overhead=round(1.0 - on / off, 4),
                graphed_prediction_overhead=round(1.0 - gon / goff, 4), launches=n_batches * 2)
+    # GPipe on the same stages and GPUs (T = 4 micro-batches, eager NCCL runner)
+    try:
+        times = []
+        for trial in range(2):
+            stage = StageModel(rank, partition_layers(layers, world)[rank], torch_init(0, device), device)
+            opt = OptimizerState(OptimizerConfig("adam"), stage.param_names, device=device)
+            nb = n_batches if trial else 2
+            tl = build_timeline("gpipe", world, nb, 4)
+            runner = PipelineStageRunner(dist, tl, stage, opt, "gpipe", data, "softmax_xent", lambda mb: 1e-4, BATCH,
+                                         host_staging=host_staging)
+            torch_mod.cuda.synchronize(device)
+            dist.barrier()
+            e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
+            e0.record()
+            runner.run()
+            e1.record()
+            torch_mod.cuda.synchronize(device)
+            dist.barrier()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        t = torch_mod.tensor([times[-1]], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["gpipe_t4"] = {"samples_per_s": round(n_batches * BATCH / float(t.item()), 1), "s": round(float(t.item()), 4)}
+        out["pipeoptim_over_gpipe"] = round(on / out["gpipe_t4"]["samples_per_s"], 4)
+    except Exception as exc:
+        out["gpipe_t4"] = {"error": f"rank {rank}: {type(exc).__name__}: {exc}"}
+    # counted-work bound for one stage per GPU (roofline.py)
+    from .roofline import mlp_pipeline_bounds
+    from .stages import build_stages
+
+    cpu_stages = build_stages(layers, world, torch_init(0, torch_mod.device("cpu")), device="cpu")
+    bound = mlp_pipeline_bounds(cpu_stages, BATCH, n_batches, "adam", True, "fast_fp32")
+    out["roofline"] = {"one_stage_per_gpu": bound["one_stage_per_gpu"], "per_stage": bound["per_stage"],
+                       "peak_source": bound["peak_source"]}
     # the peer-memory transport: a rank's whole run is one CUDA graph (no NCCL,
     # no host in the loop); reported beside the NCCL runner and, when faster,
     # as the value
@@ -657,6 +708,7 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
 
         traceback.print_exc(file=sys.stderr)
         out["peer_graphed"] = {"error": f"rank {rank}: {type(exc).__name__}: {exc}"}
+    out["frac_of_roofline"] = round(out["value"] / bound["one_stage_per_gpu"]["samples_per_s"], 4)
     return out
 
 

@@ -40,7 +40,6 @@ def main():
     if a.shape:
         b, c, u, ca = (int(x) for x in a.shape.split(","))
         la = ctypes.byref(_lib.make_launch(b, c, 8, ca, u))
-    st = torch.cuda.current_stream()
     rows = []
     for lg in (int(x) for x in a.sizes.split(",")):
         n = 1 << lg
@@ -59,6 +58,7 @@ def main():
             hp = ctypes.byref(OptimizerConfig(kind).hparams())
             for kernel in a.kernels.split(","):
                 def one(b):
+                    st = torch.cuda.current_stream()  # the capture stream inside torch.cuda.graph
                     v = None if kind == "sgdm" else b["v"].data_ptr()
                     if kernel == "predict":
                         rc = lib.po_predict(hp, b["w"].data_ptr(), b["m"].data_ptr(), v, b["o"].data_ptr(), n,

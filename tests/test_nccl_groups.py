@@ -21,12 +21,12 @@ import random
 import pytest
 
 from paper_2312_00839_b200.pipeline import exchange_plan
-from paper_2312_00839_b200.schedule import build_1f1b, stage_program
+from paper_2312_00839_b200.schedule import build_1f1b, build_gpipe, stage_program
 
 
-def _plans(depth, n):
-    tl = build_1f1b(depth, n)
-    return [exchange_plan(stage_program(tl, k), k, depth) for k in range(depth)]
+def _plans(depth, n, micros=None):
+    tl = build_1f1b(depth, n) if micros is None else build_gpipe(depth, n, micros)
+    return [exchange_plan(stage_program(tl, k, predictive=micros is None), k, depth) for k in range(depth)]
 
 
 def _simulate(plans, seed):
@@ -87,6 +87,15 @@ def test_nccl_posting_order_never_deadlocks(depth):
             assert _simulate(plans, seed), (depth, n, seed)
 
 
+@pytest.mark.parametrize("depth", [2, 4, 8])
+@pytest.mark.parametrize("micros", [1, 2, 4])
+def test_gpipe_posting_order_never_deadlocks(depth, micros):
+    for n in (1, 2, 5):
+        plans = _plans(depth, n, micros)
+        for seed in range(4):
+            assert _simulate(plans, seed), (depth, micros, n, seed)
+
+
 def test_every_message_is_sent_and_received_once():
     for depth in (2, 4, 8):
         for n in (1, 5, 19):
@@ -104,10 +113,11 @@ def test_every_message_is_sent_and_received_once():
 def test_simulator_detects_a_crossed_order():
     """Sanity of the model: two ranks that both send first to each other in
     separate groups before receiving deadlock under rendezvous."""
-    a = [[("send", ("act", 0), 1)], [("recv", ("grad", 0), 1)]]
-    b = [[("send", ("grad", 0), 1)], [("recv", ("act", 0), 1)]]
+    m = (1, 0)
+    a = [[("send", ("act", 0), m)], [("recv", ("grad", 0), m)]]
+    b = [[("send", ("grad", 0), m)], [("recv", ("act", 0), m)]]
     assert not _simulate([a, b], 0)
     # the runner's pairing ({send a, recv g} vs {send g, recv a}) completes
-    a2 = [[("send", ("act", 0), 1), ("recv", ("grad", 0), 1)]]
-    b2 = [[("send", ("grad", 0), 1), ("recv", ("act", 0), 1)]]
+    a2 = [[("send", ("act", 0), m), ("recv", ("grad", 0), m)]]
+    b2 = [[("send", ("grad", 0), m), ("recv", ("act", 0), m)]]
     assert _simulate([a2, b2], 0)

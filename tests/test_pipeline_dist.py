@@ -246,3 +246,70 @@ def test_gloo_module_stages_pipeline(tmp_path):
     want = sorted([[r[0], r[2], r[3], r[4], r[5], r[6], r[7]] for r in ref["records"]])
     assert got["records"] == want
     assert len(got["losses"]) == n and all(np.isfinite(got["losses"]))
+
+
+GOLDEN_GPIPE = [c for c in json.loads((Path(__file__).resolve().parent / "golden" / "runtime_golden.json").read_text())
+                if c["strategy"] == "gpipe"]
+
+
+class GoldenSrc:
+    """The golden runs' batches (pkg/tests/test_runtime.py:22-31 seeding)."""
+
+    def __init__(self, case):
+        self.c = case
+
+    def batch(self, mb):
+        s = rng_ref.Stream(self.c["data_seed"], f"batch-{mb}")
+        return s.normal(self.c["rows"], self.c["dims"][0]), s.normal(self.c["rows"], self.c["dims"][-1])
+
+
+def _gpipe_worker(rank, world, port, case, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.pipeline import PipelineStageRunner, gather_reports
+        from paper_2312_00839_b200.runtime import build_timeline
+        from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+        layers = build_layers(case["dims"], case["acts"])
+        stage = StageModel(rank, partition_layers(layers, world)[rank],
+                           lambda sp: rng_ref.layer_init(case["init_seed"], sp.index, sp.in_dim, sp.out_dim), "cpu")
+        opt = StandInOptimizer(case["kind"], stage.param_names)
+        tl = build_timeline("gpipe", world, case["n"], case["micros"])
+        runner = PipelineStageRunner(dist, tl, stage, opt, "gpipe", GoldenSrc(case), "mse",
+                                     lambda mb, lr=case["lr"]: lr, case["rows"])
+        rep = runner.run()
+        reps = gather_reports(dist, rep, world)
+        if rank == 0:
+            Path(out_dir, "out.json").write_text(json.dumps({
+                "records": sorted([[r.mb, r.micro, r.stage, r.forward_version, r.predicted, r.prediction_target,
+                                    r.backward_version, r.live_backward_version] for rp in reps for r in rp.records]),
+                "executed": [[list(e) for e in rp.executed] for rp in reps],
+                "losses": reps[-1].losses, "versions": [rp.final_version for rp in reps]}))
+        params = [p.detach().double().numpy().tolist() for p in stage.params]
+        Path(out_dir, f"params{rank}.json").write_text(json.dumps(params))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", GOLDEN_GPIPE, ids=lambda c: f"D{c['depth']}-T{c['micros']}-{c['kind']}")
+def test_gloo_gpipe_matches_reference_golden(tmp_path, case):
+    """§8(f)#2 on the distributed runner: GPipe (T micro-batches, gradients
+    averaged over them before the update, runtime.py:441-454) over gloo at
+    world = D against fixtures made by the reference's own execute."""
+    world = case["depth"]
+    mp.spawn(_gpipe_worker, args=(world, free_port(), case, str(tmp_path)), nprocs=world, join=True)
+    got = json.loads((tmp_path / "out.json").read_text())
+    assert got["records"] == sorted(case["records"])
+    from paper_2312_00839_b200.runtime import build_timeline
+
+    tl = build_timeline("gpipe", world, case["n"], case["micros"])
+    for k in range(world):
+        want = [(e.kind, e.mb) if case["micros"] == 1 else (e.kind, e.mb, e.micro) for e in tl.stage_events(k)]
+        assert [tuple(e) for e in got["executed"][k]] == want
+    assert got["versions"] == case["final_versions"]
+    assert np.allclose(got["losses"], case["losses"], rtol=1e-4, atol=1e-6)
+    for k in range(world):
+        params = json.loads((tmp_path / f"params{k}.json").read_text())
+        for p, want in zip(params, case["params"][k]):
+            assert optim_ref.inf_norm_rel(np.array(p), np.array(want)) <= 1e-4
