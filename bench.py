@@ -208,6 +208,55 @@ def cpu_pipeline_baseline(n_batches: int = 24, strategy: str = "optimizer_predic
                        f"optimizer elementwise single-threaded as in the reference")}
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_numpy_optimizer(kind: str, logs=(20, 22, 24, 26)):
+    """The reference's own call sequence restated in numpy float64
+    (oracle/optim_ref.py <- pipesim optim.py:63-155): OptimizerState.step,
+    then prediction_direction + predict_weights for the next forward, on one
+    (N,) parameter, N = 2^20 .. 2^26. numpy's elementwise
+    ufuncs are single-threaded, as in the reference. Best of 2 after a warm-up."""
+    import numpy as np
+
+    from oracle import optim_ref
+
+    rows = []
+    for lg in logs:
+        n = 1 << lg
+        rng = np.random.default_rng(lg)
+        w = rng.normal(0, 0.02, n)
+        opt = optim_ref.OracleOptimizer(optim_ref.Hyper(kind), ["w"])
+
+        def call(w):
+            (nw,), _ = opt.step([w], [rng.normal(0, 1e-2, n)], 1e-3)
+            (wh,) = optim_ref.predict_weights([nw], 1e-3, 3, opt.prediction_direction([nw]))
+            return nw, wh
+
+        w, _ = call(w)
+        best = float("inf")
+        for _ in range(2):
+            g_t = time.perf_counter()
+            rng.normal(0, 1e-2, n)  # the gradient draw, subtracted below
+            gen = time.perf_counter() - g_t
+            t0 = time.perf_counter()
+            w, _ = call(w)
+            best = min(best, time.perf_counter() - t0 - gen)
+        rows.append({"n": n, "ms": round(best * 1e3, 2), "ns_per_param": round(best / n * 1e9, 2),
+                     "gbs_equiv": round(BYTES_PER_PARAM[kind] * n / best / 1e9, 3)})
+        del w, opt
+    return {"cpu": cpu_model(), "threads": 1, "kind": kind,
+            "path": "oracle/optim_ref.py OracleOptimizer.step + prediction_direction + predict_weights "
+                    "(numpy float64, the reference's evaluation order)", "sizes": rows}
+
+
 def reference_arm(args):
     """--impl reference: the reference's algorithm for this path on the host
     cores (the oracle's C port, float64 like the reference, OpenMP on every
@@ -260,6 +309,11 @@ def reference_arm(args):
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "vs_baseline": None,
     }
+    line["cpu_baseline"]["cpu"] = cpu_model()
+    try:
+        line["numpy_reference_path"] = cpu_numpy_optimizer(args.kind)
+    except Exception as exc:
+        line["numpy_reference_path"] = {"error": f"{type(exc).__name__}: {exc}"}
     try:
         line["pipeline"] = {
             "pred_on": cpu_pipeline_baseline(strategy="optimizer_prediction"),

@@ -228,6 +228,12 @@ int po_relu_bwd_bias(const float* g, int32_t splits, const float* h, int64_t row
 int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols,
                     float* dpre, float* db, int32_t accumulate, void* stream);
 
+/* Invalidate the L2 lines of a dead buffer without writing them back
+ * (discard.global.L2 on every whole 128-byte line inside [p, p + bytes)):
+ * the memory contents become unspecified. For a staging buffer after the
+ * forward that consumed it, or a gradient after the update that consumed it. */
+int po_l2_discard(void* p, int64_t bytes, void* stream);
+
 /* ---- FP32-accurate tensor-core GEMM (pipeoptim_gemm.cu) -----------------
  * D[l] = A[l] @ B[l] for l < batch, fp32 in/out, computed by tcgen05 UMMA with
  * each fp32 operand split into three bf16 pieces (CUTLASS SM100 fast-FP32

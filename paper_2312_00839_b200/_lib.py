@@ -33,6 +33,7 @@ EXPORTS = (
     "po_predict_dc",
     "po_step_predict_dc",
     "po_all_finite",
+    "po_l2_discard",
     "po_loss_grad",
     "po_relu_bwd_bias",
     "po_splitk_bias_act",
@@ -115,6 +116,7 @@ _SIGNATURES = {
     "po_step_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _I64, _P, _P, _LA, _P]),
     "po_predict_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _I64, _P, _LA, _P]),
     "po_step_predict_dc": (ctypes.c_int, [_HP, _P, _P, _P, _P, _P, _I64, _P, _P, _LA, _P]),
+    "po_l2_discard": (ctypes.c_int, [_P, _I64, _P]),
     "po_all_finite": (ctypes.c_int, [_P, _I64, _P, _I64, _P]),
     "po_loss_grad": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, _I64, _P, _P, _P, _P]),
     "po_relu_bwd_bias": (ctypes.c_int, [_P, ctypes.c_int32, _P, _I64, _I64, _P, _P, ctypes.c_int32, _P]),

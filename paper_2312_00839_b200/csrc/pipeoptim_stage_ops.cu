@@ -257,6 +257,35 @@ extern "C" {
 int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h, int64_t rows, int64_t cols,
                     float* dpre, float* db, int32_t accumulate, void* stream);
 
+// Invalidate the L2 lines of a dead buffer WITHOUT writing them back
+// (discard.global.L2): a predicted-weights staging buffer after the forward
+// that consumed it, or a gradient after the update that consumed it, would
+// otherwise cost an HBM write-back of data nobody reads again. Only whole
+// 128-byte lines inside [p, p + bytes) are discarded; their memory contents
+// become unspecified.
+__global__ void l2_discard_kernel(char* base, int64_t lines) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < lines; i += stride)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + i * 128) : "memory");
+}
+
+int po_l2_discard(void* p, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && p == nullptr)) return PO_EINVAL;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t lo = (a + 127) & ~uintptr_t(127);
+  const uintptr_t hi = (a + (uintptr_t)bytes) & ~uintptr_t(127);
+  if (hi <= lo) return 0;
+  const int64_t lines = (int64_t)((hi - lo) / 128);
+  static int sms = 0;
+  if (sms == 0) sms = sm_count_ops();
+  const int block = 256;
+  int64_t grid = (lines + block - 1) / block;
+  if (grid > 4 * sms) grid = 4 * sms;
+  l2_discard_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(reinterpret_cast<char*>(lo), lines);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
 int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void* stream) {
   if (n < 0 || flags == nullptr || index < 0 || (n > 0 && x == nullptr)) return PO_EINVAL;
   if (n == 0) return 0;

@@ -125,6 +125,8 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-flush", action="store_true", help="warm L2 (pipeline-like) instead of flushing")
     ap.add_argument("--tune-small", action="store_true", help="launch-shape search at 2^20..2^24")
+    ap.add_argument("--s-sweep", action="store_true",
+                    help="K1/K3 x kinds at s = 1..7 (BASELINE configs[4]) at the first --sizes entry")
     args = ap.parse_args()
     global FLUSH
     FLUSH = not args.no_flush
@@ -132,7 +134,30 @@ def main():
     peak = peak_gbs()
     rows = []
     print(f"# device {torch.cuda.get_device_name()}  measured copy peak {peak} GB/s", flush=True)
-    if args.tune_small:
+    if args.s_sweep:
+        sz = args.sizes.split(",")[0]
+        n = int(1e9) if sz == "e9" else 1 << int(sz)
+        b = Buffers(n)
+        for kind in args.kinds.split(","):
+            for kernel in ("predict", "step_predict"):
+                for s_ in range(1, 8):
+                    stream = torch.cuda.current_stream()
+                    call(lib, kernel, kind, b, None, stream.cuda_stream, s=s_)
+                    times = []
+                    for _ in range(args.reps):
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(stream)
+                        call(lib, kernel, kind, b, None, stream.cuda_stream, s=s_)
+                        e1.record(stream)
+                        e1.synchronize()
+                        times.append(e0.elapsed_time(e1) / 1e3)
+                    med = statistics.median(times)
+                    gbs = BYTES[(kernel, kind)] * n / med / 1e9
+                    row = dict(n=n, kind=kind, kernel=kernel, s=s_, ms_median=round(med * 1e3, 4), gbs=round(gbs, 1),
+                               frac_of_measured=round(gbs / peak, 4))
+                    rows.append(row)
+                    print(json.dumps(row), flush=True)
+    elif args.tune_small:
         shapes = [(512, 1, 1), (512, 2, 1), (512, 4, 1), (256, 8, 1), (256, 4, 2), (128, 16, 1), (512, 2, 2),
                   (256, 8, 2), (128, 16, 2), (256, 6, 1), (128, 8, 1), (128, 8, 2), (128, 8, 4), (256, 4, 4),
                   (512, 2, 4), (512, 1, 4), (256, 2, 4)]
