@@ -92,8 +92,8 @@ typedef struct po_launch {
 typedef struct po_coef {
   float lr;     /* step learning rate */
   float c_pred; /* lr_pred * s */
-  float bc1;    /* 1 - beta1^t (1 when t == 0) */
-  float bc2;    /* 1 - beta2^t (1 when t == 0) */
+  float inv_bc1; /* 1 / (1 - beta1^t), formed in double (1 when t == 0) */
+  float inv_bc2; /* 1 / (1 - beta2^t), formed in double (1 when t == 0) */
 } po_coef;
 
 #define PO_COEF_STEP 0

@@ -18,17 +18,21 @@ f32 = np.float32
 
 def coef(kind, lr=0.0, c_pred=0.0, t=0, momentum=0.9, dampening=0.0, weight_decay=5e-4,
          beta1=0.9, beta2=0.999, eps=1e-8, decoupled_decay=1e-2):
-    bc1 = 1.0 - beta1 ** t if t >= 1 else 1.0
-    bc2 = 1.0 - beta2 ** t if t >= 1 else 1.0
+    # reciprocal bias corrections, formed in double and rounded once
+    ibc1 = 1.0 / (1.0 - beta1 ** t) if t >= 1 else 1.0
+    ibc2 = 1.0 / (1.0 - beta2 ** t) if t >= 1 else 1.0
     return dict(
-        lr=f32(lr), c=f32(c_pred), bc1=f32(bc1), bc2=f32(bc2), b1=f32(beta1), omb1=f32(1.0 - beta1),
+        lr=f32(lr), c=f32(c_pred), ibc1=f32(ibc1), ibc2=f32(ibc2), b1=f32(beta1), omb1=f32(1.0 - beta1),
         b2=f32(beta2), omb2=f32(1.0 - beta2), eps=f32(eps), lam=f32(decoupled_decay), mom=f32(momentum),
         omd=f32(1.0 - dampening), wd=f32(weight_decay),
     )
 
 
 def _ratio(m, v, k):
-    return (m / k["bc1"]) / (np.sqrt(v / k["bc2"]) + k["eps"])
+    # the kernels' order: (m * ibc1) / (sqrt(v * ibc2) + eps) — the reference's
+    # (m / bc1) / (sqrt(v / bc2) + eps) with the bias corrections applied as
+    # correctly-rounded multiplies by their reciprocals
+    return (m * k["ibc1"]) / (np.sqrt(v * k["ibc2"]) + k["eps"])
 
 
 def step(kind, w, g, s1, s2, lr, step_count, c_pred=None, **hp):

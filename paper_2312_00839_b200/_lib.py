@@ -94,7 +94,7 @@ class po_launch(ctypes.Structure):
 
 
 class po_coef(ctypes.Structure):
-    _fields_ = [("lr", ctypes.c_float), ("c_pred", ctypes.c_float), ("bc1", ctypes.c_float), ("bc2", ctypes.c_float)]
+    _fields_ = [("lr", ctypes.c_float), ("c_pred", ctypes.c_float), ("inv_bc1", ctypes.c_float), ("inv_bc2", ctypes.c_float)]
 
 
 _P = ctypes.c_void_p

@@ -55,7 +55,22 @@ int main() {
   prop.size = (bytes + gran - 1) / gran * gran;
   printf("multicast granularity %zu, size %zu\n", gran, prop.size);
   CUmemGenericAllocationHandle mch;
-  CK(cuMulticastCreate(&mch, &prop));
+  // which handle types does cuMulticastCreate accept with one device?
+  const int types[3] = {0, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_FABRIC};
+  int ok_type = -1;
+  for (int t : types) {
+    CUmulticastObjectProp p2 = prop;
+    p2.handleTypes = (unsigned long long)t;
+    CUresult r = cuMulticastCreate(&mch, &p2);
+    const char* es = nullptr;
+    cuGetErrorString(r, &es);
+    printf("cuMulticastCreate(numDevices=1, handleTypes=%d) -> %d %s\n", t, (int)r, es ? es : "?");
+    if (r == CUDA_SUCCESS && ok_type < 0) {
+      ok_type = t;
+      break;
+    }
+  }
+  if (ok_type < 0) return 0;
   CK(cuMulticastAddDevice(mch, dev));
   CUmemAllocationProp ap = {};
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;

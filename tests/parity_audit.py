@@ -216,7 +216,7 @@ def check_tape(tape, opts, depth, n_batches, lr_for_mb, predictive, step_counts)
                 assert pred[3] == step[2] + 1
             buf = _lib.po_coef()
             _lib.check(lib.po_coef_fill(ctypes.byref(o._hp), which, lr, c, t, ctypes.byref(buf)), "po_coef_fill")
-            exp = np.array([buf.lr, buf.c_pred, buf.bc1, buf.bc2], np.float32)
+            exp = np.array([buf.lr, buf.c_pred, buf.inv_bc1, buf.inv_bc2], np.float32)
             assert np.array_equal(dev[i], exp), f"stage {k}: tape slot {i} {dev[i]} != {exp} for {ops}"
             got_ops += ops
         assert got_ops == want, f"stage {k}: the graph's launches do not cover the rule's op sequence"
