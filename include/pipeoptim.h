@@ -81,7 +81,9 @@ typedef struct po_launch {
   int32_t cache;        /* 0 = tuned default, 1 = streaming .cs, 2 = L1::no_allocate
                            loads, 3 = plain ld/st, 4 = mixed (W / W_hat plain,
                            gradient and state streaming) */
-  int32_t unroll;       /* vectors per stream in flight per thread: 1, 2, 4; 0 = default */
+  int32_t unroll;       /* vectors per stream in flight per thread: 1, 2, 4; 3 = one vector
+                           per stream with the next one prefetched (software
+                           pipeline); 0 = default */
 } po_launch;
 
 /* One launch's step-dependent fp32 scalars, for graph-captured launches

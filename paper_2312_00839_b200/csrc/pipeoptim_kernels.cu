@@ -205,7 +205,11 @@ __host__ __device__ constexpr int pol(int cache, int stream) {
 // is correctly rounded; vs the float64 reference the direction moves by
 // <= ~3 ulp, far inside the 1e-6 contract.
 __device__ __forceinline__ float adam_dir(float m, float v, const Coef& c) {
+#ifdef PO_PROBE_ADAM_DIV3  // timing probe only (scripts/adam_dir_ab.py): the round-1 three-division cost
+  return __fdiv_rn(__fdiv_rn(m, c.ibc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, c.ibc2)), c.eps));
+#else
   return __fdiv_rn(__fmul_rn(m, c.ibc1), __fadd_rn(__fsqrt_rn(__fmul_rn(v, c.ibc2)), c.eps));
+#endif
 }
 
 // One element. w/s1/s2 are updated in place for step modes; `out` receives
@@ -280,6 +284,9 @@ __device__ __forceinline__ void do_vec(const Args& a, const Coef& c, int64_t vi,
   if constexpr (writes_out(MODE)) vstore<VEC, pol(CACHE, S_OUT)>(a.out + base, out);
 }
 
+// UNROLL code for the software-pipelined loop (po_launch.unroll = 3)
+constexpr int kPrefetch = 3;
+
 // Persistent grid-stride stream. Each thread issues UNROLL independent vector
 // loads per stream before the first use (memory-level parallelism: Little's law
 // at ~6.5 TB/s x ~0.8 us needs ~5 MB in flight chip-wide, ~35 KB per SM).
@@ -292,10 +299,49 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
   int64_t i = tid;
   const Coef c = load_coef(a);
 
-  for (; i + (UNROLL - 1) * stride < nv; i += UNROLL * stride) {
-    Vec<VEC> w[UNROLL], g[UNROLL], s1[UNROLL], s2[UNROLL], out[UNROLL];
+  if constexpr (UNROLL == kPrefetch) {
+    // Software pipeline: the next grid-stride vector's loads are issued before
+    // this vector's arithmetic and stores, so one vector per stream stays in
+    // flight while the (division + square-root) math of the current one runs.
+    // The elements a thread touches are its own (disjoint grid-stride
+    // partition), so hoisting the next loads above the current stores is safe.
+    Vec<VEC> w{}, g{}, s1{}, s2{};
+    auto load = [&](int64_t vi, Vec<VEC>& w_, Vec<VEC>& g_, Vec<VEC>& s1_, Vec<VEC>& s2_) {
+      const int64_t base = vi * VEC;
+      if constexpr (uses_w(MODE)) w_ = vload<VEC, pol(CACHE, S_W), !writes_w(MODE)>(a.w + base);
+      if constexpr (uses_g(MODE)) g_ = vload<VEC, pol(CACHE, S_G), true>(a.g + base);
+      if constexpr (uses_s1(MODE)) s1_ = vload<VEC, pol(CACHE, S_STATE), !writes_state(MODE)>(a.s1 + base);
+      if constexpr (uses_s2(KIND, MODE)) s2_ = vload<VEC, pol(CACHE, S_STATE), !writes_state(MODE)>(a.s2 + base);
+    };
+    if (i < nv) load(i, w, g, s1, s2);
+    for (; i < nv; i += stride) {
+      const int64_t base = i * VEC;
+      Vec<VEC> nw{}, ng{}, ns1{}, ns2{}, out;
+      if (i + stride < nv) load(i + stride, nw, ng, ns1, ns2);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+      for (int j = 0; j < VEC; ++j) {
+        bool e = false;
+        elem<KIND, MODE>(c, w.v[j], g.v[j], s1.v[j], s2.v[j], out.v[j], e);
+        if (e && bad == INT64_MAX) bad = base + j;
+      }
+      if constexpr (writes_w(MODE)) vstore<VEC, pol(CACHE, S_W)>(a.w + base, w);
+      if constexpr (writes_state(MODE)) {
+        vstore<VEC, pol(CACHE, S_STATE)>(a.s1 + base, s1);
+        if constexpr (KIND != PO_SGDM) vstore<VEC, pol(CACHE, S_STATE)>(a.s2 + base, s2);
+      }
+      if constexpr (writes_out(MODE)) vstore<VEC, pol(CACHE, S_OUT)>(a.out + base, out);
+      w = nw;
+      g = ng;
+      s1 = ns1;
+      s2 = ns2;
+    }
+  }
+
+  for (; UNROLL != kPrefetch && i + (UNROLL - 1) * stride < nv; i += UNROLL * stride) {
+    constexpr int U = UNROLL == kPrefetch ? 1 : UNROLL;
+    Vec<VEC> w[U], g[U], s1[U], s2[U], out[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
       const int64_t base = (i + u * stride) * VEC;
       if constexpr (uses_w(MODE)) w[u] = vload<VEC, pol(CACHE, S_W), !writes_w(MODE)>(a.w + base);
       if constexpr (uses_g(MODE)) g[u] = vload<VEC, pol(CACHE, S_G), true>(a.g + base);
@@ -303,7 +349,7 @@ __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
       if constexpr (uses_s2(KIND, MODE)) s2[u] = vload<VEC, pol(CACHE, S_STATE), !writes_state(MODE)>(a.s2 + base);
     }
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < U; ++u) {
       const int64_t base = (i + u * stride) * VEC;
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
@@ -379,6 +425,7 @@ cudaError_t launch_unroll(const Args& a, const Shape& sh, dim3 grid, dim3 block,
   if constexpr (tunable(MODE) && VEC > 1) {
     switch (sh.unroll) {
       case 1: po_stream_kernel<KIND, MODE, VEC, CACHE, 1><<<grid, block, 0, s>>>(a); break;
+      case kPrefetch: po_stream_kernel<KIND, MODE, VEC, CACHE, kPrefetch><<<grid, block, 0, s>>>(a); break;
       case 4: po_stream_kernel<KIND, MODE, VEC, CACHE, 4><<<grid, block, 0, s>>>(a); break;
       default: po_stream_kernel<KIND, MODE, VEC, CACHE, 2><<<grid, block, 0, s>>>(a); break;
     }
@@ -452,13 +499,23 @@ DefaultShape default_shape(int kind, int mode, int64_t n) {
   // shape for K1 and K3 (SGDM and Adam) at 2^20 / 2^22 / 2^24 in the L2-flushed
   // round-2 sweep (profiles/r2_kernel_tune_small.jsonl): K1 Adam at 2^24
   // 53.3 -> 45.1 us (0.77 -> 0.91 of copy), at 2^22 20.5 -> 16.4 us
+  // (the prefetching loop is faster for K3 Adam alone at 2^24, 6,362 ->
+  // 6,518 GB/s L2-flushed, profiles/r2_ab_small.jsonl, but costs config 1's
+  // 1F1B run 3 % with prediction on, where K3 shares the GPU with the other
+  // stages' GEMMs: not adopted)
   if (n < (int64_t(1) << 25)) return DefaultShape{128, 16, 1, 1};
+  // >= 2^25: re-tuned at 1e9 with the one-division Adam direction
+  // (profiles/r2_tune_1e9.jsonl, all shapes timed in alternation on one box):
+  // K3 Adam 320 threads x 1 CTA/SM with the next vector prefetched 6,543 GB/s
+  // (512 x 1, one vector in flight: 6,244); K2 Adam 512 x 1, one vector in
+  // flight 6,623 (512 x 1 x 2 plain: 6,228). More requests in flight than
+  // these is slower: the DRAM sees finer read/write interleaving.
   switch (mode) {
     case MODE_PREDICT: return sg ? DefaultShape{256, 8, 2, 1} : DefaultShape{512, 2, 1, 1};
-    case MODE_STEP: return sg ? DefaultShape{512, 1, 1, 1} : DefaultShape{512, 1, 2, 0};
+    case MODE_STEP: return sg ? DefaultShape{512, 1, 1, 1} : DefaultShape{512, 1, 1, 1};
     case MODE_STEP_PREDICT:
       if (sg) return DefaultShape{384, 1, 1, 1};
-      return DefaultShape{512, 1, 1, 1};  // Adam and AdamW (2^30 re-tune: AdamW 6,549 GB/s vs 6,270 before)
+      return DefaultShape{320, 1, 3, 1};  // Adam and AdamW
     default: return DefaultShape{256, 4, 2, 1};
   }
 }
@@ -475,7 +532,7 @@ int run(int kind, int mode, Args a, const po_launch* L, cudaStream_t s) {
   if (L && L->cache == 3) cache = 0;  // explicit plain ld/st request
   int unroll = (L && L->unroll > 0) ? L->unroll : d.unroll;
   if (block % 32 != 0 || block > 512) return PO_EINVAL;
-  if (unroll != 1 && unroll != 2 && unroll != 4) return PO_EINVAL;
+  if (unroll != 1 && unroll != 2 && unroll != 4 && unroll != kPrefetch) return PO_EINVAL;
   if (vec != 8 && vec != 4 && vec != 1) return PO_EINVAL;
   // fall back to narrower vectors when any stream is misaligned
   const void* ptrs[5] = {a.w, a.g, a.s1, a.s2, a.out};
@@ -884,7 +941,10 @@ static int step_predict_dp_impl(const po_hparams* hp, float* w, const float* con
   while (vec > 1 && !all_aligned(vec * 4)) vec = vec == 8 ? 4 : 1;
   // K3's launch shape for this size (block x CTAs/SM); one vector per stream
   // in flight, dp of them for the gradient
-  const DefaultShape ds = default_shape(hp->kind, MODE_STEP_PREDICT, n);
+  // (large sizes: 512 x 1 CTA/SM, the shape the dp = 1 kernel matches K3 with
+  // under ncu, profiles/r2_dp_kernel_dp1_2p28_ncu.csv; no prefetch variant here)
+  const DefaultShape ds = n < (int64_t(1) << 25) ? default_shape(hp->kind, MODE_STEP_PREDICT, n)
+                                                 : DefaultShape{512, 1, 1, 1};
   const int block = ds.block;
   const int64_t nv = n / vec;
   int64_t want = (nv + block - 1) / block;

@@ -203,7 +203,7 @@ def test_fused_equals_unfused_bitwise(lib, kind):
 
 @pytest.mark.parametrize("vec", [1, 4, 8])
 @pytest.mark.parametrize("cache", [1, 2, 3, 4])
-@pytest.mark.parametrize("unroll", [1, 2, 4])
+@pytest.mark.parametrize("unroll", [1, 2, 3, 4])
 def test_launch_shapes_bit_identical(lib, vec, cache, unroll):
     """Every launch shape computes the same bits (the arithmetic is shape-free)."""
     import torch
@@ -223,6 +223,35 @@ def test_launch_shapes_bit_identical(lib, vec, cache, unroll):
                                    3, None, launch(block, cps, vec, cache, unroll), stream()) == 0
         assert torch.equal(o_ref, o_got)
         assert torch.equal(ref[0], got[0])
+
+
+@pytest.mark.parametrize("kind", ["sgdm", "adam", "adamw"])
+@pytest.mark.parametrize("n", [1, 9, 8 * 320 * 148 + 13, (1 << 20) + 7])
+def test_prefetch_loop_all_kernels_bit_identical(lib, kind, n):
+    """The software-pipelined loop (po_launch.unroll = 3, the K3 Adam default
+    at >= 2^25 and below 2^25) == the one-vector loop for K1, K2 and K3, with
+    odd grids whose threads own 0, 1 or several vectors plus a scalar tail."""
+    import torch
+
+    H = ctypes.byref(hp(kind))
+    w, g, s1, s2 = make_inputs(kind, n, 3, seed=11)
+    s2p = (lambda t: None) if kind == "sgdm" else (lambda t: t.data_ptr())
+    for block, cps in ((320, 1), (128, 16), (96, 3)):
+        outs = []
+        for unroll in (1, 3):
+            b = [dev(x) for x in (w, g, s1, s2)]
+            o1 = torch.empty(n, device="cuda")
+            o3 = torch.empty(n, device="cuda")
+            la = launch(block, cps, 8, 1, unroll)
+            assert lib.po_predict(H, b[0].data_ptr(), b[2].data_ptr(), s2p(b[3]), o1.data_ptr(), n, 3e-3, 4, la,
+                                  stream()) == 0
+            assert lib.po_step_predict(H, *[x.data_ptr() for x in b[:3]], s2p(b[3]), o3.data_ptr(), n, 1e-3,
+                                       2e-3, 3, None, la, stream()) == 0
+            assert lib.po_step(H, *[x.data_ptr() for x in b[:3]], s2p(b[3]), None, n, 1e-3, 4, None, la,
+                               stream()) == 0
+            outs.append([o1, o3, *b])
+        for x, y in zip(*outs):
+            assert torch.equal(x, y)
 
 
 @pytest.mark.parametrize("offset", [1, 2, 4])
