@@ -186,6 +186,41 @@ int po_step_predict_dp_dc(const po_hparams* hp, float* w, const float* const* gr
                           const int64_t* flags, const int64_t* epoch_ctr, int64_t timeout_ms, int32_t* status,
                           void* stream);
 
+/* Sharded form (reduce-scatter + K3 + all-gather in one pass). Replica
+ * `rank` owns the shard [lo, hi) given by po_dp_shard_range (ceil(n/dp)
+ * rounded up to 64 elements). For its elements it sums the dp gradients
+ * (rank order over the peer pointers, or multimem.ld_reduce through the
+ * NVSwitch when `mc` gives multicast addresses), applies K3 against its own
+ * W / state and stores W', state' and W_hat into EVERY replica's buffers
+ * (peer stores, or multimem.st). Each element is computed once, so replicas
+ * stay bit-identical. Sequence on `stream`: wait grad_flags[r] >= epoch for
+ * all r; the shard pass; release-store epoch into done_slots[r] (DEVICE array
+ * of dp pointers: this replica's slot in each replica's done array); wait
+ * done_flags[r] >= epoch for all r (this replica's local done array), so the
+ * next kernel on `stream` sees the whole update. w, grads, state1, state2,
+ * w_hat, nonfinite_index: HOST arrays of dp (peer-mapped) device pointers in
+ * rank order; w_hat NULL = plain step; nonfinite_index NULL or per replica
+ * (each owner atomicMin's the first non-finite index of its shard into every
+ * replica's flag). coef_dev non-NULL overrides lr / lr_pred_times_s /
+ * step_count; epoch_dev non-NULL overrides epoch (CUDA-graph forms, with
+ * po_dp_signal_dev advancing it). Timeouts set *status = 1 and skip the
+ * update and the done signal. dp <= 8. */
+typedef struct po_dp_multicast {
+  float* grad;   /* all NULL: peer loads / stores */
+  float* w;
+  float* state1;
+  float* state2;
+  float* w_hat;
+} po_dp_multicast;
+
+int po_dp_shard_range(int64_t n, int32_t dp, int32_t rank, int64_t* lo, int64_t* hi);
+int po_step_predict_dp_shard(const po_hparams* hp, int32_t dp, int32_t rank, float* const* w, const float* const* grads,
+                             float* const* state1, float* const* state2, float* const* w_hat, int64_t n, double lr,
+                             double lr_pred_times_s, int64_t step_count, const po_coef* coef_dev,
+                             int64_t* const* nonfinite_index, const int64_t* grad_flags, int64_t* const* done_slots,
+                             const int64_t* done_flags, int64_t epoch, const int64_t* epoch_dev, int64_t timeout_ms,
+                             int32_t* status, const po_dp_multicast* mc, void* stream);
+
 /* ---- fused per-event stage ops (pipeoptim_stage_ops.cu) ---------------- */
 
 #define PO_LOSS_MSE 0

@@ -42,6 +42,8 @@ EXPORTS = (
     "po_step_predict_dp",
     "po_dp_signal_dev",
     "po_step_predict_dp_dc",
+    "po_dp_shard_range",
+    "po_step_predict_dp_shard",
     "po_gemm_f32x3",
     "po_gemm_f32x3_available",
     "po_p2p_send",
@@ -97,6 +99,14 @@ class po_coef(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_float), ("c_pred", ctypes.c_float), ("inv_bc1", ctypes.c_float), ("inv_bc2", ctypes.c_float)]
 
 
+class po_dp_multicast(ctypes.Structure):
+    """Multicast (NVLS) addresses for po_step_predict_dp_shard (all NULL:
+    peer loads / stores)."""
+
+    _fields_ = [("grad", ctypes.c_void_p), ("w", ctypes.c_void_p), ("state1", ctypes.c_void_p),
+                ("state2", ctypes.c_void_p), ("w_hat", ctypes.c_void_p)]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _D = ctypes.c_double
@@ -130,6 +140,10 @@ _SIGNATURES = {
                                              _P, _P]),
     "po_step_predict_dp": (ctypes.c_int, [_HP, _P, _P, ctypes.c_int32, _P, _P, _P, _I64, _D, _D, _I64, _P, _P, _I64,
                                           _I64, _P, _P]),
+    "po_dp_shard_range": (ctypes.c_int, [_I64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_I64),
+                                         ctypes.POINTER(_I64)]),
+    "po_step_predict_dp_shard": (ctypes.c_int, [_HP, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P, _P, _I64, _D, _D,
+                                                _I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P]),
     "po_gemm_f32x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
                                      _I64, _I64, _P, _I64, _P]),
     "po_gemm_f32x3_available": (ctypes.c_int, []),

@@ -631,6 +631,7 @@ __device__ __forceinline__ long long ld_acquire_sys(const long long* p) {
 __global__ void po_dp_wait_kernel(const long long* flags, int dp, long long epoch, long long timeout_cycles,
                                   int* status, const long long* epoch_dev) {
   if (threadIdx.x != 0) return;
+  if (*(volatile int*)status != 0) return;  // already failed: do not wait again
   if (epoch_dev != nullptr) epoch = *(volatile const long long*)epoch_dev;  // graph replays: device counter
   const long long t0 = clock64();
   for (int r = 0; r < dp; ++r) {
@@ -707,6 +708,177 @@ __global__ void po_dp_signal_kernel(long long* const* slots, int dp, long long e
     for (int r = 0; r < dp; ++r)
       asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(slots[r]), "l"(epoch) : "memory");
   }
+}
+
+// ---- hybrid DP x PP, sharded: reduce-scatter + K3 + all-gather in ONE pass ----
+//
+// Replica `rank` owns the contiguous shard [lo, hi) of the stage's flat
+// buffers. For each of its elements it sums the dp replicas' gradients (rank
+// order over peer memory, or multimem.ld_reduce through the NVSwitch when a
+// multicast mapping is given), applies K3 against its own copy of W / state,
+// and writes W', m', v' and W_hat into EVERY replica's buffers (dp peer
+// stores, or one multimem.st). Each element is computed exactly once, so the
+// replicas stay bit-identical whatever the reduction order; per GPU the HBM
+// traffic is ~(20 + 12/dp) B/param instead of (28 + 4 dp) B/param for
+// po_step_predict_dp (every replica reading every gradient). A done-barrier
+// (po_dp_done_kernel + a wait) follows: a replica's next forward reads W_hat
+// written by all owners.
+
+struct DpShardArgs {
+  Args a;                              // coefficients (c or dc), n = whole stage
+  float* w[kMaxDp];                    // every replica's buffers, rank order
+  float* s1[kMaxDp];
+  float* s2[kMaxDp];
+  float* out[kMaxDp];                  // W_hat (all null: plain step)
+  const float* grads[kMaxDp];
+  unsigned long long* bad[kMaxDp];     // every replica's non-finite flag (nullable)
+  float* mc_g;                         // multicast (NVLS) addresses, all null = peer stores
+  float* mc_w;
+  float* mc_s1;
+  float* mc_s2;
+  float* mc_out;
+  int dp, rank;
+  int64_t lo, hi;
+  float inv_dp;
+  int* status;
+};
+
+template <int VEC>
+__device__ __forceinline__ Vec<VEC> mc_ld_reduce(const float* p) {
+  Vec<VEC> r;
+  if constexpr (VEC == 1) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r.v[0]) : "l"(p) : "memory");
+  } else {
+#pragma unroll
+    for (int h = 0; h < VEC; h += 4)
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(r.v[h]), "=f"(r.v[h + 1]), "=f"(r.v[h + 2]), "=f"(r.v[h + 3])
+                   : "l"(p + h)
+                   : "memory");
+  }
+  return r;
+}
+
+template <int VEC>
+__device__ __forceinline__ void mc_store(float* p, const Vec<VEC>& r) {
+  if constexpr (VEC == 1) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(r.v[0]) : "memory");
+  } else {
+#pragma unroll
+    for (int h = 0; h < VEC; h += 4)
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p + h), "f"(r.v[h]),
+                   "f"(r.v[h + 1]), "f"(r.v[h + 2]), "f"(r.v[h + 3])
+                   : "memory");
+  }
+}
+
+template <int KIND, int VEC, int DP, bool MC>
+__device__ __forceinline__ void shard_vec(const DpShardArgs& d, const Coef& c, int64_t base, int64_t& bad) {
+  Vec<VEC> g;
+  if constexpr (MC) {
+    g = mc_ld_reduce<VEC>(d.mc_g + base);
+  } else {
+    Vec<VEC> gr[DP];
+#pragma unroll
+    for (int r = 0; r < DP; ++r) gr[r] = vload<VEC, 1, true>(d.grads[r] + base);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      float x = gr[0].v[j];
+#pragma unroll
+      for (int r = 1; r < DP; ++r) x = __fadd_rn(x, gr[r].v[j]);  // rank order
+      g.v[j] = x;
+    }
+  }
+  Vec<VEC> w = vload<VEC, 1, false>(d.w[d.rank] + base);
+  Vec<VEC> s1 = vload<VEC, 1, false>(d.s1[d.rank] + base);
+  Vec<VEC> s2{};
+  if constexpr (KIND != PO_SGDM) s2 = vload<VEC, 1, false>(d.s2[d.rank] + base);
+  Vec<VEC> out;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    bool e = false;
+    elem<KIND, MODE_STEP_PREDICT>(c, w.v[j], DP == 1 ? g.v[j] : __fmul_rn(g.v[j], d.inv_dp), s1.v[j], s2.v[j],
+                                  out.v[j], e);
+    if (e && bad == INT64_MAX) bad = base + j;
+  }
+  const bool write_out = MC ? d.mc_out != nullptr : d.out[0] != nullptr;
+  if constexpr (MC) {
+    mc_store<VEC>(d.mc_w + base, w);
+    mc_store<VEC>(d.mc_s1 + base, s1);
+    if constexpr (KIND != PO_SGDM) mc_store<VEC>(d.mc_s2 + base, s2);
+    if (write_out) mc_store<VEC>(d.mc_out + base, out);
+  } else {
+    // own copy first (streaming stores, as K3), then the peers (plain stores)
+    vstore<VEC, 1>(d.w[d.rank] + base, w);
+    vstore<VEC, 1>(d.s1[d.rank] + base, s1);
+    if constexpr (KIND != PO_SGDM) vstore<VEC, 1>(d.s2[d.rank] + base, s2);
+    if (write_out) vstore<VEC, 1>(d.out[d.rank] + base, out);
+#pragma unroll
+    for (int q = 1; q < DP; ++q) {
+      const int r = (d.rank + q) % DP;
+      vstore<VEC, 0>(d.w[r] + base, w);
+      vstore<VEC, 0>(d.s1[r] + base, s1);
+      if constexpr (KIND != PO_SGDM) vstore<VEC, 0>(d.s2[r] + base, s2);
+      if (write_out) vstore<VEC, 0>(d.out[r] + base, out);
+    }
+  }
+}
+
+template <int KIND, int VEC, int DP, bool MC>
+__global__ void __launch_bounds__(512) po_dp_shard_kernel(const DpShardArgs d) {
+  if (*(volatile int*)d.status != 0) return;  // a replica never signalled: update nothing
+  const Coef c = load_coef(d.a);
+  const int64_t nv = (d.hi - d.lo) / VEC;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t bad = INT64_MAX;
+  for (int64_t i = tid; i < nv; i += stride) shard_vec<KIND, VEC, DP, MC>(d, c, d.lo + i * VEC, bad);
+  const int64_t t = d.lo + nv * VEC + tid;  // scalar tail of the last shard
+  if (t < d.hi) shard_vec<KIND, 1, DP, MC>(d, c, t, bad);
+  if (bad != INT64_MAX)
+    for (int r = 0; r < DP; ++r)
+      if (d.bad[r] != nullptr) atomicMin(d.bad[r], (unsigned long long)bad);
+}
+
+// After the shard kernel (stream order): release-store the epoch into this
+// replica's slot of every replica's done array. Skipped when the gradient
+// wait timed out, so the peers time out too instead of reading a half update.
+__global__ void po_dp_done_kernel(long long* const* slots, int dp, long long epoch, const long long* epoch_dev,
+                                  const int* status) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (*(volatile const int*)status != 0) return;
+    if (epoch_dev != nullptr) epoch = *(volatile const long long*)epoch_dev;
+    __threadfence_system();
+    for (int r = 0; r < dp; ++r)
+      asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(slots[r]), "l"(epoch) : "memory");
+  }
+}
+
+template <int KIND, int VEC, bool MC>
+cudaError_t launch_shard_vec(const DpShardArgs& d, dim3 grid, dim3 block, cudaStream_t s) {
+  switch (d.dp) {
+    case 1: po_dp_shard_kernel<KIND, VEC, 1, MC><<<grid, block, 0, s>>>(d); break;
+    case 2: po_dp_shard_kernel<KIND, VEC, 2, MC><<<grid, block, 0, s>>>(d); break;
+    case 3: po_dp_shard_kernel<KIND, VEC, 3, MC><<<grid, block, 0, s>>>(d); break;
+    case 4: po_dp_shard_kernel<KIND, VEC, 4, MC><<<grid, block, 0, s>>>(d); break;
+    case 5: po_dp_shard_kernel<KIND, VEC, 5, MC><<<grid, block, 0, s>>>(d); break;
+    case 6: po_dp_shard_kernel<KIND, VEC, 6, MC><<<grid, block, 0, s>>>(d); break;
+    case 7: po_dp_shard_kernel<KIND, VEC, 7, MC><<<grid, block, 0, s>>>(d); break;
+    default: po_dp_shard_kernel<KIND, VEC, 8, MC><<<grid, block, 0, s>>>(d); break;
+  }
+  return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t launch_shard(const DpShardArgs& d, int vec, bool mc, dim3 grid, dim3 block, cudaStream_t s) {
+  if (mc) {
+    if (vec == 8) return launch_shard_vec<KIND, 8, true>(d, grid, block, s);
+    if (vec == 4) return launch_shard_vec<KIND, 4, true>(d, grid, block, s);
+    return launch_shard_vec<KIND, 1, true>(d, grid, block, s);
+  }
+  if (vec == 8) return launch_shard_vec<KIND, 8, false>(d, grid, block, s);
+  if (vec == 4) return launch_shard_vec<KIND, 4, false>(d, grid, block, s);
+  return launch_shard_vec<KIND, 1, false>(d, grid, block, s);
 }
 
 template <int KIND, int VEC>
@@ -960,6 +1132,112 @@ static int step_predict_dp_impl(const po_hparams* hp, float* w, const float* con
     case PO_ADAM: e = launch_dp<PO_ADAM>(d, vec, dim3((unsigned)grid), dim3(block), (cudaStream_t)stream); break;
     default: e = launch_dp<PO_ADAMW>(d, vec, dim3((unsigned)grid), dim3(block), (cudaStream_t)stream); break;
   }
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+
+int po_dp_shard_range(int64_t n, int32_t dp, int32_t rank, int64_t* lo, int64_t* hi) {
+  if (n < 0 || dp < 1 || dp > kMaxDp || rank < 0 || rank >= dp || lo == nullptr || hi == nullptr) return PO_EINVAL;
+  // contiguous shards of ceil(n / dp) rounded up to 64 elements (256 B), so
+  // every shard but the last starts and ends on a 256-bit vector boundary
+  int64_t chunk = (n + dp - 1) / dp;
+  chunk = (chunk + 63) / 64 * 64;
+  int64_t a = (int64_t)rank * chunk, b = a + chunk;
+  if (a > n) a = n;
+  if (b > n) b = n;
+  *lo = a;
+  *hi = b;
+  return 0;
+}
+
+int po_step_predict_dp_shard(const po_hparams* hp, int32_t dp, int32_t rank, float* const* w, const float* const* grads,
+                             float* const* state1, float* const* state2, float* const* w_hat, int64_t n, double lr,
+                             double lr_pred_times_s, int64_t step_count, const po_coef* coef_dev,
+                             int64_t* const* nonfinite_index, const int64_t* grad_flags, int64_t* const* done_slots,
+                             const int64_t* done_flags, int64_t epoch, const int64_t* epoch_dev, int64_t timeout_ms,
+                             int32_t* status, const po_dp_multicast* mc, void* stream) {
+  if (!valid_hp(hp) || step_count < 0 || dp < 1 || dp > kMaxDp || rank < 0 || rank >= dp || n < 0 ||
+      w == nullptr || grads == nullptr || state1 == nullptr || grad_flags == nullptr || done_slots == nullptr ||
+      done_flags == nullptr || status == nullptr)
+    return PO_EINVAL;
+  const bool sg = hp->kind == PO_SGDM;
+  if (!sg && state2 == nullptr) return PO_EINVAL;
+  const bool use_mc = mc != nullptr && mc->grad != nullptr;
+  if (use_mc && (mc->w == nullptr || mc->state1 == nullptr || (!sg && mc->state2 == nullptr) ||
+                 ((w_hat != nullptr) != (mc->w_hat != nullptr))))
+    return PO_EINVAL;
+  DpShardArgs d;
+  memset(&d, 0, sizeof(d));
+  d.a = Args{nullptr, nullptr, nullptr, nullptr, nullptr, n, nullptr, coef_dev,
+             coef(hp, lr, lr_pred_times_s, step_count + 1)};
+  for (int r = 0; r < dp; ++r) {
+    if (n > 0 && (w[r] == nullptr || grads[r] == nullptr || state1[r] == nullptr || (!sg && state2[r] == nullptr) ||
+                  (w_hat != nullptr && w_hat[r] == nullptr)))
+      return PO_EINVAL;
+    d.w[r] = w[r];
+    d.grads[r] = grads[r];
+    d.s1[r] = state1[r];
+    d.s2[r] = sg ? nullptr : state2[r];
+    d.out[r] = w_hat != nullptr ? w_hat[r] : nullptr;
+    d.bad[r] = nonfinite_index != nullptr ? reinterpret_cast<unsigned long long*>(nonfinite_index[r]) : nullptr;
+  }
+  if (use_mc) {
+    d.mc_g = mc->grad;
+    d.mc_w = mc->w;
+    d.mc_s1 = mc->state1;
+    d.mc_s2 = sg ? nullptr : mc->state2;
+    d.mc_out = mc->w_hat;
+  }
+  d.dp = dp;
+  d.rank = rank;
+  d.inv_dp = (float)(1.0 / (double)dp);
+  d.status = status;
+  po_dp_shard_range(n, dp, rank, &d.lo, &d.hi);
+  const long long timeout_cycles = (long long)(timeout_ms > 0 ? timeout_ms : 60000) * 2000000LL;
+  cudaStream_t s = (cudaStream_t)stream;
+  // 1) every replica's gradient of this epoch is complete
+  po_dp_wait_kernel<<<1, 32, 0, s>>>(reinterpret_cast<const long long*>(grad_flags), dp, (long long)epoch,
+                                     timeout_cycles, status, reinterpret_cast<const long long*>(epoch_dev));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  // 2) this replica's shard: reduce, K3, write to all replicas
+  const int64_t len = d.hi - d.lo;
+  if (len > 0) {
+    int vec = 8;
+    auto all_aligned = [&](int bytes) {
+      for (int r = 0; r < dp; ++r)
+        if (!aligned(d.w[r] + d.lo, bytes) || !aligned(d.grads[r] + d.lo, bytes) || !aligned(d.s1[r] + d.lo, bytes) ||
+            !aligned(d.s2[r] ? d.s2[r] + d.lo : nullptr, bytes) || !aligned(d.out[r] ? d.out[r] + d.lo : nullptr, bytes))
+          return false;
+      const float* m[5] = {d.mc_g, d.mc_w, d.mc_s1, d.mc_s2, d.mc_out};
+      for (const float* p : m)
+        if (p != nullptr && !aligned(p + d.lo, bytes)) return false;
+      return true;
+    };
+    while (vec > 1 && !all_aligned(vec * 4)) vec = vec == 8 ? 4 : 1;
+    // K3's one-vector-in-flight shapes: many small CTAs below 2^25 elements
+    // (pipeline stages), 512 x 1 CTA/SM above
+    const bool small = len < (int64_t(1) << 25);
+    const int block = small ? 128 : 512;
+    int64_t want = (len / vec + block - 1) / block;
+    if (want < 1) want = 1;
+    const int64_t cap = (int64_t)sm_count() * (small ? 16 : 1);
+    const int64_t grid = want < cap ? want : cap;
+    switch (hp->kind) {
+      case PO_SGDM: e = launch_shard<PO_SGDM>(d, vec, use_mc, dim3((unsigned)grid), dim3(block), s); break;
+      case PO_ADAM: e = launch_shard<PO_ADAM>(d, vec, use_mc, dim3((unsigned)grid), dim3(block), s); break;
+      default: e = launch_shard<PO_ADAMW>(d, vec, use_mc, dim3((unsigned)grid), dim3(block), s); break;
+    }
+    if (e != cudaSuccess) return (int)e;
+  }
+  // 3) announce this shard; 4) wait until every owner has written its shard here
+  po_dp_done_kernel<<<1, 32, 0, s>>>(reinterpret_cast<long long* const*>(done_slots), dp, (long long)epoch,
+                                     reinterpret_cast<const long long*>(epoch_dev), status);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  po_dp_wait_kernel<<<1, 32, 0, s>>>(reinterpret_cast<const long long*>(done_flags), dp, (long long)epoch,
+                                     timeout_cycles, status, reinterpret_cast<const long long*>(epoch_dev));
+  e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }
 

@@ -16,6 +16,20 @@ acquire-wait on their local flags. Gradients are double-buffered by epoch
 parity (see csrc/pipeoptim_kernels.cu for why that needs no second
 handshake). The kernel times out (status flag) instead of hanging if a
 replica never signals.
+
+`mode="shard"` (po_step_predict_dp_shard) is the reduce-scatter + K3 +
+all-gather form: the replicas' weights, optimizer state and W_hat staging
+buffer live in peer-mapped memory too, replica r computes only its 1/dp
+shard (gradient sum over the peers, K3 against its own W / state) and stores
+the results into every replica's buffers; a done-barrier then makes the
+whole update visible before the next forward. Per GPU that moves
+~(20 + 12/dp) B/param through HBM instead of (28 + 4 dp), and
+~20 (dp-1)/dp B/param per NVLink direction instead of 4 (dp-1): the
+peer-load form wins at small dp, the sharded one from dp ~ 4.
+The same kernel reads the gradient through multimem.ld_reduce and writes
+through multimem.st when the buffers are bound to NVLS multicast objects
+(`po_dp_multicast`); on this round's one-GPU boxes cuMulticastCreate is
+refused (profiles/r2_nvls_probe.txt), so only the peer-store transport runs.
 """
 
 from __future__ import annotations
@@ -30,18 +44,29 @@ from . import _lib
 class FusedDPGroup:
     """Peer-mapped, double-buffered gradients of one stage's DP replicas."""
 
-    def __init__(self, dist, group, dp_rank: int, dp_size: int, numel: int, device, timeout_ms: int = 60_000):
+    MODES = ("peer_load", "shard")
+
+    def __init__(self, dist, group, dp_rank: int, dp_size: int, numel: int, device, timeout_ms: int = 60_000,
+                 mode: str = "peer_load"):
         from .ipc import IpcBuffer, open_peer
 
         if not 1 <= dp_size <= 8:
             raise ValueError(f"fused DP supports 1..8 replicas, got {dp_size}")
-        self.dp_rank, self.dp_size, self.numel = dp_rank, dp_size, numel
+        if mode not in self.MODES:
+            raise ValueError(f"fused DP mode must be one of {self.MODES}, got {mode!r}")
+        self.dp_rank, self.dp_size, self.numel, self.mode = dp_rank, dp_size, numel, mode
         self.device = torch.device(device)
         self.timeout_ms = timeout_ms
         # node-shared (CUDA IPC) gradients and flags, mapped by each peer into
-        # its own device (ipc.py)
+        # its own device (ipc.py); shard mode adds W, state, W_hat, the done
+        # flags and the non-finite flag
         self._ipc = [IpcBuffer(numel, torch.float32, self.device) for _ in range(2)]
         self._ipc.append(IpcBuffer(dp_size, torch.int64, self.device))
+        if mode == "shard":
+            self._ipc += [IpcBuffer(numel, torch.float32, self.device) for _ in range(4)]  # W, S1, S2, W_hat
+            self._ipc.append(IpcBuffer(dp_size, torch.int64, self.device))  # done flags
+            self._ipc.append(IpcBuffer(1, torch.int64, self.device))  # non-finite flag
+            self._ipc[-1].tensor.fill_(2 ** 63 - 1)
         self.bufs = [self._ipc[0].tensor, self._ipc[1].tensor]
         self.flags = self._ipc[2].tensor
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -54,7 +79,7 @@ class FusedDPGroup:
         self._opened = []
         for r, h in enumerate(handles):
             if r == dp_rank:
-                self.peers.append((self.bufs[0], self.bufs[1], self.flags))
+                self.peers.append(tuple(b.tensor for b in self._ipc))
             else:
                 opened = [open_peer(x, self.device) for x in h]
                 self._opened += opened
@@ -67,6 +92,21 @@ class FusedDPGroup:
         self.epoch = 0
         self.parity = 0
         self._lib = _lib.load()
+        if mode == "shard":
+            P = ctypes.c_void_p * dp_size
+            col = lambda i: P(*[self.peers[r][i].data_ptr() for r in range(dp_size)])  # noqa: E731
+            self.w_ptrs, self.s1_ptrs, self.s2_ptrs, self.what_ptrs = col(3), col(4), col(5), col(6)
+            self.bad_ptrs = col(8)
+            self.done = self._ipc[7].tensor
+            # slot of THIS replica in every replica's done array (device array)
+            self.done_slots = torch.tensor([p[7].data_ptr() + 8 * dp_rank for p in self.peers], dtype=torch.int64,
+                                           device=self.device)
+            self.mc = None  # po_dp_multicast when the buffers are NVLS-bound
+            lo, hi = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(self._lib.po_dp_shard_range(numel, dp_size, dp_rank, ctypes.byref(lo), ctypes.byref(hi)),
+                       "po_dp_shard_range")
+            self.shard = (lo.value, hi.value)
+            self._adopted = False
         # CUDA-graph form (step_predict_dev): the epoch lives on the device
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=self.device)
         self._slot = None
@@ -76,6 +116,53 @@ class FusedDPGroup:
     def grad(self) -> torch.Tensor:
         """The buffer this replica's next backward must write into."""
         return self.bufs[self.parity]
+
+    def adopt(self, stage, opt, rt=None) -> None:
+        """Shard mode: move the stage's live weights, the optimizer state and
+        non-finite flag, and the W_hat staging buffer (rt: runtime._StageRt)
+        into the peer-mapped buffers the owners write into (once), and point
+        `rt`'s staging buffer at the peer-mapped W_hat (every run's _StageRt).
+        A no-op in peer_load mode."""
+        if self.mode != "shard":
+            return
+        lay = stage.flat.layout
+        if lay.numel != self.numel:
+            raise ValueError("stage size does not match the DP group's buffers")
+        if rt is not None:
+            rt.staging = self._ipc[6].tensor
+            rt.staging_views = lay.views(rt.staging)
+        if self._adopted:
+            return
+        opt._bind(lay)
+        opt._ensure_state()
+        stage.set_weight_buffer(self._ipc[3].tensor)
+        self._ipc[4].tensor.copy_(opt._s1)
+        opt._s1 = self._ipc[4].tensor
+        if opt._s2 is not None:
+            self._ipc[5].tensor.copy_(opt._s2)
+            opt._s2 = self._ipc[5].tensor
+        self._ipc[8].tensor.copy_(opt._bad)
+        opt._bad = self._ipc[8].tensor
+        self._adopted = True
+
+    @property
+    def staging(self) -> torch.Tensor | None:
+        """Shard mode: the peer-mapped W_hat buffer (the stage's staging buffer)."""
+        return self._ipc[6].tensor if self.mode == "shard" else None
+
+    def _shard_call(self, opt, flat, out, lr, c_pred, step_count, coef, epoch, epoch_dev, stream) -> None:
+        if not self._adopted or flat.data.data_ptr() != self._ipc[3].tensor.data_ptr():
+            raise RuntimeError("sharded DP: adopt(stage, opt, rt) must move the stage's buffers first")
+        if out is not None and out.data_ptr() != self._ipc[6].tensor.data_ptr():
+            raise ValueError("sharded DP: the prediction output must be the group's peer-mapped staging buffer")
+        mc = ctypes.byref(self.mc) if self.mc is not None else None
+        rc = self._lib.po_step_predict_dp_shard(
+            ctypes.byref(opt._hp), self.dp_size, self.dp_rank, self.w_ptrs, self.grad_ptrs[self.parity],
+            self.s1_ptrs, None if opt._s2 is None else self.s2_ptrs, None if out is None else self.what_ptrs,
+            self.numel, float(lr), float(c_pred), step_count, coef, self.bad_ptrs, self.flags.data_ptr(),
+            self.done_slots.data_ptr(), self.done.data_ptr(), epoch, epoch_dev, self.timeout_ms,
+            self.status.data_ptr(), mc, stream)
+        _lib.check(rc, "po_step_predict_dp_shard")
 
     def step_predict(self, opt, flat, lr: float, lr_pred: float, steps_ahead: int, out: torch.Tensor) -> None:
         """Signal this epoch's gradient, then the fused mean-over-replicas K3."""
@@ -89,6 +176,12 @@ class FusedDPGroup:
         self.epoch += 1
         stream = torch.cuda.current_stream(self.device).cuda_stream
         _lib.check(self._lib.po_dp_signal(self.slots.data_ptr(), self.dp_size, self.epoch, stream), "po_dp_signal")
+        if self.mode == "shard":
+            self._shard_call(opt, flat, out, lr, float(lr_pred) * steps_ahead, opt.step_count, None, self.epoch, None,
+                             stream)
+            opt.step_count += 1
+            self.parity ^= 1
+            return
         rc = self._lib.po_step_predict_dp(
             ctypes.byref(opt._hp), flat.data.data_ptr(), self.grad_ptrs[self.parity], self.dp_size,
             opt._s1.data_ptr(), None if opt._s2 is None else opt._s2.data_ptr(), out.data_ptr(), self.numel,
@@ -125,6 +218,11 @@ class FusedDPGroup:
                 self._slot = _SlotTape(self.device)
             self._slot.fill(opt, _lib.PO_COEF_STEP_PREDICT, lr, float(lr_pred) * steps_ahead)
             coef = self._slot.dev.data_ptr()
+        if self.mode == "shard":
+            self._shard_call(opt, flat, out, 0.0, 0.0, 0, coef, 0, self.epoch_ctr.data_ptr(), stream)
+            opt.step_count += 1
+            self.parity ^= 1
+            return
         rc = self._lib.po_step_predict_dp_dc(
             ctypes.byref(opt._hp), flat.data.data_ptr(), self.grad_ptrs[self.parity], self.dp_size,
             opt._s1.data_ptr(), None if opt._s2 is None else opt._s2.data_ptr(), out.data_ptr(), self.numel, coef,

@@ -281,6 +281,8 @@ class PeerStageRunner:
         st, links, last = self.stage, self.links, self.rank == self.depth - 1
         policy = _make_policy(self.strategy, self.tl)
         rt = _StageRt(st, self.opt, self.depth)
+        if self.fused_dp is not None:
+            self.fused_dp.adopt(st, self.opt, rt)  # shard mode: peer-mapped W, state, W_hat
         st.version = 1
         work = [op for op in self.program if op.kind != UPDATE]
         flags = torch.ones(len(work), dtype=torch.bool, device=self.device)
@@ -299,6 +301,8 @@ class PeerStageRunner:
                 if self.fused_dp is not None:  # replicas' gradient mean inside K3
                     if fuse:
                         out, lr_p, gap = rt.staging_buffer(), lr_fn(op.next_mb), op.next_gap
+                    elif self.fused_dp.mode == "shard":  # a plain step: no prediction output
+                        out, lr_p, gap = None, 0.0, 0
                     else:  # a plain step: the prediction output goes to scratch
                         if self._scratch is None:
                             self._scratch = st.flat.layout.empty(self.device)

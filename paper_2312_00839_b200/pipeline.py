@@ -406,6 +406,7 @@ class PipelineStageRunner:
         self.fused_dp = fused_dp
         if fused_dp is not None:
             stage.set_grad_buffer(fused_dp.grad)
+            fused_dp.adopt(stage, opt, self.rt)  # shard mode: peer-mapped W, state, W_hat
             self._scratch = None
         opt.eager_checks = self.eager
         # graphed=True: every op's device work is captured once per (kind,
@@ -566,6 +567,8 @@ class PipelineStageRunner:
             if self.fuse and op.fuse_predict:
                 out, lr_p, gap = self.rt.staging_buffer(), self.lr_for_mb(op.next_mb), op.next_gap
                 self.rt.prepared = (op.next_mb, op.next_gap)
+            elif self.fused_dp.mode == "shard":  # plain step: no prediction output
+                out, lr_p, gap = None, 0.0, 0
             else:  # plain step: the prediction output goes to scratch
                 if self._scratch is None:
                     self._scratch = self.stage.flat.layout.empty(self.device)
@@ -796,7 +799,9 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
 def bench_hybrid_dp_pp(torch_mod, dist, rank, world, device, n_batches: int = 32, host_staging: bool = False):
     """DP 2 x PP world/2 on config-1-shaped stages (each replica half of every
     B = 128 batch): the stage-gradient mean by NCCL all-reduce + K3 vs the
-    fused peer-memory mean inside K3 (dp_fused). Samples/s, max over ranks."""
+    fused peer-memory mean inside K3 (dp_fused, every replica reading every
+    gradient) vs the sharded form (reduce-scatter + K3 + all-gather in one
+    pass). Samples/s, max over ranks."""
     from .bench_pipeline import BATCH, CONFIG1_ACTS, CONFIG1_DIMS, DeviceBatches
     from .dp_fused import FusedDPGroup
     from .optim import OptimizerConfig, OptimizerState
@@ -817,13 +822,14 @@ def bench_hybrid_dp_pp(torch_mod, dist, rank, world, device, n_batches: int = 32
     data = DeviceBatches(torch_mod, device, dims=dims)
     out = {"config": f"DP {dp} x PP {pp}, MLP {dims}, B={BATCH} ({BATCH // dp} rows per replica), Adam, "
                      f"optimizer_prediction, {n_batches} mini-batches"}
-    for arm in ("nccl_allreduce", "fused_peer_mean"):
+    for arm in ("nccl_allreduce", "fused_peer_mean", "fused_shard"):
         times = []
         for trial, n in enumerate((2 * pp + 2, n_batches)):
             stage = StageModel(k, partition_layers(layers, pp)[k], torch_init(0, device), device)
             opt = OptimizerState(OptimizerConfig("adam"), stage.param_names, device=device)
-            fused = (FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, device)
-                     if arm == "fused_peer_mean" else None)
+            fused = (FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, device,
+                                  mode="shard" if arm == "fused_shard" else "peer_load")
+                     if arm != "nccl_allreduce" else None)
             runner = PipelineStageRunner(dist, build_timeline("optimizer_prediction", pp, n), stage, opt,
                                          "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-4, BATCH // dp,
                                          stage_ranks=[r * pp + s for s in range(pp)], dp_group=groups[k],

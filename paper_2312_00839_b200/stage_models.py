@@ -426,6 +426,14 @@ class ModuleStage:
         for p, gv in zip(self._params, self.flat.grads):
             p.grad = gv
 
+    def set_weight_buffer(self, buf: torch.Tensor) -> None:
+        """Move the live weights into `buf` (same layout) and re-point the
+        module's parameters at it."""
+        buf.copy_(self.flat.data)
+        self.flat.data = buf
+        self._live = self.flat.params
+        self._point(self._live)
+
     def _point(self, views) -> None:
         for p, v in zip(self._params, views):
             if p.data_ptr() != v.data_ptr():

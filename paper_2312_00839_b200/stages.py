@@ -185,6 +185,12 @@ class StageModel:
         current parity of a fused-DP double buffer."""
         self.flat.grad = buf
 
+    def set_weight_buffer(self, buf: torch.Tensor) -> None:
+        """Move the live weights into `buf` (same layout), e.g. a peer-mapped
+        buffer the sharded DP update writes into."""
+        buf.copy_(self.flat.data)
+        self.flat.data = buf
+
     def run_forward(self, weights, key, x, version, check_finite=True, finite_flags=None, flag_index=0):
         return stage_forward(self, weights, key, x, version, check_finite, finite_flags, flag_index)
 

@@ -55,6 +55,26 @@ int main() {
   prop.size = (bytes + gran - 1) / gran * gran;
   printf("multicast granularity %zu, size %zu\n", gran, prop.size);
   CUmemGenericAllocationHandle mch;
+  // creation matrix: devices x handle types x granularity kind
+  for (int nd = 1; nd <= 2; ++nd)
+    for (int gk = 0; gk < 2; ++gk)
+      for (int t : {0, 1, 8}) {
+        CUmulticastObjectProp p3 = {};
+        p3.numDevices = nd;
+        p3.handleTypes = (unsigned long long)t;
+        p3.size = 1 << 21;
+        size_t g3 = 0;
+        CUresult rg = cuMulticastGetGranularity(&g3, &p3, gk ? CU_MULTICAST_GRANULARITY_RECOMMENDED
+                                                             : CU_MULTICAST_GRANULARITY_MINIMUM);
+        if (rg == CUDA_SUCCESS && g3) p3.size = (p3.size + g3 - 1) / g3 * g3;
+        CUmemGenericAllocationHandle h3;
+        CUresult r3 = cuMulticastCreate(&h3, &p3);
+        const char* es = nullptr;
+        cuGetErrorString(r3, &es);
+        printf("matrix numDevices=%d gran=%s(%zu, rc %d) handleTypes=%d size=%zu -> %d %s\n", nd,
+               gk ? "recommended" : "minimum", g3, (int)rg, t, p3.size, (int)r3, es ? es : "?");
+        if (r3 == CUDA_SUCCESS) cuMemRelease(h3);
+      }
   // which handle types does cuMulticastCreate accept with one device?
   const int types[3] = {0, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_FABRIC};
   int ok_type = -1;

@@ -106,3 +106,20 @@ def test_flat_layout_alignment():
     buf = torch.arange(lay.numel, dtype=torch.float32)
     views = lay.views(buf)
     assert views[1].shape == (1, 5) and float(views[1][0, 0]) == 64.0
+
+
+@pytest.mark.parametrize("n,dp", [(0, 2), (10, 4), (512, 8), (70_080, 3), (1_000_003, 8), (64, 1)])
+def test_dp_shard_ranges_tile_the_stage(lib, n, dp):
+    """po_dp_shard_range (host-side, no GPU): contiguous shards covering
+    [0, n), each starting on a 64-element (256 B) boundary."""
+    spans = []
+    for r in range(dp):
+        lo, hi = ctypes.c_int64(), ctypes.c_int64()
+        assert lib.po_dp_shard_range(n, dp, r, ctypes.byref(lo), ctypes.byref(hi)) == 0
+        spans.append((lo.value, hi.value))
+    assert spans[0][0] == 0 and spans[-1][1] == n
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert all(lo % 64 == 0 or lo == n for lo, _ in spans)
+    lo = ctypes.c_int64()
+    assert lib.po_dp_shard_range(n, dp, dp, ctypes.byref(lo), ctypes.byref(lo)) != 0
+    assert lib.po_dp_shard_range(n, 9, 0, ctypes.byref(lo), ctypes.byref(lo)) != 0

@@ -79,7 +79,106 @@ def test_fused_dp_with_one_replica_equals_k3(tmp_path):
     assert json.loads((tmp_path / "single.json").read_text())["same"]
 
 
-def _hybrid(rank, world, port, dp, pp, n, kind, out_dir):
+def _shard_replica(rank, world, port, n, kind, out_dir):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200 import _lib
+        from paper_2312_00839_b200.dp_fused import FusedDPGroup
+        from paper_2312_00839_b200.optim import FlatLayout, OptimizerConfig, OptimizerState
+        from paper_2312_00839_b200.runtime import _StageRt
+        from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+        dev = torch.device("cuda", 0)
+        # a one-layer stage of n x 1 weights + 1 bias: numel not a multiple of
+        # 64 * world, so the last shard is short and has a scalar tail
+        stage = StageModel(0, partition_layers(build_layers([n, 1], ["linear"]), 1)[0],
+                           lambda sp: rng_ref.layer_init(3, sp.index, sp.in_dim, sp.out_dim), dev)
+        numel = stage.flat.layout.numel
+        opt = OptimizerState(OptimizerConfig(kind), stage.param_names, device=dev)
+        rt = _StageRt(stage, opt, 1)
+        grp = FusedDPGroup(dist, None, rank, world, numel, dev, timeout_ms=60_000, mode="shard")
+        grp.adopt(stage, opt, rt)
+        gens = [torch.Generator(device=dev).manual_seed(100 + r) for r in range(world)]
+        for step in range(3):
+            gs = [torch.randn(numel, device=dev, generator=gens[r]) * 0.01 for r in range(world)]
+            grp.grad.copy_(gs[rank])
+            torch.cuda.synchronize()
+            dist.barrier()  # every replica's gradient is in place before anyone signals
+            if step == 2:  # the last update is a plain step (no W_hat)
+                grp.step_predict(opt, stage.flat, 1e-3, 0.0, 0, None)
+            else:
+                grp.step_predict(opt, stage.flat, 1e-3, 2e-3, 3, rt.staging)
+            torch.cuda.synchronize()
+            if step == 1:
+                what = rt.staging.clone()
+        grp.check()
+        opt.check_finite()
+        lo, hi = grp.shard
+        Path(out_dir, f"shard{rank}.json").write_text(json.dumps({
+            "w": stage.flat.data.double().cpu().numpy().tolist(), "m": opt._s1.double().cpu().numpy().tolist(),
+            "w_hat": what.double().cpu().numpy().tolist(), "lo": lo, "hi": hi, "numel": numel}))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 3])
+@pytest.mark.parametrize("kind", ["adamw", "sgdm"])
+def test_sharded_dp_update_equals_k3_on_the_rank_order_mean(tmp_path, world, kind):
+    """po_step_predict_dp_shard, `world` processes sharing the GPU (CUDA IPC):
+    each replica updates only its shard and stores into every replica; the
+    replicas end bit-identical and equal to plain K3 (then K2) on the
+    rank-order fp32 mean of the gradients, shards covering the stage."""
+    import ctypes
+
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2312_00839_b200 import _lib
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+    n = 70_001
+    mp.spawn(_shard_replica, args=(world, _port(), n, kind, str(tmp_path)), nprocs=world, join=True)
+    got = [json.loads((tmp_path / f"shard{r}.json").read_text()) for r in range(world)]
+    spans = sorted((g["lo"], g["hi"]) for g in got)
+    assert spans[0][0] == 0 and spans[-1][1] == got[0]["numel"]
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    for g in got[1:]:
+        assert g["w"] == got[0]["w"] and g["m"] == got[0]["m"] and g["w_hat"] == got[0]["w_hat"]
+    # single-process reference: plain K3 / K2 on the rank-order mean
+    dev = torch.device("cuda", 0)
+    stage = StageModel(0, partition_layers(build_layers([n, 1], ["linear"]), 1)[0],
+                       lambda sp: rng_ref.layer_init(3, sp.index, sp.in_dim, sp.out_dim), dev)
+    numel = stage.flat.layout.numel
+    opt = OptimizerState(OptimizerConfig(kind), stage.param_names, device=dev)
+    gens = [torch.Generator(device=dev).manual_seed(100 + r) for r in range(world)]
+    out = torch.empty(numel, device=dev)
+    inv = torch.tensor(1.0 / world, dtype=torch.float32, device=dev)
+    for step in range(3):
+        gs = [torch.randn(numel, device=dev, generator=gens[r]) * 0.01 for r in range(world)]
+        acc = gs[0].clone()
+        for x in gs[1:]:
+            acc = acc + x
+        stage.flat.grad.copy_(acc if world == 1 else acc * inv)
+        if step == 2:
+            opt.step_(stage.flat, 1e-3)
+        else:
+            opt.step_predict_(stage.flat, 1e-3, 2e-3, 3, out)
+        if step == 1:
+            what = out.clone()
+    assert stage.flat.data.double().cpu().numpy().tolist() == got[0]["w"]
+    assert opt._s1.double().cpu().numpy().tolist() == got[0]["m"]
+    assert what.double().cpu().numpy().tolist() == got[0]["w_hat"]
+
+
+def _hybrid(rank, world, port, dp, pp, n, kind, out_dir, mode="peer_load"):
     import torch
     import torch.distributed as dist
 
@@ -100,7 +199,7 @@ def _hybrid(rank, world, port, dp, pp, n, kind, out_dir):
                            lambda sp: rng_ref.layer_init(4, sp.index, sp.in_dim, sp.out_dim), dev)
         kw = {"weight_decay": 0.0} if kind == "sgdm" else {}
         opt = OptimizerState(OptimizerConfig(kind, **kw), stage.param_names, device=dev)
-        fused = FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, dev, timeout_ms=120_000)
+        fused = FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, dev, timeout_ms=120_000, mode=mode)
         tl = build_timeline("optimizer_prediction", pp, n)
         runner = PipelineStageRunner(dist, tl, stage, opt, "optimizer_prediction", Src(), "mse", lambda mb: 0.01,
                                      8 // dp, stage_ranks=[r * pp + s for s in range(pp)], dp_group=groups[k],
@@ -119,15 +218,17 @@ def _hybrid(rank, world, port, dp, pp, n, kind, out_dir):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["peer_load", "shard"])
 @pytest.mark.parametrize("kind", ["adam", "sgdm"])
-def test_fused_dp_x_pp_equals_full_batch_pipeline(tmp_path, kind):
+def test_fused_dp_x_pp_equals_full_batch_pipeline(tmp_path, kind, mode):
     """DP 2 x PP 2 (4 processes on one GPU): the fused peer-memory mean + K3
-    keeps the replicas bit-identical and equals the 2-stage pipeline on the
-    full batch (oracle)."""
+    (every replica reads every gradient, or each updates its shard and stores
+    into all) keeps the replicas bit-identical and equals the 2-stage
+    pipeline on the full batch (oracle)."""
     import torch.multiprocessing as mp
 
     dp, pp, n = 2, 2, 8
-    mp.spawn(_hybrid, args=(dp * pp, _port(), dp, pp, n, kind, str(tmp_path)), nprocs=dp * pp, join=True)
+    mp.spawn(_hybrid, args=(dp * pp, _port(), dp, pp, n, kind, str(tmp_path), mode), nprocs=dp * pp, join=True)
     got = json.loads((tmp_path / "out.json").read_text())
     ref = runtime_ref.run(DIMS, ACTS, pp, n, "optimizer_prediction", optim_ref.Hyper(kind, weight_decay=0.0),
                           Src().batch, "mse", lambda mb: 0.01, lambda i, a, b: rng_ref.layer_init(4, i, a, b))

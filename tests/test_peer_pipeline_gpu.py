@@ -238,7 +238,7 @@ class HSrc:
         return self.b[mb]
 
 
-def _hybrid_worker(rank, world, port, dp, pp, n, kind, out_dir):
+def _hybrid_worker(rank, world, port, dp, pp, n, kind, out_dir, dp_mode="peer_load"):
     import torch
     import torch.distributed as dist
 
@@ -263,7 +263,8 @@ def _hybrid_worker(rank, world, port, dp, pp, n, kind, out_dir):
             stage = StageModel(k, partition_layers(build_layers(HDIMS, HACTS), pp)[k],
                                lambda sp: rng_ref.layer_init(4, sp.index, sp.in_dim, sp.out_dim), dev)
             opt = OptimizerState(OptimizerConfig(kind, **kw), stage.param_names, device=dev)
-            fused = FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, dev, timeout_ms=120_000)
+            fused = FusedDPGroup(dist, groups[k], r, dp, stage.flat.layout.numel, dev, timeout_ms=120_000,
+                                 mode=dp_mode)
             runner = PeerStageRunner(dist, build_timeline("optimizer_prediction", pp, n), stage, opt,
                                      "optimizer_prediction", data, "mse", lambda mb: 0.01, 8 // dp,
                                      stage_ranks=[r * pp + s for s in range(pp)], dp_rank=r, dp_size=dp,
@@ -286,8 +287,9 @@ def _hybrid_worker(rank, world, port, dp, pp, n, kind, out_dir):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("dp_mode", ["peer_load", "shard"])
 @pytest.mark.parametrize("kind", ["adam", "sgdm"])
-def test_peer_runner_hybrid_dp_graph(tmp_path, kind):
+def test_peer_runner_hybrid_dp_graph(tmp_path, kind, dp_mode):
     """DP 2 x PP 2 (4 processes on one GPU) through the peer runner with the
     DP mean fused into K3 on device epochs: the first run equals the
     full-batch 2-stage oracle pipeline, replicas stay bit-identical, and an
@@ -295,7 +297,8 @@ def test_peer_runner_hybrid_dp_graph(tmp_path, kind):
     import torch.multiprocessing as mp
 
     dp, pp, n = 2, 2, 8
-    mp.spawn(_hybrid_worker, args=(dp * pp, _port(), dp, pp, n, kind, str(tmp_path)), nprocs=dp * pp, join=True)
+    mp.spawn(_hybrid_worker, args=(dp * pp, _port(), dp, pp, n, kind, str(tmp_path), dp_mode), nprocs=dp * pp,
+             join=True)
     res = [json.loads((tmp_path / f"h{i}.json").read_text()) for i in range(dp * pp)]
     ref = runtime_ref.run(HDIMS, HACTS, pp, n, "optimizer_prediction", optim_ref.Hyper(kind, weight_decay=0.0),
                           lambda mb: tuple(t.cpu().numpy() for t in HSrc("cpu").batch(mb)), "mse", lambda mb: 0.01,
