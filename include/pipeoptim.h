@@ -54,6 +54,7 @@ extern "C" {
 
 #define PO_ABI_VERSION 1
 #define PO_EINVAL (-22)
+#define PO_EDRIVER_BASE 100000 /* CUDA driver-API error r is returned as PO_EDRIVER_BASE + r */
 
 /* optimizer kinds, OPTIMIZER_KINDS optim.py:17 */
 #define PO_SGDM 0
@@ -220,6 +221,23 @@ int po_step_predict_dp_shard(const po_hparams* hp, int32_t dp, int32_t rank, flo
                              int64_t* const* nonfinite_index, const int64_t* grad_flags, int64_t* const* done_slots,
                              const int64_t* done_flags, int64_t epoch, const int64_t* epoch_dev, int64_t timeout_ms,
                              int32_t* status, const po_dp_multicast* mc, void* stream);
+
+/* NVLS multicast objects for the sharded update (pipeoptim_nvls.cu). One
+ * object per DP group covers a replica's update buffers; the creator exports
+ * it as a POSIX fd (the host passes it to the other replicas over a UNIX
+ * socket), every replica opens it, adds its current device, and — after all
+ * have added — binds one zero-filled local allocation of po_nvls_size bytes,
+ * getting a unicast VA (its own buffers) and a multicast VA (for
+ * po_dp_multicast). po_nvls_probe: 0 if an object for n_devices can be
+ * created on this device (created and released), else the error. */
+typedef struct po_nvls po_nvls;
+int po_nvls_probe(int32_t n_devices, int64_t bytes, int64_t* granularity);
+int po_nvls_create(int32_t n_devices, int64_t bytes, int32_t* fd_out, po_nvls** out);
+int po_nvls_open(int32_t fd, int32_t n_devices, int64_t bytes, po_nvls** out);
+int po_nvls_add_device(po_nvls* g);
+int po_nvls_bind(po_nvls* g, void** uc_ptr, void** mc_ptr);
+int64_t po_nvls_size(const po_nvls* g);
+int po_nvls_free(po_nvls* g);
 
 /* ---- fused per-event stage ops (pipeoptim_stage_ops.cu) ---------------- */
 

@@ -44,6 +44,13 @@ EXPORTS = (
     "po_step_predict_dp_dc",
     "po_dp_shard_range",
     "po_step_predict_dp_shard",
+    "po_nvls_probe",
+    "po_nvls_create",
+    "po_nvls_open",
+    "po_nvls_add_device",
+    "po_nvls_bind",
+    "po_nvls_size",
+    "po_nvls_free",
     "po_gemm_f32x3",
     "po_gemm_f32x3_available",
     "po_p2p_send",
@@ -144,6 +151,14 @@ _SIGNATURES = {
                                          ctypes.POINTER(_I64)]),
     "po_step_predict_dp_shard": (ctypes.c_int, [_HP, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P, _P, _I64, _D, _D,
                                                 _I64, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, _P]),
+    "po_nvls_probe": (ctypes.c_int, [ctypes.c_int32, _I64, ctypes.POINTER(_I64)]),
+    "po_nvls_create": (ctypes.c_int, [ctypes.c_int32, _I64, ctypes.POINTER(ctypes.c_int32),
+                                      ctypes.POINTER(ctypes.c_void_p)]),
+    "po_nvls_open": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _I64, ctypes.POINTER(ctypes.c_void_p)]),
+    "po_nvls_add_device": (ctypes.c_int, [_P]),
+    "po_nvls_bind": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]),
+    "po_nvls_size": (_I64, [_P]),
+    "po_nvls_free": (ctypes.c_int, [_P]),
     "po_gemm_f32x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
                                      _I64, _I64, _P, _I64, _P]),
     "po_gemm_f32x3_available": (ctypes.c_int, []),

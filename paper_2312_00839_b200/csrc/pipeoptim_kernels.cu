@@ -19,6 +19,7 @@
 //
 // Numerics follow the reference formulas in fp32 with IEEE div/sqrt (no
 // fast-math): see Appendix A of SURVEY.md and the per-line citations below.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
@@ -912,6 +913,16 @@ int po_abi_version(void) { return PO_ABI_VERSION; }
 const char* po_strerror(int code) {
   if (code == 0) return "ok";
   if (code == PO_EINVAL) return "invalid argument";
+  if (code >= PO_EDRIVER_BASE) {  // resolved at run time: no link-time libcuda dependency
+    using Fn = CUresult (*)(CUresult, const char**);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const char* s = nullptr;
+    if (cudaGetDriverEntryPoint("cuGetErrorString", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      reinterpret_cast<Fn>(fn)((CUresult)(code - PO_EDRIVER_BASE), &s);
+    return s != nullptr ? s : "CUDA driver error";
+  }
   return cudaGetErrorString((cudaError_t)code);
 }
 

@@ -35,73 +35,126 @@ refused (profiles/r2_nvls_probe.txt), so only the peer-store transport runs.
 from __future__ import annotations
 
 import ctypes
+import os
+import socket
 
 import torch
 
 from . import _lib
 
 
+def send_fd(dist, group, rank: int, size: int, fd):
+    """Pass a file descriptor from replica 0 to replicas 1..size-1 of `group`
+    over an abstract UNIX socket (SCM_RIGHTS); returns the received fd on the
+    others (a new descriptor the caller owns), None on replica 0. Used for
+    the NVLS multicast object's POSIX handle."""
+    token = [os.urandom(8).hex() if rank == 0 else None]
+    dist.broadcast_object_list(token, src=_group_src(dist, group), group=group)
+    name = f"\0pipeoptim-fd-{os.getuid()}-{token[0]}"
+    if rank == 0:
+        with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as srv:
+            srv.bind(name)
+            srv.listen(size)
+            dist.barrier(group=group)
+            for _ in range(size - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"fd"], [fd])
+        dist.barrier(group=group)
+        return None
+    dist.barrier(group=group)
+    with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as c:
+        c.connect(name)
+        _, fds, _, _ = socket.recv_fds(c, 16, 1)
+    dist.barrier(group=group)
+    return fds[0]
+
+
+def _group_src(dist, group) -> int:
+    """Global rank of the group's replica 0 (broadcast_object_list takes a
+    global source rank)."""
+    if group is None:
+        return 0
+    return dist.get_global_rank(group, 0)
+
+
 class FusedDPGroup:
-    """Peer-mapped, double-buffered gradients of one stage's DP replicas."""
+    """Peer-mapped, double-buffered gradients of one stage's DP replicas
+    (shard mode: also the weights, optimizer state and W_hat)."""
 
     MODES = ("peer_load", "shard")
+    TRANSPORTS = ("peer", "nvls")
+    _BIG = ("grad0", "grad1", "w", "s1", "s2", "w_hat")  # fp32 [numel] each
 
     def __init__(self, dist, group, dp_rank: int, dp_size: int, numel: int, device, timeout_ms: int = 60_000,
-                 mode: str = "peer_load"):
+                 mode: str = "peer_load", transport: str = "peer"):
         from .ipc import IpcBuffer, open_peer
 
         if not 1 <= dp_size <= 8:
             raise ValueError(f"fused DP supports 1..8 replicas, got {dp_size}")
         if mode not in self.MODES:
             raise ValueError(f"fused DP mode must be one of {self.MODES}, got {mode!r}")
-        self.dp_rank, self.dp_size, self.numel, self.mode = dp_rank, dp_size, numel, mode
+        if transport not in self.TRANSPORTS or (transport == "nvls" and mode != "shard"):
+            raise ValueError(f"transport must be 'peer', or 'nvls' with mode='shard'; got {transport!r}")
+        self.dp_rank, self.dp_size, self.numel, self.mode, self.transport = dp_rank, dp_size, numel, mode, transport
         self.device = torch.device(device)
         self.timeout_ms = timeout_ms
-        # node-shared (CUDA IPC) gradients and flags, mapped by each peer into
-        # its own device (ipc.py); shard mode adds W, state, W_hat, the done
-        # flags and the non-finite flag
-        self._ipc = [IpcBuffer(numel, torch.float32, self.device) for _ in range(2)]
-        self._ipc.append(IpcBuffer(dp_size, torch.int64, self.device))
+        self._lib = _lib.load()
+        big = self._BIG if mode == "shard" else self._BIG[:2]
+        # node-shared (CUDA IPC) buffers, mapped by each peer into its own
+        # device (ipc.py): the big fp32 buffers (unless NVLS-bound) and the
+        # flag arrays (gradient-ready [dp], done [dp], non-finite [1])
+        ipc_specs = [] if transport == "nvls" else [(name, numel, torch.float32) for name in big]
+        ipc_specs.append(("flags", dp_size, torch.int64))
         if mode == "shard":
-            self._ipc += [IpcBuffer(numel, torch.float32, self.device) for _ in range(4)]  # W, S1, S2, W_hat
-            self._ipc.append(IpcBuffer(dp_size, torch.int64, self.device))  # done flags
-            self._ipc.append(IpcBuffer(1, torch.int64, self.device))  # non-finite flag
-            self._ipc[-1].tensor.fill_(2 ** 63 - 1)
-        self.bufs = [self._ipc[0].tensor, self._ipc[1].tensor]
-        self.flags = self._ipc[2].tensor
+            ipc_specs += [("done", dp_size, torch.int64), ("bad", 1, torch.int64)]
+        self._ipc = {name: IpcBuffer(n, dt, self.device) for name, n, dt in ipc_specs}
+        self.local = {name: b.tensor for name, b in self._ipc.items()}
+        self.mc = None  # per gradient parity: po_dp_multicast (NVLS transport)
+        self._nvls = None
+        if transport == "nvls":
+            self._bind_nvls(dist, group, big)
+        if "bad" in self.local:
+            self.local["bad"].fill_(2 ** 63 - 1)
+        self.bufs = [self.local["grad0"], self.local["grad1"]]
+        self.flags = self.local["flags"]
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.poisoned = False
         torch.cuda.synchronize(self.device)
-        mine = [b.export() for b in self._ipc]
+        names = list(self._ipc)
+        mine = [self._ipc[n].export() for n in names]
         handles = [None] * dp_size
         dist.all_gather_object(handles, mine, group=group)
-        self.peers = []
         self._opened = []
+        # peer[name][r]: replica r's buffer mapped here (own buffers for r == dp_rank,
+        # and for every r where the transport is NVLS — those are reached via multicast)
+        self.peer = {n: [None] * dp_size for n in self.local}
         for r, h in enumerate(handles):
-            if r == dp_rank:
-                self.peers.append(tuple(b.tensor for b in self._ipc))
-            else:
-                opened = [open_peer(x, self.device) for x in h]
-                self._opened += opened
-                self.peers.append(tuple(pb.tensor for pb in opened))
+            for n, x in zip(names, h):
+                if r == dp_rank:
+                    self.peer[n][r] = self.local[n]
+                else:
+                    pb = open_peer(x, self.device)
+                    self._opened.append(pb)
+                    self.peer[n][r] = pb.tensor
+        for n in self.local:
+            if n not in self._ipc:
+                self.peer[n] = [self.local[n]] * dp_size
         # slot of THIS replica in every replica's flag array
-        self.slots = torch.tensor([p[2].data_ptr() + 8 * dp_rank for p in self.peers], dtype=torch.int64,
+        self.slots = torch.tensor([t.data_ptr() + 8 * dp_rank for t in self.peer["flags"]], dtype=torch.int64,
                                   device=self.device)
-        self.grad_ptrs = [(ctypes.c_void_p * dp_size)(*[self.peers[r][par].data_ptr() for r in range(dp_size)])
-                          for par in (0, 1)]
+        P = ctypes.c_void_p * dp_size
+        col = lambda n: P(*[t.data_ptr() for t in self.peer[n]])  # noqa: E731
+        self.grad_ptrs = [col("grad0"), col("grad1")]
         self.epoch = 0
         self.parity = 0
-        self._lib = _lib.load()
         if mode == "shard":
-            P = ctypes.c_void_p * dp_size
-            col = lambda i: P(*[self.peers[r][i].data_ptr() for r in range(dp_size)])  # noqa: E731
-            self.w_ptrs, self.s1_ptrs, self.s2_ptrs, self.what_ptrs = col(3), col(4), col(5), col(6)
-            self.bad_ptrs = col(8)
-            self.done = self._ipc[7].tensor
+            self.w_ptrs, self.s1_ptrs, self.s2_ptrs, self.what_ptrs = col("w"), col("s1"), col("s2"), col("w_hat")
+            self.bad_ptrs = col("bad")
+            self.done = self.local["done"]
             # slot of THIS replica in every replica's done array (device array)
-            self.done_slots = torch.tensor([p[7].data_ptr() + 8 * dp_rank for p in self.peers], dtype=torch.int64,
-                                           device=self.device)
-            self.mc = None  # po_dp_multicast when the buffers are NVLS-bound
+            self.done_slots = torch.tensor([t.data_ptr() + 8 * dp_rank for t in self.peer["done"]],
+                                           dtype=torch.int64, device=self.device)
             lo, hi = ctypes.c_int64(), ctypes.c_int64()
             _lib.check(self._lib.po_dp_shard_range(numel, dp_size, dp_rank, ctypes.byref(lo), ctypes.byref(hi)),
                        "po_dp_shard_range")
@@ -111,6 +164,37 @@ class FusedDPGroup:
         self.epoch_ctr = torch.zeros(1, dtype=torch.int64, device=self.device)
         self._slot = None
         dist.barrier(group=group)
+
+    def _bind_nvls(self, dist, group, big) -> None:
+        """One NVLS multicast object over all the replicas' big buffers:
+        replica 0 creates it and passes its POSIX fd to the others over a
+        UNIX socket (SCM_RIGHTS); every replica adds its device, then binds its
+        own physical memory and maps the unicast and multicast addresses."""
+        from .ipc import _wrap
+
+        region = self.numel * 4
+        total = region * len(big)
+        lib = self._lib
+        h = ctypes.c_void_p()
+        if self.dp_rank == 0:
+            fd = ctypes.c_int32(-1)
+            _lib.check(lib.po_nvls_create(self.dp_size, total, ctypes.byref(fd), ctypes.byref(h)), "po_nvls_create")
+            send_fd(dist, group, self.dp_rank, self.dp_size, fd.value)
+            os.close(fd.value)
+        else:
+            fd = send_fd(dist, group, self.dp_rank, self.dp_size, None)
+            _lib.check(lib.po_nvls_open(fd, self.dp_size, total, ctypes.byref(h)), "po_nvls_open")
+            os.close(fd)
+        self._nvls = h
+        _lib.check(lib.po_nvls_add_device(h), "po_nvls_add_device")
+        dist.barrier(group=group)  # every device is in the team before anyone binds
+        uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(lib.po_nvls_bind(h, ctypes.byref(uc), ctypes.byref(mc)), "po_nvls_bind")
+        dist.barrier(group=group)
+        for i, name in enumerate(big):
+            self.local[name] = _wrap(uc.value + i * region, self.numel, torch.float32, self.device)
+        at = {name: mc.value + i * region for i, name in enumerate(big)}
+        self.mc = [_lib.po_dp_multicast(at[g], at["w"], at["s1"], at["s2"], at["w_hat"]) for g in ("grad0", "grad1")]
 
     @property
     def grad(self) -> torch.Tensor:
@@ -129,33 +213,33 @@ class FusedDPGroup:
         if lay.numel != self.numel:
             raise ValueError("stage size does not match the DP group's buffers")
         if rt is not None:
-            rt.staging = self._ipc[6].tensor
+            rt.staging = self.local["w_hat"]
             rt.staging_views = lay.views(rt.staging)
         if self._adopted:
             return
         opt._bind(lay)
         opt._ensure_state()
-        stage.set_weight_buffer(self._ipc[3].tensor)
-        self._ipc[4].tensor.copy_(opt._s1)
-        opt._s1 = self._ipc[4].tensor
+        stage.set_weight_buffer(self.local["w"])
+        self.local["s1"].copy_(opt._s1)
+        opt._s1 = self.local["s1"]
         if opt._s2 is not None:
-            self._ipc[5].tensor.copy_(opt._s2)
-            opt._s2 = self._ipc[5].tensor
-        self._ipc[8].tensor.copy_(opt._bad)
-        opt._bad = self._ipc[8].tensor
+            self.local["s2"].copy_(opt._s2)
+            opt._s2 = self.local["s2"]
+        self.local["bad"].copy_(opt._bad)
+        opt._bad = self.local["bad"]
         self._adopted = True
 
     @property
     def staging(self) -> torch.Tensor | None:
         """Shard mode: the peer-mapped W_hat buffer (the stage's staging buffer)."""
-        return self._ipc[6].tensor if self.mode == "shard" else None
+        return self.local["w_hat"] if self.mode == "shard" else None
 
     def _shard_call(self, opt, flat, out, lr, c_pred, step_count, coef, epoch, epoch_dev, stream) -> None:
-        if not self._adopted or flat.data.data_ptr() != self._ipc[3].tensor.data_ptr():
+        if not self._adopted or flat.data.data_ptr() != self.local["w"].data_ptr():
             raise RuntimeError("sharded DP: adopt(stage, opt, rt) must move the stage's buffers first")
-        if out is not None and out.data_ptr() != self._ipc[6].tensor.data_ptr():
+        if out is not None and out.data_ptr() != self.local["w_hat"].data_ptr():
             raise ValueError("sharded DP: the prediction output must be the group's peer-mapped staging buffer")
-        mc = ctypes.byref(self.mc) if self.mc is not None else None
+        mc = ctypes.byref(self.mc[self.parity]) if self.mc is not None else None
         rc = self._lib.po_step_predict_dp_shard(
             ctypes.byref(opt._hp), self.dp_size, self.dp_rank, self.w_ptrs, self.grad_ptrs[self.parity],
             self.s1_ptrs, None if opt._s2 is None else self.s2_ptrs, None if out is None else self.what_ptrs,

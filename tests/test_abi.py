@@ -13,7 +13,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def declared_symbols():
     text = (ROOT / "include" / "pipeoptim.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(po_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(po_\w+)\s*\(", text, re.M)))
 
 
 @pytest.fixture(scope="module")

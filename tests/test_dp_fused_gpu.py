@@ -79,7 +79,7 @@ def test_fused_dp_with_one_replica_equals_k3(tmp_path):
     assert json.loads((tmp_path / "single.json").read_text())["same"]
 
 
-def _shard_replica(rank, world, port, n, kind, out_dir):
+def _shard_replica(rank, world, port, n, kind, out_dir, transport="peer"):
     import ctypes
 
     import torch
@@ -102,7 +102,7 @@ def _shard_replica(rank, world, port, n, kind, out_dir):
         numel = stage.flat.layout.numel
         opt = OptimizerState(OptimizerConfig(kind), stage.param_names, device=dev)
         rt = _StageRt(stage, opt, 1)
-        grp = FusedDPGroup(dist, None, rank, world, numel, dev, timeout_ms=60_000, mode="shard")
+        grp = FusedDPGroup(dist, None, rank, world, numel, dev, timeout_ms=60_000, mode="shard", transport=transport)
         grp.adopt(stage, opt, rt)
         gens = [torch.Generator(device=dev).manual_seed(100 + r) for r in range(world)]
         for step in range(3):
@@ -135,17 +135,37 @@ def test_sharded_dp_update_equals_k3_on_the_rank_order_mean(tmp_path, world, kin
     each replica updates only its shard and stores into every replica; the
     replicas end bit-identical and equal to plain K3 (then K2) on the
     rank-order fp32 mean of the gradients, shards covering the stage."""
+    _check_sharded(tmp_path, world, kind, "peer")
+
+
+def test_sharded_dp_update_over_nvls_multicast(tmp_path):
+    """The NVLS transport of the sharded update (multimem.ld_reduce of the
+    gradient, multimem.st of the results through a multicast object bound to
+    every replica's buffers): one replica == plain K3 bit for bit. Skips, with
+    the driver's reason, where multicast objects cannot be created (the
+    one-GPU boxes of this round: profiles/r2_nvls_probe.txt)."""
     import ctypes
 
+    from paper_2312_00839_b200 import _lib
+
+    lib = _lib.load()
+    gran = ctypes.c_int64()
+    rc = lib.po_nvls_probe(1, 1 << 21, ctypes.byref(gran))
+    if rc != 0:
+        assert rc >= 100_000, rc  # a driver refusal (PO_EDRIVER_BASE + CUresult), not a library error
+        pytest.skip(f"NVLS multicast objects unavailable here: {lib.po_strerror(rc).decode()}")
+    _check_sharded(tmp_path, 1, "adam", "nvls")
+
+
+def _check_sharded(tmp_path, world, kind, transport):
     import torch
     import torch.multiprocessing as mp
 
-    from paper_2312_00839_b200 import _lib
     from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
     from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
 
     n = 70_001
-    mp.spawn(_shard_replica, args=(world, _port(), n, kind, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_shard_replica, args=(world, _port(), n, kind, str(tmp_path), transport), nprocs=world, join=True)
     got = [json.loads((tmp_path / f"shard{r}.json").read_text()) for r in range(world)]
     spans = sorted((g["lo"], g["hi"]) for g in got)
     assert spans[0][0] == 0 and spans[-1][1] == got[0]["numel"]

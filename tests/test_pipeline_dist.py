@@ -313,3 +313,39 @@ def test_gloo_gpipe_matches_reference_golden(tmp_path, case):
         params = json.loads((tmp_path / f"params{k}.json").read_text())
         for p, want in zip(params, case["params"][k]):
             assert optim_ref.inf_norm_rel(np.array(p), np.array(want)) <= 1e-4
+
+
+def _fd_worker(rank, world, port, out_dir):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.dp_fused import send_fd
+
+        if rank == 0:
+            r, w = os.pipe()
+            os.write(w, b"nvls-handle")
+            os.close(w)
+            send_fd(dist, None, rank, world, r)
+            os.close(r)
+        else:
+            fd = send_fd(dist, None, rank, world, None)
+            data = os.read(fd, 64) if rank == 1 else b"(pipe drained by rank 1)"
+            os.close(fd)
+            Path(out_dir, f"fd{rank}.txt").write_bytes(data)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fd_passing_for_nvls_handles(tmp_path):
+    """dp_fused.send_fd: replica 0's POSIX fd (the NVLS multicast object's
+    exported handle on a GPU box; a pipe here) reaches every other replica
+    over an abstract UNIX socket (SCM_RIGHTS) — all receive the same open file."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_fd_worker, args=(3, free_port(), str(tmp_path)), nprocs=3, join=True)
+    assert (tmp_path / "fd1.txt").read_bytes() == b"nvls-handle"
+    assert (tmp_path / "fd2.txt").exists()
