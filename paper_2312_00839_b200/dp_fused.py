@@ -120,6 +120,7 @@ class FusedDPGroup:
         self.flags = self.local["flags"]
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.poisoned = False
+        self.closed = False
         torch.cuda.synchronize(self.device)
         names = list(self._ipc)
         mine = [self._ipc[n].export() for n in names]
@@ -326,6 +327,27 @@ class FusedDPGroup:
             self.poisoned = True
             raise RuntimeError("fused DP update timed out waiting for a replica's gradient signal")
 
+    def close(self, dist=None, group=None) -> None:
+        """Unmap the peers' buffers, free this replica's, release the NVLS
+        object. Every replica must be done with the group: pass `dist` (and
+        the group) to barrier first, or call it only after a barrier. The
+        stage / optimizer must not use adopted buffers afterwards."""
+        torch.cuda.synchronize(self.device)
+        if dist is not None:
+            dist.barrier(group=group)
+        for pb in self._opened:
+            pb.close()
+        self._opened = []
+        for b in self._ipc.values():
+            b.free()
+        self._ipc = {}
+        if self._nvls is not None:
+            _lib.check(self._lib.po_nvls_free(self._nvls), "po_nvls_free")
+            self._nvls = None
+        self.closed = True
+
     def _live(self) -> None:
+        if self.closed:
+            raise RuntimeError("fused DP group is closed")
         if self.poisoned:
             raise RuntimeError("fused DP group is poisoned: an earlier update timed out waiting for a replica")
