@@ -96,16 +96,27 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
     last stage) + backward + update (K3 when predictive and not last, else K2)."""
     from .stages import loss_and_grad
 
+    from .runtime import staging_in_grad_ok
+
     last = k == depth - 1
     x0, y0 = data.batch(1)
     x = x0 if k == 0 else torch.randn((x0.shape[0], *st.in_shape), device=device)
     g_last = None if last else torch.randn((x0.shape[0], *st.out_shape), device=device)
-    staging = st.flat.layout.empty(device)
+    predicted = predictive and not last
+    # as in the pipeline: W_hat over the dead gradient where that is exact,
+    # and the predicted forward reads it (the run's F_{j+D-k} after U_j)
+    if predicted and staging_in_grad_ok(st, True, 1):
+        staging = st.flat.grad
+    else:
+        staging = st.flat.layout.empty(device)
+        if predicted:
+            staging.copy_(st.flat.data)
+    fwd_weights = st.flat.layout.views(staging) if predicted else st.params
     opt._bind(st.flat.layout)
     opt._ensure_state()
 
     def unit():
-        out = st.run_forward(st.params, (0, 0), x, 1, check_finite=False)
+        out = st.run_forward(fwd_weights, (0, 0), x, 1, check_finite=False)
         g = loss_and_grad(out, y0, loss_kind)[1] if last else g_last
         st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0)
         if predictive and not last:
@@ -247,8 +258,9 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
         r_on, r_off = out["pred_on"]["projection"], out["pred_off"]["projection"]
         out["projected_one_stage_per_gpu_prediction_overhead"] = round(
             1.0 - r_on["one_stage_per_gpu_samples_per_s"] / r_off["one_stage_per_gpu_samples_per_s"], 4)
-        out["single_gpu_note"] = ("all stages share one GPU's SMs and 126 MB L2 here; the predicted-weights "
-                                  "staging buffers add ~21 MB to a ~105 MB per-mini-batch working set")
+        out["single_gpu_note"] = ("all stages share one GPU's SMs and 126 MB L2 here; W_hat lives in each "
+                                  "stage's dead gradient buffer (runtime.STAGING_IN_GRAD), so prediction adds "
+                                  "no buffer to the ~105 MB per-mini-batch working set")
     if with_eager:
         out["eager_prediction_overhead"] = round(
             1.0 - out["pred_on"]["eager_samples_per_s"] / out["pred_off"]["eager_samples_per_s"], 4)

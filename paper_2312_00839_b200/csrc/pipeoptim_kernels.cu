@@ -93,7 +93,11 @@ __host__ __device__ constexpr bool uses_s2(int kind, int mode) {
   return kind != PO_SGDM && mode != MODE_AXPY && uses_s1(mode);
 }
 __host__ __device__ constexpr bool writes_state(int mode) { return writes_w(mode); }
+#ifdef PO_PROBE_K3_NO_WHAT  // timing probe only (scripts/k3_no_what_probe.py): K3 skips its W_hat store
+__host__ __device__ constexpr bool writes_out(int mode) { return mode != MODE_STEP && mode != MODE_STEP_PREDICT; }
+#else
 __host__ __device__ constexpr bool writes_out(int mode) { return mode != MODE_STEP; }
+#endif
 
 // ---- vector memory access -------------------------------------------------
 
@@ -532,6 +536,9 @@ int run(int kind, int mode, Args a, const po_launch* L, cudaStream_t s) {
   int cache = (L && L->cache > 0 && L->cache <= 4) ? L->cache : d.cache;
   if (L && L->cache == 3) cache = 0;  // explicit plain ld/st request
   int unroll = (L && L->unroll > 0) ? L->unroll : d.unroll;
+  // W_hat written over the gradient (the runtime's staging-in-gradient): no
+  // non-coherent (.nc) gradient loads on memory this launch writes
+  if (cache == 2 && a.out != nullptr && a.out == a.g) cache = 1;
   if (block % 32 != 0 || block > 512) return PO_EINVAL;
   if (unroll != 1 && unroll != 2 && unroll != 4 && unroll != kPrefetch) return PO_EINVAL;
   if (vec != 8 && vec != 4 && vec != 1) return PO_EINVAL;

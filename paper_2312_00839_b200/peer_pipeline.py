@@ -42,6 +42,7 @@ from .runtime import (
     _StageRt,
     _to_device,
     capture,
+    staging_in_grad_ok,
 )
 from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
 from .stages import loss_and_grad
@@ -283,6 +284,8 @@ class PeerStageRunner:
         rt = _StageRt(st, self.opt, self.depth)
         if self.fused_dp is not None:
             self.fused_dp.adopt(st, self.opt, rt)  # shard mode: peer-mapped W, state, W_hat
+        else:  # W_hat in the gradient's storage (runtime._StageRt)
+            rt.alias_grad = staging_in_grad_ok(st, policy.predictive, self.tl.micro_per_mini)
         st.version = 1
         work = [op for op in self.program if op.kind != UPDATE]
         flags = torch.ones(len(work), dtype=torch.bool, device=self.device)

@@ -33,6 +33,7 @@ from .runtime import (
     _StageRt,
     _to_device,
     capture,
+    staging_in_grad_ok,
 )
 from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
 from .stages import StageModel, loss_and_grad
@@ -408,6 +409,8 @@ class PipelineStageRunner:
             stage.set_grad_buffer(fused_dp.grad)
             fused_dp.adopt(stage, opt, self.rt)  # shard mode: peer-mapped W, state, W_hat
             self._scratch = None
+        else:  # W_hat in the gradient's storage (runtime._StageRt)
+            self.rt.alias_grad = staging_in_grad_ok(stage, self.predictive, self.micros)
         opt.eager_checks = self.eager
         # graphed=True: every op's device work is captured once per (kind,
         # stash slot) into a CUDA graph and replayed (the eager per-op Python

@@ -46,3 +46,28 @@ def test_capture_guard_collects_and_disables_gc(monkeypatch):
         pass
     assert seen == {"mode": "thread_local", "enabled_inside": False}
     assert gc.isenabled()
+
+
+def test_staging_in_gradient_only_where_exact():
+    """runtime.staging_in_grad_ok: W_hat may live in the gradient's storage
+    only for predictive 1F1B, one micro-batch, MLP stages, switch on."""
+    import numpy as np
+
+    from paper_2312_00839_b200 import runtime
+    from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers
+
+    st = StageModel(0, partition_layers(build_layers([4, 3, 2], ["relu", "linear"]), 1)[0],
+                    lambda sp: (np.zeros((sp.in_dim, sp.out_dim)), np.zeros((1, sp.out_dim))), "cpu")
+    assert runtime.staging_in_grad_ok(st, True, 1)
+    assert not runtime.staging_in_grad_ok(st, False, 1)  # live policies never predict
+    assert not runtime.staging_in_grad_ok(st, True, 4)  # micro-batches accumulate into the gradient
+    assert not runtime.staging_in_grad_ok(object(), True, 1)  # module stages may save weight views
+    runtime.STAGING_IN_GRAD = False
+    try:
+        assert not runtime.staging_in_grad_ok(st, True, 1)
+    finally:
+        runtime.STAGING_IN_GRAD = True
+    rt = runtime._StageRt(st, None, 1, alias_grad=True)
+    assert rt.staging_buffer() is st.flat.grad
+    st.set_grad_buffer(st.flat.grad.clone())  # follows a re-pointed gradient
+    assert rt.staging_buffer() is st.flat.grad

@@ -96,3 +96,67 @@ def test_graphed_stage_streams_equal_graphed_serial(strategy, kind):
     assert out["serial"][0] == out["stage"][0]
     for x, y in zip(out["serial"][1], out["stage"][1]):
         assert torch.equal(x, y)
+
+
+@pytest.fixture
+def separate_staging():
+    """runtime.STAGING_IN_GRAD = False for the duration of a test."""
+    from paper_2312_00839_b200 import runtime
+
+    runtime.STAGING_IN_GRAD = False
+    yield
+    runtime.STAGING_IN_GRAD = True
+
+
+def _run_both(case, streams, fuse=True, checks="eager"):
+    from paper_2312_00839_b200 import runtime
+
+    runtime.STAGING_IN_GRAD = False
+    try:
+        a = _run(case, streams, checks=checks, fuse=fuse)
+    finally:
+        runtime.STAGING_IN_GRAD = True
+    return a, _run(case, streams, checks=checks, fuse=fuse)
+
+
+@pytest.mark.parametrize("case", [c for c in SMALL + CONFIG1 if c["strategy"] == "optimizer_prediction"],
+                         ids=lambda c: f"{c['name']}-D{c['depth']}-{c['kind']}")
+@pytest.mark.parametrize("streams,fuse", [("serial", True), ("stage", True), ("stage", False)])
+def test_staging_in_gradient_storage_is_exact(case, streams, fuse):
+    """W_hat written over the dead gradient (runtime.STAGING_IN_GRAD, the
+    default) == a separate staging buffer, bit for bit: records, losses,
+    weights — fused K3 and K1 predictions, serial and stage streams."""
+    (a, sa), (b, sb) = _run_both(case, streams, fuse=fuse, checks="deferred" if case in CONFIG1 else "eager")
+    _same(a, sa, b, sb)
+
+
+def test_staging_in_gradient_storage_graphed(separate_staging):
+    """The same for CUDA-graph replays (config-1-shaped MLP, stage streams)."""
+    import torch
+
+    from paper_2312_00839_b200 import runtime
+    from paper_2312_00839_b200.bench_pipeline import DeviceBatches
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import GraphedExecute, build_timeline
+    from paper_2312_00839_b200.stages import build_layers, build_stages, torch_init
+
+    dev = torch.device("cuda", 0)
+    dims, acts = [512, 384, 384, 256, 10], ["relu", "relu", "relu", "linear"]
+    data = DeviceBatches(torch, dev, dims=dims)
+    tl = build_timeline("optimizer_prediction", 4, 12)
+    out = {}
+    for alias in (False, True):
+        runtime.STAGING_IN_GRAD = alias
+        stages = build_stages(build_layers(dims, acts), 4, torch_init(3, dev), device=dev)
+        opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=dev) for s in stages]
+        g = GraphedExecute(tl, stages, opts, "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-3,
+                           streams="stage")
+        losses = []
+        for _ in range(3):
+            g.replay()
+            losses.append(g.report().losses)
+        torch.cuda.synchronize()
+        out[alias] = (losses, [s.flat.data.clone() for s in stages])
+    assert out[False][0] == out[True][0]
+    for x, y in zip(out[False][1], out[True][1]):
+        assert torch.equal(x, y)
