@@ -289,6 +289,25 @@ int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h,
  * forward that consumed it, or a gradient after the update that consumed it. */
 int po_l2_discard(void* p, int64_t bytes, void* stream);
 
+/* ---- weight gradient + update in one kernel (pipeoptim_wgrad.cu) --------
+ * g = x^T @ dpre for one MLP layer (x: rows x in, row-major, leading dim
+ * ldx; dpre: rows x out, ldd) on the tcgen05 tensor cores (each fp32 operand
+ * split into three bf16 pieces, fp32 accumulation in TMEM), never written to
+ * memory unless g_out is given: the epilogue applies K3 (w_hat non-NULL) or
+ * K2 (w_hat NULL) to the (in x out) row-major weight tensor w and its state
+ * (same shape, 32-byte aligned) with the step / prediction coefficients of
+ * po_step_predict / po_step (coef_dev non-NULL: from device memory, as the
+ * _dc forms). nonfinite_index gets flat_offset + the smallest non-finite
+ * index (atomicMin), flat_offset being the tensor's offset in the stage's flat
+ * buffer. Shapes: rows % 16 == 0, in % 128 == 0, out % 128 == 0
+ * (po_wgrad_update_supported). Replaces the weight-gradient GEMM of
+ * stage_backward (stages.py:203) followed by the update (runtime.py:449-463). */
+int po_wgrad_update_supported(int64_t rows, int64_t in, int64_t out);
+int po_wgrad_update(const po_hparams* hp, const float* x, int64_t ldx, const float* dpre, int64_t ldd, int64_t rows,
+                    int64_t in, int64_t out, float* w, float* state1, float* state2, float* w_hat, float* g_out,
+                    double lr, double lr_pred_times_s, int64_t step_count, const po_coef* coef_dev,
+                    int64_t* nonfinite_index, int64_t flat_offset, void* stream);
+
 /* ---- FP32-accurate tensor-core GEMM (pipeoptim_gemm.cu) -----------------
  * D[l] = A[l] @ B[l] for l < batch, fp32 in/out, computed by tcgen05 UMMA with
  * each fp32 operand split into three bf16 pieces (CUTLASS SM100 fast-FP32

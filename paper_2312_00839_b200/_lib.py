@@ -51,6 +51,8 @@ EXPORTS = (
     "po_nvls_bind",
     "po_nvls_size",
     "po_nvls_free",
+    "po_wgrad_update_supported",
+    "po_wgrad_update",
     "po_gemm_f32x3",
     "po_gemm_f32x3_available",
     "po_p2p_send",
@@ -159,6 +161,9 @@ _SIGNATURES = {
     "po_nvls_bind": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]),
     "po_nvls_size": (_I64, [_P]),
     "po_nvls_free": (ctypes.c_int, [_P]),
+    "po_wgrad_update_supported": (ctypes.c_int, [_I64, _I64, _I64]),
+    "po_wgrad_update": (ctypes.c_int, [_HP, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _D, _D, _I64,
+                                       _P, _P, _I64, _P]),
     "po_gemm_f32x3": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
                                      _I64, _I64, _P, _I64, _P]),
     "po_gemm_f32x3_available": (ctypes.c_int, []),

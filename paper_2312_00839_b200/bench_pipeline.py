@@ -115,12 +115,27 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
     opt._bind(st.flat.layout)
     opt._ensure_state()
 
+    from . import stages as _stages
+    from .stages import StageModel
+
+    defer = _stages.FUSE_WGRAD_UPDATE and isinstance(st, StageModel)  # as the runners do
+
     def unit():
         out = st.run_forward(fwd_weights, (0, 0), x, 1, check_finite=False)
         g = loss_and_grad(out, y0, loss_kind)[1] if last else g_last
-        st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0)
+        if defer:
+            st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0, defer_wgrad=True)
+            wg = st.take_deferred_wgrad()
+        else:
+            st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0)
+            wg = []
         if predictive and not last:
-            opt.step_predict_(st.flat, 1e-4, 1e-4, depth - k - 1, staging)
+            if wg:
+                opt.step_fused_(st.flat, 1e-4, 1e-4, depth - k - 1, staging, wg)
+            else:
+                opt.step_predict_(st.flat, 1e-4, 1e-4, depth - k - 1, staging)
+        elif wg:
+            opt.step_fused_(st.flat, 1e-4, 0.0, 0, None, wg)
         else:
             opt.step_(st.flat, 1e-4)
 

@@ -248,6 +248,7 @@ class OptimizerState:
         self._s1: torch.Tensor | None = None  # sgdm buf | adam exp_avg
         self._s2: torch.Tensor | None = None  # adam exp_avg_sq
         self._bad: torch.Tensor | None = None
+        self._seg_flags: dict[int, torch.Tensor] = {}  # step_fused_ segment starts -> non-finite flags
         self._hp = config.hparams()
         self._launch = launch
         self._lib = _lib.load()
@@ -336,6 +337,11 @@ class OptimizerState:
         if self._bad is None:
             return
         idx = int(self._bad.item())
+        for lo, flag in self._seg_flags.items():  # segment launches of step_fused_
+            j = int(flag.item())
+            if j != _INT64_MAX:
+                flag.fill_(_INT64_MAX)
+                idx = min(idx, lo + j)
         if idx != _INT64_MAX:
             self._bad.fill_(_INT64_MAX)
             name = self._layout.locate(idx)
@@ -422,6 +428,90 @@ class OptimizerState:
             AUDIT.after(tok, lr, lr_pred, steps_ahead)
         self._after_step()
         self.step_count += 1
+
+    def step_fused_(self, flat: FlatParams, lr: float, lr_pred: float, steps_ahead: int,
+                    out: torch.Tensor | None, wgrad: list) -> None:
+        """step_ (out None) or step_predict_ whose weight gradients for the
+        params in `wgrad` — (param index, x, dpre) left by
+        stage_backward(defer_wgrad=True) — are formed inside the update:
+        po_wgrad_update computes x^T @ dpre on the tensor cores and applies
+        K2/K3 in its epilogue; the other params (biases, unfused weights) go
+        through K2/K3 from flat.grad, segment by segment. Same coefficients,
+        same per-element rule, one step_count increment."""
+        if steps_ahead < 0:
+            raise ValueError(f"steps_ahead must be >= 0, got {steps_ahead}")
+        self._bind(flat.layout)
+        self._ensure_state()
+        lay, dev = flat.layout, flat.data.device
+        stream = _stream(dev)
+        which = _lib.PO_COEF_STEP if out is None else _lib.PO_COEF_STEP_PREDICT
+        coef = self.tape.record(self, which, lr, lr_pred, steps_ahead) if self.tape is not None else None
+        c_pred = 0.0 if out is None else float(lr_pred) * steps_ahead
+        hp = ctypes.byref(self._hp)
+        fused = {}
+        for idx, x, dpre in wgrad:
+            fused[idx] = (x, dpre)
+        for i, (o, n) in enumerate(zip(lay.offsets, lay.sizes)):
+            if i not in fused:
+                continue
+            x, dpre = fused[i]
+            rows, fin = x.shape
+            fout = dpre.shape[1]
+            rc = self._lib.po_wgrad_update(
+                hp, _ptr(x), fin, _ptr(dpre), fout, rows, fin, fout, flat.data.data_ptr() + 4 * o,
+                self._s1.data_ptr() + 4 * o, None if self._s2 is None else self._s2.data_ptr() + 4 * o,
+                None if out is None else out.data_ptr() + 4 * o, None, float(lr), c_pred, self.step_count, coef,
+                _ptr(self._bad), o, stream)
+            _lib.check(rc, "po_wgrad_update")
+        # the remaining params: maximal runs of consecutive non-fused params (padding included)
+        i, k = 0, len(lay.offsets)
+        while i < k:
+            if i in fused:
+                i += 1
+                continue
+            j = i
+            while j + 1 < k and (j + 1) not in fused:
+                j += 1
+            lo = lay.offsets[i]
+            hi = lay.offsets[j + 1] if j + 1 < k else lay.numel
+            self._segment(flat, lo, hi - lo, lr, c_pred, out, coef, stream)
+            i = j + 1
+        if self.tape is None:
+            self._after_step()
+        self.step_count += 1
+
+    def _segment(self, flat, lo, n, lr, c_pred, out, coef, stream) -> None:
+        """K2/K3 on flat[lo : lo + n]. The kernels report a non-finite index
+        relative to the launch, so each segment start has its own flag
+        (`_seg_bad`), mapped back to the flat index by check_finite."""
+        if n <= 0:
+            return
+        off = 4 * lo
+        hp = ctypes.byref(self._hp)
+        w, g, s1 = flat.data.data_ptr() + off, flat.grad.data_ptr() + off, self._s1.data_ptr() + off
+        s2 = None if self._s2 is None else self._s2.data_ptr() + off
+        bad = self._seg_bad(lo)
+        if out is None:
+            if coef is not None:
+                rc = self._lib.po_step_dc(hp, w, g, s1, s2, n, coef, bad, self._launch_ref(), stream)
+            else:
+                rc = self._lib.po_step(hp, w, g, s1, s2, None, n, float(lr), self.step_count, bad,
+                                       self._launch_ref(), stream)
+        else:
+            o = out.data_ptr() + off
+            if coef is not None:
+                rc = self._lib.po_step_predict_dc(hp, w, g, s1, s2, o, n, coef, bad, self._launch_ref(), stream)
+            else:
+                rc = self._lib.po_step_predict(hp, w, g, s1, s2, o, n, float(lr), c_pred, self.step_count, bad,
+                                               self._launch_ref(), stream)
+        _lib.check(rc, "po_step (segment)")
+
+    def _seg_bad(self, lo: int) -> int:
+        if lo == 0:
+            return _ptr(self._bad)
+        if lo not in self._seg_flags:
+            self._seg_flags[lo] = torch.full((1,), _INT64_MAX, dtype=torch.int64, device=self.device)
+        return self._seg_flags[lo].data_ptr()
 
     def _launch_ref(self):
         return ctypes.byref(self._launch) if self._launch is not None else None

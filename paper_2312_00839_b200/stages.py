@@ -194,8 +194,14 @@ class StageModel:
     def run_forward(self, weights, key, x, version, check_finite=True, finite_flags=None, flag_index=0):
         return stage_forward(self, weights, key, x, version, check_finite, finite_flags, flag_index)
 
-    def run_backward(self, weights, key, grad_out, accumulate=False, need_input_grad=True):
-        return stage_backward(self, weights, key, grad_out, accumulate, need_input_grad)
+    def run_backward(self, weights, key, grad_out, accumulate=False, need_input_grad=True, defer_wgrad=False):
+        return stage_backward(self, weights, key, grad_out, accumulate, need_input_grad, defer_wgrad)
+
+    def take_deferred_wgrad(self) -> list:
+        """The (param index, x, dpre) the last backward left for the update."""
+        d = getattr(self, "deferred_wgrad", None) or []
+        self.deferred_wgrad = []
+        return d
 
 
 def build_stages(layers: list[LayerSpec], depth: int, init: InitFn, device=None) -> list[StageModel]:
@@ -457,8 +463,26 @@ def record_finite(t: torch.Tensor, flags: torch.Tensor, index: int) -> None:
         flags[index] = torch.isfinite(t).all()
 
 
+# Weight gradients of MLP layers fused into the update that follows the
+# backward (po_wgrad_update, a tcgen05 GEMM with K2/K3 in its epilogue):
+# stage_backward(defer_wgrad=True) leaves those layers' dW uncomputed and
+# records (param index, x, dpre) in stage.deferred_wgrad for
+# OptimizerState.step_fused_. Off by default: measured no faster than the
+# split-K GEMM + K3 at config 1's shapes (csrc/pipeoptim_wgrad.cu header,
+# profiles/r2_wgrad_fused_bench.jsonl); True runs it (tests cover both).
+FUSE_WGRAD_UPDATE = False
+
+
+def _wgrad_fusable(x: torch.Tensor, dpre: torch.Tensor, gw: torch.Tensor) -> bool:
+    from . import _lib
+
+    return (x.is_cuda and x.dtype == torch.float32 and dpre.dtype == torch.float32 and x.is_contiguous()
+            and dpre.is_contiguous() and gw.is_contiguous()
+            and _lib.load().po_wgrad_update_supported(x.shape[0], x.shape[1], dpre.shape[1]) == 1)
+
+
 def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
-                   accumulate: bool = False, need_input_grad: bool = True):
+                   accumulate: bool = False, need_input_grad: bool = True, defer_wgrad: bool = False):
     """Backpropagate through the stash (stages.py:187-209). Parameter grads go
     into stage.flat.grad's views (overwritten, or added when `accumulate`);
     the input gradient uses `weights` — the view at BACKWARD time.
@@ -466,8 +490,16 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
 
     On the device an input gradient that feeds a ReLU layer stays as its
     split-K partial products: po_relu_bwd_bias sums them (fixed order) in the
-    same launch that applies the ReLU mask and forms the bias gradient."""
+    same launch that applies the ReLU mask and forms the bias gradient.
+
+    defer_wgrad (the caller runs the stage's update next, nothing reads the
+    gradient in between): the weight gradients of the ReLU / linear layers
+    whose shapes po_wgrad_update handles are not computed here; their
+    (param index, x, dpre) go to stage.deferred_wgrad for
+    OptimizerState.step_fused_, which forms them on the tensor cores inside
+    the update."""
     entry = stage.stash.pop(key)
+    stage.deferred_wgrad = []
     gviews = stage.flat.grads
     if not grad_out.is_cuda:
         return _stage_backward_host(stage, entry, weights, gviews, grad_out, accumulate, need_input_grad)
@@ -488,7 +520,10 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
             rc = lib.po_act_bwd_bias(int(relu), g.data_ptr(), splits, entry.pre_acts[i].data_ptr() if relu else None,
                                      rows, cols, dpre.data_ptr(), gb.data_ptr(), int(accumulate), stream)
             _lib.check(rc, "po_act_bwd_bias")
-            _weight_grad(x, dpre, gw, accumulate)
+            if defer_wgrad and not accumulate and FUSE_WGRAD_UPDATE and _wgrad_fusable(x, dpre, gw):
+                stage.deferred_wgrad.append((2 * i, x, dpre))
+            else:
+                _weight_grad(x, dpre, gw, accumulate)
         else:
             gfull = g[0] if g.shape[0] == 1 else _splitk_reduce(g, None, "linear")
             dpre = _activation_grad_mul(gfull, entry.pre_acts[i], spec.activation)
