@@ -120,6 +120,11 @@ __device__ __forceinline__ uint32_t core_off(int r, int g) {
 }
 
 __device__ __forceinline__ void split_store(const float (&v)[8], uint8_t* base, uint32_t off, int piece) {
+#ifdef PO_PROBE_NO_SPLIT  // timing probe only: the operand split's cost (results are wrong)
+  *reinterpret_cast<uint4*>(base + off) = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                                     __float_as_uint(v[2]), __float_as_uint(v[3]));
+  return;
+#endif
   uint32_t p0[4], p1[4], p2[4];
 #pragma unroll
   for (int j = 0; j < 8; j += 2) {

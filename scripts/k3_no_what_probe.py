@@ -16,22 +16,26 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-PROBE = ROOT / "paper_2312_00839_b200" / "build" / "probe" / "libpipeoptim_no_what.so"
+PROBE_DIR = ROOT / "paper_2312_00839_b200" / "build" / "probe"
+PROBE = PROBE_DIR / "libpipeoptim_no_what.so"
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--build", action="store_true")
+ap.add_argument("--define", default="PO_PROBE_K3_NO_WHAT", help="probe macro (build); the library name follows it")
 ap.add_argument("--probe", action="store_true")
 a = ap.parse_args()
 if a.build:
     from paper_2312_00839_b200 import build as b
 
+    PROBE = PROBE_DIR / ("libpipeoptim_no_what.so" if a.define == "PO_PROBE_K3_NO_WHAT" else
+                         f"libpipeoptim_{a.define.lower()}.so")
     cut = b.cutlass_root()
     objs = []
     PROBE.parent.mkdir(parents=True, exist_ok=True)
     for src in b.sources(cut):
-        obj = PROBE.parent / (src.stem + "_nw.o")
+        obj = PROBE.parent / (src.stem + "_" + a.define.lower() + ".o")
         extra = b._cutlass_include(cut) if src.name == b.GEMM_TU else []
-        cmd = [b.nvcc_path(), *b.ARCH_FLAGS, *b.NVCC_FLAGS, f"-I{b.INCLUDE}", *extra, "-DPO_PROBE_K3_NO_WHAT", "-c",
+        cmd = [b.nvcc_path(), *b.ARCH_FLAGS, *b.NVCC_FLAGS, f"-I{b.INCLUDE}", *extra, f"-D{a.define}", "-c",
                "-o", str(obj), str(src)]
         if src.suffix == ".cpp":
             cmd[1:1] = ["-x", "cu"]
