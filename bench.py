@@ -498,6 +498,28 @@ def e2e_leg(args, torch, dist, world, device):
     torch.cuda.synchronize(device)
     ms_list = (time.perf_counter() - t_l) / l_steps * 1e3
     del lopt
+    # the e2e step's own bound, measured: the same 8 B/param in and 8 B/param
+    # out as two plain copies per direction on two streams at once (pinned
+    # host <-> device, no kernel)
+    d_a, d_b = torch.empty(n, device=device), torch.empty(n, device=device)
+    s_in, s_out = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    torch.cuda.synchronize(device)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for st_ in (s_in, s_out):
+        st_.wait_stream(torch.cuda.current_stream(device))
+    with torch.cuda.stream(s_in):
+        d_a.copy_(w_h, non_blocking=True)
+        d_b.copy_(g_h, non_blocking=True)
+    with torch.cuda.stream(s_out):
+        wo_h.copy_(d_b, non_blocking=True)
+        wh_h.copy_(d_a, non_blocking=True)
+    for st_ in (s_in, s_out):
+        torch.cuda.current_stream(device).wait_stream(st_)
+    p1.record()
+    torch.cuda.synchronize(device)
+    ms_pcie = p0.elapsed_time(p1)
+    del d_a, d_b
     # `e2e` is the reference-shaped round trip: the caller's W and G come from
     # pinned host memory every step and W' and W_hat go back (one fused K3
     # call, HostStreamer.step_predict); the training-loop setting with W, m, v
@@ -513,6 +535,12 @@ def e2e_leg(args, torch, dist, world, device):
         "path": "OptimizerState + HostStreamer.step_predict: pinned host W, G -> device (chunked) -> K3 against "
                 "device-resident m, v -> W', W_hat -> pinned host (H2D and D2H streams overlapped)",
         "launches": launches[0],
+        "pcie_bound": {
+            "ms_per_step": round(ms_pcie, 3),
+            "frac": round(ms_pcie / ms, 4),
+            "how": "the step's bytes (8 B/param H2D + 8 B/param D2H) as plain pinned copies, both directions at "
+                   "once, no kernel: frac = that time / the e2e step time",
+        },
         "grad_in_state_resident": {
             "value": round(world * BYTES_PER_PARAM[kind] * n / (ms_res * 1e-3) / 1e9, 2),
             "unit": "GB/s",

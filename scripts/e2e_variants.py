@@ -46,3 +46,24 @@ for name, fn in (("h2d", lambda: d.copy_(w, non_blocking=True)), ("d2h", lambda:
     e1.record()
     torch.cuda.synchronize()
     print(json.dumps({name: round(4 * n / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)}), flush=True)
+# both directions at once (the e2e step's bound: 8 B/param each way)
+d2 = torch.empty(n, device=dev)
+s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+s_in.wait_stream(torch.cuda.current_stream())
+s_out.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s_in):
+    d.copy_(w, non_blocking=True)
+    d2.copy_(g, non_blocking=True)
+with torch.cuda.stream(s_out):
+    wo.copy_(d2, non_blocking=True)
+    wh.copy_(d, non_blocking=True)
+torch.cuda.current_stream().wait_stream(s_in)
+torch.cuda.current_stream().wait_stream(s_out)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1)
+print(json.dumps({"bidirectional_8B_each_way_ms": round(ms, 1),
+                  "bidirectional_gbs_per_dir": round(8 * n / (ms * 1e-3) / 1e9, 1)}), flush=True)
