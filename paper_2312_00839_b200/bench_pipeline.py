@@ -452,7 +452,11 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
                      f"CUDA-graph replay of whole {n_batches}-mini-batch runs), batch {cfg['batch']}, "
                      f"{cfg['opt']} lr {lr}, "
                      f"{'bf16 autocast' if amp == 'bf16' else 'TF32' if tf32 else 'fp32'} convs/GEMMs, "
-                     f"fp32 master weights"}
+                     f"fp32 master weights",
+           "data": f"synthetic, throughput only: {len(data.x)} random batches cycled, so final_loss measures "
+                   f"memorisation, not convergence (the reference has no conv/LSTM stages: loss parity is "
+                   f"unpinned, SURVEY.md 8(c)); GNMT-8 is an LSTM stack with a last-position vocabulary head, "
+                   f"no attention"}
     try:
         graphs = {}
         for strategy in ("async_raw", "optimizer_prediction"):
