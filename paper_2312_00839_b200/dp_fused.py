@@ -43,14 +43,19 @@ import torch
 from . import _lib
 
 
-def send_fd(dist, group, rank: int, size: int, fd):
+def send_fd(dist, group, rank: int, size: int, fd, error: str | None = None):
     """Pass a file descriptor from replica 0 to replicas 1..size-1 of `group`
     over an abstract UNIX socket (SCM_RIGHTS); returns the received fd on the
     others (a new descriptor the caller owns), None on replica 0. Used for
-    the NVLS multicast object's POSIX handle."""
-    token = [os.urandom(8).hex() if rank == 0 else None]
+    the NVLS multicast object's POSIX handle. Replica 0 passes `error`
+    instead of a descriptor when it could not make one: every replica then
+    raises it (nobody is left waiting on the socket)."""
+    token = [(os.urandom(8).hex(), error) if rank == 0 else None]
     dist.broadcast_object_list(token, src=_group_src(dist, group), group=group)
-    name = f"\0pipeoptim-fd-{os.getuid()}-{token[0]}"
+    tok, err = token[0]
+    if err is not None:
+        raise RuntimeError(f"replica 0 could not share the handle: {err}")
+    name = f"\0pipeoptim-fd-{os.getuid()}-{tok}"
     if rank == 0:
         with socket.socket(socket.AF_UNIX, socket.SOCK_STREAM) as srv:
             srv.bind(name)
@@ -179,7 +184,10 @@ class FusedDPGroup:
         h = ctypes.c_void_p()
         if self.dp_rank == 0:
             fd = ctypes.c_int32(-1)
-            _lib.check(lib.po_nvls_create(self.dp_size, total, ctypes.byref(fd), ctypes.byref(h)), "po_nvls_create")
+            rc = lib.po_nvls_create(self.dp_size, total, ctypes.byref(fd), ctypes.byref(h))
+            if rc != 0:  # tell the other replicas before raising (they wait in send_fd)
+                err = f"po_nvls_create: {lib.po_strerror(rc).decode()} (rc {rc})"
+                send_fd(dist, group, self.dp_rank, self.dp_size, None, error=err)
             send_fd(dist, group, self.dp_rank, self.dp_size, fd.value)
             os.close(fd.value)
         else:

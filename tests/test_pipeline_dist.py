@@ -340,6 +340,36 @@ def _fd_worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
+def _fd_error_worker(rank, world, port, out_dir):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2312_00839_b200.dp_fused import send_fd
+
+        try:
+            send_fd(dist, None, rank, world, None, error="no multicast" if rank == 0 else None)
+            msg = "returned"
+        except RuntimeError as exc:
+            msg = str(exc)
+        Path(out_dir, f"err{rank}.txt").write_text(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fd_passing_propagates_replica0_failure(tmp_path):
+    """If replica 0 cannot create the handle, every replica raises its error
+    instead of waiting on the socket."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_fd_error_worker, args=(3, free_port(), str(tmp_path)), nprocs=3, join=True)
+    for r in range(3):
+        assert "no multicast" in (tmp_path / f"err{r}.txt").read_text()
+
+
 def test_fd_passing_for_nvls_handles(tmp_path):
     """dp_fused.send_fd: replica 0's POSIX fd (the NVLS multicast object's
     exported handle on a GPU box; a pipe here) reaches every other replica
