@@ -604,6 +604,11 @@ def pipeline_leg(args, torch, dist, rank, world, device):
         progress("projected 8-GPU")
         out["depth_sweep_1gpu"] = bp.depth_sweep(torch, device, n_batches=args.pipeline_batches)
         progress("depth sweep")
+        try:
+            out["strategies"] = bp.strategy_comparison(torch, device, n_batches=args.pipeline_batches)
+        except Exception as exc:
+            out["strategies"] = {"error": f"{type(exc).__name__}: {exc}"}
+        progress("weight-policy comparison")
         out["gpipe"] = {}
         for name, nb in (("config1", args.pipeline_batches), ("config2_vgg16", 32), ("config3_resnet101", 16)):
             try:

@@ -606,3 +606,46 @@ def gpipe_comparison(torch, device, name: str = "config1", n_batches: int = 64, 
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
     return out
+
+
+def strategy_comparison(torch, device, n_batches: int = 64, trials: int = 5):
+    """SURVEY.md §8(f) rows 1-2 at the same measurement bar as the headline:
+    config 1 (fp32, Adam lr 1e-4, D = 4, stage-concurrent whole-run CUDA
+    graphs on one GPU, replayed in alternation) under every 1F1B weight
+    policy — async_raw (no prediction), PipeDream weight stashing, PipeDream
+    2BW, PipeOptim — plus GPipe (T = 4): samples/s, the weight-version memory
+    peaks of the reference's report (snapshot_peaks, runtime.py:66-154) and
+    the run's final loss."""
+    import statistics
+
+    from .optim import OptimizerConfig, OptimizerState
+    from .runtime import GraphedExecute, build_timeline
+    from .stages import build_layers, build_stages, torch_init
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    data = DeviceBatches(torch, device)
+    graphs = {}
+    try:
+        for strategy, t in (("async_raw", 1), ("weight_stashing", 1), ("two_buffered", 1),
+                            ("optimizer_prediction", 1), ("gpipe", 4)):
+            st = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), 4, torch_init(0, device), device=device)
+            opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=device) for s in st]
+            g = GraphedExecute(build_timeline(strategy, 4, n_batches, t), st, opts, strategy, data, "softmax_xent",
+                               lambda mb: 1e-4, warmup_runs=1, streams="stage")
+            g.replay()
+            torch.cuda.synchronize(device)
+            graphs[strategy] = g
+        times = {s: [] for s in graphs}
+        for _ in range(trials):
+            for s, g in graphs.items():
+                times[s].append(_time_replays(torch, device, g, 1))
+        out = {"config": f"config1 MLP {CONFIG1_DIMS}, B={BATCH}, Adam lr 1e-4, D=4 on 1 GPU, {n_batches} "
+                         f"mini-batches per graphed run, one stream per stage, fp32; gpipe T=4"}
+        for s, g in graphs.items():
+            rep = g.report()
+            out[s] = {"samples_per_s": round(n_batches * BATCH / statistics.median(times[s]), 1),
+                      "snapshot_peaks": rep.snapshot_peaks, "final_loss": rep.losses[-1]}
+        return out
+    finally:
+        graphs = None
+        torch.cuda.empty_cache()
