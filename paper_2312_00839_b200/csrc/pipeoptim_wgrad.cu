@@ -313,13 +313,11 @@ __global__ void __launch_bounds__(kThreads, 2) wgrad_update_kernel(const WgradAr
 
 template <int KIND, bool PREDICT>
 cudaError_t launch(const WgradArgs& a, cudaStream_t s) {
-  static bool attr = false;  // per instantiation, set once
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(wgrad_update_kernel<KIND, PREDICT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // the dynamic shared-memory opt-in (> 48 KB), once per instantiation
+  // (thread-safe static initialisation)
+  static const cudaError_t attr = cudaFuncSetAttribute(wgrad_update_kernel<KIND, PREDICT>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  if (attr != cudaSuccess) return attr;
   dim3 grid((unsigned)(a.out / kTN), (unsigned)(a.in / kTM));
   wgrad_update_kernel<KIND, PREDICT><<<grid, kThreads, kSmem, s>>>(a);
   return cudaGetLastError();

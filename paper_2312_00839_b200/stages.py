@@ -477,7 +477,8 @@ def _wgrad_fusable(x: torch.Tensor, dpre: torch.Tensor, gw: torch.Tensor) -> boo
     from . import _lib
 
     return (x.is_cuda and x.dtype == torch.float32 and dpre.dtype == torch.float32 and x.is_contiguous()
-            and dpre.is_contiguous() and gw.is_contiguous()
+            and dpre.is_contiguous() and gw.is_contiguous() and x.data_ptr() % 16 == 0 and dpre.data_ptr() % 16 == 0
+            and gw.data_ptr() % 32 == 0
             and _lib.load().po_wgrad_update_supported(x.shape[0], x.shape[1], dpre.shape[1]) == 1)
 
 
