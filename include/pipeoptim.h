@@ -289,6 +289,21 @@ int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h,
  * forward that consumed it, or a gradient after the update that consumed it. */
 int po_l2_discard(void* p, int64_t bytes, void* stream);
 
+/* ---- narrow output layer (pipeoptim_head.cu) --------------------------
+ * An MLP layer in -> C with C <= 32 and linear activation (config 1's
+ * classifier), x: rows x in, W: in x C, both row-major, contiguous.
+ * po_head_fwd: out (rows x C) = x @ W + b (b nullable); a non-finite output
+ * clears flags[flag_index] (flags nullable) — stages.py:175-178, :182.
+ * po_head_bwd: given g = dL/dout (rows x C): dx = g @ W^T (dx nullable: not
+ * needed), dW = x^T @ g, db = colsum(g), written or (accumulate) added —
+ * stages.py:200-208 for a linear layer. Fixed summation orders
+ * (deterministic). po_head_supported: 1 if the shape is handled. */
+int po_head_supported(int64_t rows, int64_t in, int64_t classes);
+int po_head_fwd(const float* x, int64_t rows, int64_t in, const float* w, const float* b, int32_t classes,
+                float* out, uint8_t* flags, int64_t flag_index, void* stream);
+int po_head_bwd(const float* x, int64_t rows, int64_t in, const float* g, int32_t classes, const float* w, float* dx,
+                float* dw, float* db, int32_t accumulate, void* stream);
+
 /* ---- weight gradient + update in one kernel (pipeoptim_wgrad.cu) --------
  * g = x^T @ dpre for one MLP layer (x: rows x in, row-major, leading dim
  * ldx; dpre: rows x out, ldd) on the tcgen05 tensor cores (each fp32 operand

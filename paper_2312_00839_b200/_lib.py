@@ -51,6 +51,9 @@ EXPORTS = (
     "po_nvls_bind",
     "po_nvls_size",
     "po_nvls_free",
+    "po_head_supported",
+    "po_head_fwd",
+    "po_head_bwd",
     "po_wgrad_update_supported",
     "po_wgrad_update",
     "po_gemm_f32x3",
@@ -161,6 +164,9 @@ _SIGNATURES = {
     "po_nvls_bind": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]),
     "po_nvls_size": (_I64, [_P]),
     "po_nvls_free": (ctypes.c_int, [_P]),
+    "po_head_supported": (ctypes.c_int, [_I64, _I64, _I64]),
+    "po_head_fwd": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, _P, _I64, _P]),
+    "po_head_bwd": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int32, _P]),
     "po_wgrad_update_supported": (ctypes.c_int, [_I64, _I64, _I64]),
     "po_wgrad_update": (ctypes.c_int, [_HP, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _D, _D, _I64,
                                        _P, _P, _I64, _P]),

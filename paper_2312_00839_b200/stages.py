@@ -308,14 +308,36 @@ def _splitk_reduce(part: torch.Tensor, bias, act: str, pre_out=None, flags=None,
     return out
 
 
+# Narrow linear layers (out <= 32: config 1's classifier) on po_head_fwd /
+# po_head_bwd — one launch each way — instead of the library GEMMs (A/B switch)
+FUSED_HEAD = True
+
+
+def _head_ok(h: torch.Tensor, w: torch.Tensor, act: str) -> bool:
+    from . import _lib
+
+    return (FUSED_HEAD and act == "linear" and h.is_cuda and h.dtype == torch.float32 and w.is_contiguous()
+            and _lib.load().po_head_supported(h.shape[0], h.shape[1], w.shape[1]) == 1)
+
+
 def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str, flags=None, flag_index: int = 0):
     """Device forward of one layer: (pre, h_out, checked) with the stash's
     convention — relu layers stash relu(pre) (its sign pattern is pre's),
     others pre. checked: the finiteness flag was already written (split-K
-    epilogue)."""
+    epilogue / head kernel)."""
     rows, k = h.shape
     n = w.shape[1]
     h = h if h.is_contiguous() else h.contiguous()
+    if _head_ok(h, w, act):  # narrow linear layer: one launch (po_head_fwd)
+        from . import _lib
+
+        out = torch.empty((rows, n), dtype=torch.float32, device=h.device)
+        bias = b.reshape(-1)
+        rc = _lib.load().po_head_fwd(h.data_ptr(), rows, k, w.data_ptr(), bias.data_ptr(), n, out.data_ptr(),
+                                     None if flags is None else flags.data_ptr(), flag_index,
+                                     torch.cuda.current_stream(h.device).cuda_stream)
+        _lib.check(rc, "po_head_fwd")
+        return out, out, flags is not None
     tc = n % 4 == 0 and k % 4 == 0 and _tc_ok(h, w)
     s = _splitk_tc(rows, k) if tc else _splitk(rows, k, n)
     if tc:  # tensor-core fp32 GEMM, batch = K slice, into the fused epilogue
@@ -513,6 +535,20 @@ def stage_backward(stage: StageModel, weights, key, grad_out: torch.Tensor,
         spec = stage.layers[i]
         x = entry.layer_inputs[i]
         gw, gb = gviews[2 * i], gviews[2 * i + 1]
+        if spec.activation == "linear" and g.shape[0] == 1 and _head_ok(x, weights[2 * i], "linear") \
+                and gw.is_contiguous():
+            # narrow linear layer: dx, dW, db in one launch (po_head_bwd)
+            rows = x.shape[0]
+            need = i > 0 or need_input_grad
+            dx = torch.empty((rows, x.shape[1]), dtype=torch.float32, device=g.device) if need else None
+            xc = x if x.is_contiguous() else x.contiguous()
+            gc = g[0] if g[0].is_contiguous() else g[0].contiguous()
+            rc = lib.po_head_bwd(xc.data_ptr(), rows, x.shape[1], gc.data_ptr(), gw.shape[1],
+                                 weights[2 * i].data_ptr(), None if dx is None else dx.data_ptr(), gw.data_ptr(),
+                                 gb.data_ptr(), int(accumulate), stream)
+            _lib.check(rc, "po_head_bwd")
+            g = None if dx is None else dx.unsqueeze(0)
+            continue
         if spec.activation in ("relu", "linear"):
             # sum of the partials, dpre = g * act'(pre) and db = colsum(dpre) in one launch
             splits, rows, cols = g.shape
