@@ -190,20 +190,32 @@ class FusedDPGroup:
                 send_fd(dist, group, self.dp_rank, self.dp_size, None, error=err)
             send_fd(dist, group, self.dp_rank, self.dp_size, fd.value)
             os.close(fd.value)
+            rc = 0
         else:
             fd = send_fd(dist, group, self.dp_rank, self.dp_size, None)
-            _lib.check(lib.po_nvls_open(fd, self.dp_size, total, ctypes.byref(h)), "po_nvls_open")
+            rc = lib.po_nvls_open(fd, self.dp_size, total, ctypes.byref(h))
             os.close(fd)
-        self._nvls = h
-        _lib.check(lib.po_nvls_add_device(h), "po_nvls_add_device")
-        dist.barrier(group=group)  # every device is in the team before anyone binds
+        if rc == 0:
+            self._nvls = h
+            rc = lib.po_nvls_add_device(h)
+        self._agree(dist, group, rc, "po_nvls_open / po_nvls_add_device")  # every device is in the team ...
         uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
-        _lib.check(lib.po_nvls_bind(h, ctypes.byref(uc), ctypes.byref(mc)), "po_nvls_bind")
-        dist.barrier(group=group)
+        rc = lib.po_nvls_bind(h, ctypes.byref(uc), ctypes.byref(mc))  # ... before anyone binds
+        self._agree(dist, group, rc, "po_nvls_bind")
         for i, name in enumerate(big):
             self.local[name] = _wrap(uc.value + i * region, self.numel, torch.float32, self.device)
         at = {name: mc.value + i * region for i, name in enumerate(big)}
         self.mc = [_lib.po_dp_multicast(at[g], at["w"], at["s1"], at["s2"], at["w_hat"]) for g in ("grad0", "grad1")]
+
+    def _agree(self, dist, group, rc: int, what: str) -> None:
+        """A collective step: every replica learns whether all succeeded, so
+        a failure raises everywhere instead of leaving peers in a barrier."""
+        codes = [None] * self.dp_size
+        dist.all_gather_object(codes, int(rc), group=group)
+        bad = [(r, c) for r, c in enumerate(codes) if c != 0]
+        if bad:
+            r, c = bad[0]
+            raise RuntimeError(f"{what} failed on replica {r}: {self._lib.po_strerror(c).decode()} (rc {c})")
 
     @property
     def grad(self) -> torch.Tensor:
