@@ -17,7 +17,8 @@
 //      in / out, all of a thread's loads in flight together), split each value
 //      into three bf16 pieces
 //      (a = a0 + a1 + a2 exactly to 24 bits) and store the pieces in shared
-//      memory in the UMMA canonical K-major, no-swizzle layout (8-row x 16-byte
+//      memory (3xTF32 by default: two fp32 pieces, see kTf32) in the UMMA
+//      canonical K-major, no-swizzle layout (8-row x 16-byte
 //      core matrices; LBO 128 B between the two K halves of an MMA, SBO
 //      1 KB + 16 B between 8-row groups, which spreads a warp's stores over
 //      all bank groups);
@@ -32,16 +33,17 @@
 //      the shared per-element rule (pipeoptim_rules.cuh) — every W / m / v /
 //      W_hat access of a half-warp one contiguous 256-byte segment.
 //
-// Measured (scripts/wgrad_kernel_bench.py, graph-timed, L2 warm): config-1
-// stage 0 (128 x 3072 x 1024) 27.3 us vs 26.2 us for the split-K
-// tensor-core GEMM + K3; stages 1-2 (128 x 1024 x 1024) 12.3 vs 12.4 us. The
-// per-CTA phases (operand loads + split, MMAs, update) run back to back with
-// 1.3 waves of CTAs, so the saved gradient round trip (~2 us) is eaten by
-// exposed latency; not adopted (stages.FUSE_WGRAD_UPDATE = False). Variants
-// tried: 128 x 128 tiles (25.7 / 17.6 us: too few CTAs for 1024 x 1024),
-// W / m / v staged by cp.async from the start (36.1 / 12.8 us: one CTA / SM).
-// The result differs from an fp32 GEMM only in summation order (relative
-// error ~1e-7 vs float64, like the CUTLASS fast-FP32 GEMM it replaces).
+// Measured (scripts/wgrad_kernel_bench.py, graph-timed, L2 warm; the
+// variants in profiles/r2_wgrad_fused_bench.jsonl): with the 3xTF32 split,
+// config-1 stage 0 (128 x 3072 x 1024) 23.5 us vs 26.2 us for the split-K
+// tensor-core GEMM + K3, stages 1-2 (128 x 1024 x 1024) 10.4 vs 12.4 us
+// (bf16x3: 27.1 / 12.3 — its in-tile split cost ~6 us). In config 1's
+// single-GPU 1F1B run (profiles/r2_wgrad_fusion_pipeline_ab_3xtf32.jsonl) it
+// lifts prediction-off throughput 6 % but prediction-on only 2 %, the
+// prediction overhead rises from 1.9 % to 5.2 % and the per-stage unit times
+// do not improve, so stages.FUSE_WGRAD_UPDATE stays off by default (and the
+// path is for fp32 runs: with TF32 GEMMs allowed the library TF32 GEMM is
+// cheaper than 3xTF32).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -57,11 +59,26 @@ constexpr int kKC = 64;                        // K chunk staged in shared memor
 constexpr int kThreads = 256;                  // 8 warps: 2 per TMEM lane quadrant
 // 8-row group stride: the (kKC / 8) 128-byte core matrices of a group plus 16
 // bytes, so the 16-byte stores of a warp (rows 4 apart) hit all 8 bank groups
-constexpr uint32_t kSBO = (kKC / 8) * 128 + 16;
-constexpr uint32_t kLBO = 128;                 // K-half stride within one MMA (bytes)
-constexpr int kPieceA = (kTM / 8) * kSBO;      // one bf16 piece of the A chunk (16.25 KB)
-constexpr int kPieceB = (kTN / 8) * kSBO;      // one bf16 piece of the B chunk (8.1 KB)
-constexpr int kOperands = 3 * (kPieceA + kPieceB);  // 73 KB of bf16 operand pieces
+// Operand precision split (compile-time): 3xTF32 (default) — a = big + small
+// with big = tf32(a) and small = a - big exactly, products big*big +
+// big*small + small*big on tcgen05.mma.kind::tf32 — or bf16x3 (three bf16
+// pieces, six products on kind::f16). 3xTF32 costs two instructions per
+// element to split (bf16x3 ~10) and half the MMAs.
+#ifndef PO_WGRAD_BF16X3
+constexpr bool kTf32 = true;
+#else
+constexpr bool kTf32 = false;
+#endif
+constexpr int kPieces = kTf32 ? 2 : 3;
+constexpr int kElemsPerChunk = kTf32 ? 4 : 8;  // operand elements per 16-byte core-matrix row
+constexpr int kMmaK = kTf32 ? 8 : 16;          // K of one MMA (32 bytes of each operand row)
+// 8-row group stride: the core matrices along K plus 16 bytes, so the
+// 16-byte stores of a warp (rows 4 apart) hit all 8 bank groups
+constexpr uint32_t kSBO = (kKC / kElemsPerChunk) * 128 + 16;
+constexpr uint32_t kLBO = 128;                 // K-chunk stride within one MMA (bytes)
+constexpr int kPieceA = (kTM / 8) * kSBO;      // one piece of the A chunk
+constexpr int kPieceB = (kTN / 8) * kSBO;      // one piece of the B chunk
+constexpr int kOperands = kPieces * (kPieceA + kPieceB);  // 99 KB (3xTF32) / 73 KB (bf16x3)
 constexpr int kSmem = kOperands;               // 2 CTAs / SM
 constexpr uint32_t kTmemCols = kTN;            // fp32 accumulator columns
 constexpr int kTS = kTN + 4;                   // epilogue tile row stride (floats)
@@ -93,17 +110,26 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
          ((uint64_t)((kSBO >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-// kind::f16 instruction descriptor (cute::UMMA::InstrDescriptor): D f32 [4,6),
-// A bf16 [7,10), B bf16 [10,13), both K-major, N >> 3 [17,23), M >> 4 [24,29).
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
+// instruction descriptor (cute::UMMA::InstrDescriptor): D f32 [4,6), A and B
+// format [7,10) / [10,13) (1 = BF16, 2 = TF32), both K-major, N >> 3
+// [17,23), M >> 4 [24,29)
+constexpr uint32_t kFmt = kTf32 ? 2u : 1u;
+constexpr uint32_t kIdesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | ((uint32_t)(kTN >> 3) << 17) |
                             ((uint32_t)(kTM >> 4) << 24);
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
-      : "memory");
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  if constexpr (kTf32)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+        : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -119,7 +145,22 @@ __device__ __forceinline__ uint32_t core_off(int r, int g) {
   return (uint32_t)(r >> 3) * kSBO + (uint32_t)g * 128u + (uint32_t)(r & 7) * 16u;
 }
 
-__device__ __forceinline__ void split_store(const float (&v)[8], uint8_t* base, uint32_t off, int piece) {
+// 3xTF32 pieces of 4 consecutive K elements of one operand row: big =
+// tf32(a) (round to nearest), small = a - big (exact in fp32; the MMA reads
+// its top 19 bits)
+__device__ __forceinline__ void split_store_tf32(const float (&v)[4], uint8_t* base, uint32_t off, int piece) {
+  uint32_t big[4], small[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(big[j]) : "f"(v[j]));
+    small[j] = __float_as_uint(__fsub_rn(v[j], __uint_as_float(big[j])));
+  }
+  *reinterpret_cast<uint4*>(base + off) = make_uint4(big[0], big[1], big[2], big[3]);
+  *reinterpret_cast<uint4*>(base + piece + off) = make_uint4(small[0], small[1], small[2], small[3]);
+}
+
+[[maybe_unused]] __device__ __forceinline__ void split_store(const float (&v)[8], uint8_t* base, uint32_t off,
+                                                            int piece) {
 #ifdef PO_PROBE_NO_SPLIT  // timing probe only: the operand split's cost (results are wrong)
   *reinterpret_cast<uint4*>(base + off) = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
                                                      __float_as_uint(v[2]), __float_as_uint(v[3]));
@@ -149,8 +190,8 @@ __device__ __forceinline__ void split_store(const float (&v)[8], uint8_t* base, 
 template <int KIND, bool PREDICT>
 __global__ void __launch_bounds__(kThreads, 2) wgrad_update_kernel(const WgradArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem;                   // 3 pieces of x^T (rows = in)
-  uint8_t* sB = smem + 3 * kPieceA;     // 3 pieces of dpre^T (rows = out)
+  uint8_t* sA = smem;                      // the pieces of x^T (rows = in)
+  uint8_t* sB = smem + kPieces * kPieceA;  // the pieces of dpre^T (rows = out)
   __shared__ __align__(8) uint64_t mma_bar;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -196,8 +237,18 @@ __global__ void __launch_bounds__(kThreads, 2) wgrad_update_kernel(const WgradAr
           ca[j] = u == 0 ? av[j].x : u == 1 ? av[j].y : u == 2 ? av[j].z : av[j].w;
           cb[j] = u == 0 ? bv[j].x : u == 1 ? bv[j].y : u == 2 ? bv[j].z : bv[j].w;
         }
-        split_store(ca, sA, core_off(4 * lane + u, warp), kPieceA);
-        if (bl) split_store(cb, sB, core_off(4 * lane + u, warp), kPieceB);
+        if constexpr (kTf32) {  // two 4-element K chunks (2w, 2w + 1) per row
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float qa[4] = {ca[4 * h], ca[4 * h + 1], ca[4 * h + 2], ca[4 * h + 3]};
+            const float qb[4] = {cb[4 * h], cb[4 * h + 1], cb[4 * h + 2], cb[4 * h + 3]};
+            split_store_tf32(qa, sA, core_off(4 * lane + u, 2 * warp + h), kPieceA);
+            if (bl) split_store_tf32(qb, sB, core_off(4 * lane + u, 2 * warp + h), kPieceB);
+          }
+        } else {
+          split_store(ca, sA, core_off(4 * lane + u, warp), kPieceA);
+          if (bl) split_store(cb, sB, core_off(4 * lane + u, warp), kPieceB);
+        }
       }
     }
     // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
@@ -206,15 +257,18 @@ __global__ void __launch_bounds__(kThreads, 2) wgrad_update_kernel(const WgradAr
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      // (A piece, B piece) products carrying 24-bit accuracy, smallest first
-      const int pa[6] = {2, 1, 0, 1, 0, 0};
-      const int pb[6] = {0, 1, 2, 0, 1, 0};
-      for (int s = 0; s < kc / 16; ++s) {
+      // (A piece, B piece) products carrying fp32-level accuracy, smallest
+      // first: 3xTF32 small*big, big*small, big*big; bf16x3 the six of
+      // a2b0 + a1b1 + a0b2 + a1b0 + a0b1 + a0b0
+      constexpr int kProducts = kTf32 ? 3 : 6;
+      constexpr int pa[6] = {kTf32 ? 1 : 2, kTf32 ? 0 : 1, 0, 1, 0, 0};
+      constexpr int pb[6] = {0, kTf32 ? 1 : 1, kTf32 ? 0 : 2, 0, 1, 0};
+      for (int s = 0; s < kc / kMmaK; ++s) {
 #pragma unroll
-        for (int p = 0; p < 6; ++p) {
+        for (int p = 0; p < kProducts; ++p) {
           const uint64_t da = smem_desc(a0 + (uint32_t)(pa[p] * kPieceA) + (uint32_t)s * 256u);
           const uint64_t db = smem_desc(b0 + (uint32_t)(pb[p] * kPieceB) + (uint32_t)s * 256u);
-          mma_bf16(tmem, da, db, (ch > 0 || s > 0 || p > 0) ? 1u : 0u);
+          mma(tmem, da, db, (ch > 0 || s > 0 || p > 0) ? 1u : 0u);
         }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

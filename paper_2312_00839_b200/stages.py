@@ -489,8 +489,9 @@ def record_finite(t: torch.Tensor, flags: torch.Tensor, index: int) -> None:
 # backward (po_wgrad_update, a tcgen05 GEMM with K2/K3 in its epilogue):
 # stage_backward(defer_wgrad=True) leaves those layers' dW uncomputed and
 # records (param index, x, dpre) in stage.deferred_wgrad for
-# OptimizerState.step_fused_. Off by default: measured no faster than the
-# split-K GEMM + K3 at config 1's shapes (csrc/pipeoptim_wgrad.cu header,
+# OptimizerState.step_fused_. Off by default: 10-16 % faster than the
+# split-K GEMM + K3 per stage at config 1's shapes, but in the 1F1B run it
+# raises the prediction overhead (csrc/pipeoptim_wgrad.cu header,
 # profiles/r2_wgrad_fused_bench.jsonl); True runs it (tests cover both).
 FUSE_WGRAD_UPDATE = False
 
