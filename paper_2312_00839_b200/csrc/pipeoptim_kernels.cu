@@ -551,15 +551,26 @@ __global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t bad = INT64_MAX;
+  // PF (dp <= 2): the software-pipelined loop of K3 — the next vector's
+  // loads (dp gradients, W, state) issued before this vector's arithmetic
+  constexpr bool PF = DP <= 2;
+  Vec<VEC> gr[DP], w{}, s1{}, s2{};
+  auto load = [&](int64_t base, Vec<VEC>(&gr_)[DP], Vec<VEC>& w_, Vec<VEC>& s1_, Vec<VEC>& s2_) {
+#pragma unroll
+    for (int r = 0; r < DP; ++r) gr_[r] = vload<VEC, 1, true>(d.grads[r] + base);
+    w_ = vload<VEC, 1, false>(a.w + base);
+    s1_ = vload<VEC, 1, false>(a.s1 + base);
+    if constexpr (KIND != PO_SGDM) s2_ = vload<VEC, 1, false>(a.s2 + base);
+  };
+  if (PF && tid < nv) load(tid * VEC, gr, w, s1, s2);
   for (int64_t i = tid; i < nv; i += stride) {
     const int64_t base = i * VEC;
-    Vec<VEC> gr[DP];
-#pragma unroll
-    for (int r = 0; r < DP; ++r) gr[r] = vload<VEC, 1, true>(d.grads[r] + base);
-    Vec<VEC> w = vload<VEC, 1, false>(a.w + base);
-    Vec<VEC> s1 = vload<VEC, 1, false>(a.s1 + base);
-    Vec<VEC> s2{};
-    if constexpr (KIND != PO_SGDM) s2 = vload<VEC, 1, false>(a.s2 + base);
+    Vec<VEC> ngr[PF ? DP : 1], nw{}, ns1{}, ns2{};
+    if constexpr (PF) {
+      if (i + stride < nv) load((i + stride) * VEC, ngr, nw, ns1, ns2);
+    } else {
+      load(base, gr, w, s1, s2);
+    }
     Vec<VEC> out;
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
@@ -574,6 +585,13 @@ __global__ void __launch_bounds__(512) po_dp_kernel(const DpArgs d) {
     vstore<VEC, 1>(a.s1 + base, s1);
     if constexpr (KIND != PO_SGDM) vstore<VEC, 1>(a.s2 + base, s2);
     vstore<VEC, 1>(a.out + base, out);
+    if constexpr (PF) {
+#pragma unroll
+      for (int r = 0; r < DP; ++r) gr[r] = ngr[r];
+      w = nw;
+      s1 = ns1;
+      s2 = ns2;
+    }
   }
   const int64_t t = nv * VEC + tid;  // scalar tail
   if (t < a.n) {
@@ -1017,10 +1035,12 @@ static int step_predict_dp_impl(const po_hparams* hp, float* w, const float* con
   while (vec > 1 && !all_aligned(vec * 4)) vec = vec == 8 ? 4 : 1;
   // K3's launch shape for this size (block x CTAs/SM); one vector per stream
   // in flight, dp of them for the gradient
-  // (large sizes: 512 x 1 CTA/SM, the shape the dp = 1 kernel matches K3 with
-  // under ncu, profiles/r2_dp_kernel_dp1_2p28_ncu.csv; no prefetch variant here)
+  // (large sizes: K3's 320 x 1 CTA/SM with the prefetching loop for dp <= 2,
+  // 512 x 1 with one vector in flight above — the dp gradient loads are then
+  // the requests in flight)
   const DefaultShape ds = n < (int64_t(1) << 25) ? default_shape(hp->kind, MODE_STEP_PREDICT, n)
-                                                 : DefaultShape{512, 1, 1, 1};
+                          : dp <= 2             ? DefaultShape{320, 1, 3, 1}
+                                                : DefaultShape{512, 1, 1, 1};
   const int block = ds.block;
   const int64_t nv = n / vec;
   int64_t want = (nv + block - 1) / block;
