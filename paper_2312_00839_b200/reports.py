@@ -105,3 +105,19 @@ def write_run_outputs(report: RunReport, out_dir: Path, steps_per_epoch: int, fm
         (out_dir / "losses.csv").write_text(csv_text(LOSS_CSV_HEADER.split(","), losses))
         (out_dir / "versions.csv").write_text(csv_text(VERSIONS_CSV_HEADER.split(","), versions))
     return out_dir
+
+
+DEVICE_TIMELINE_CSV_HEADER = "stage,kind,mb,micro,start_us,end_us"
+
+
+def write_device_timeline(report: RunReport, path: Path) -> Path:
+    """`device_timeline.csv` of a traced run (execute(..., trace=True)): one
+    row per executed event in the reference's event order, with its start
+    and end on the device clock (µs from the run's first event) — the
+    measured counterpart of the slot timeline (schedule.timeline_csv_text)."""
+    rows = getattr(report, "device_timeline", None)
+    if rows is None:
+        raise ValueError("the report has no device_timeline: run execute(..., trace=True)")
+    path = Path(path)
+    path.write_text(csv_text(DEVICE_TIMELINE_CSV_HEADER.split(","), rows))
+    return path

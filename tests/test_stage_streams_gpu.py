@@ -160,3 +160,36 @@ def test_staging_in_gradient_storage_graphed(separate_staging):
     assert out[False][0] == out[True][0]
     for x, y in zip(out[False][1], out[True][1]):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("streams", ["serial", "stage"])
+def test_traced_run_device_timeline(tmp_path, streams):
+    """execute(trace=True): one device-timed entry per event in the
+    reference's order; within a stage (one stream) events never overlap and
+    follow tl.stage_events(k); the results are those of the untraced run;
+    reports.write_device_timeline writes them."""
+    import torch
+
+    from paper_2312_00839_b200 import reports
+    from paper_2312_00839_b200.runtime import execute
+    from test_runtime_gpu import Source
+
+    case = next(c for c in SMALL if c["depth"] == 4 and c["strategy"] == "optimizer_prediction")
+    a, sa = _run(case, streams)
+    tl, stages, opts = build(case)
+    src = Source(case["data_seed"], case["rows"], case["dims"][0], case["dims"][-1])
+    rep = execute(tl, stages, opts, case["strategy"], src, "mse", lambda mb, lr=case["lr"]: lr, checks="eager",
+                  streams=streams, trace=True)
+    _same(a, sa, rep, stages)
+    tlog = rep.device_timeline
+    assert [(r["stage"], r["kind"], r["mb"], r["micro"]) for r in tlog] == \
+        [(e.stage, e.kind, e.mb, e.micro) for e in tl.events]
+    for k in range(tl.depth):
+        mine = [r for r in tlog if r["stage"] == k]
+        assert [(r["kind"], r["mb"]) for r in mine] == [(e.kind, e.mb) for e in tl.stage_events(k)]
+        for x, y in zip(mine, mine[1:]):
+            assert x["start_us"] <= x["end_us"] <= y["start_us"] + 1e-3
+    out = reports.write_device_timeline(rep, tmp_path / "device_timeline.csv")
+    lines = out.read_text().splitlines()
+    assert lines[0] == reports.DEVICE_TIMELINE_CSV_HEADER and len(lines) == 1 + len(tl.events)
+    torch.cuda.synchronize()
