@@ -449,3 +449,20 @@ def test_ac10_prediction_convergence_two_spirals():
     # device run is held to 3/5 per optimizer and 11/15 overall
     assert all(s >= 4 and a >= 3 for s, a in summary.values()), summary
     assert sum(a for _, a in summary.values()) >= 11, summary
+
+
+def test_ac11_spectrain_is_prediction_under_sgdm():
+    """AC11 (pkg/tests/test_acceptance.py:348-370): SpecTrain's update rule is
+    PipeOptim's under SGD-momentum — the same run gives bit-identical
+    losses, records (flagged predicted with the same targets) and weights —
+    and it refuses other optimizers (runtime.py:381-382)."""
+    case = next(c for c in SMALL if c["depth"] == 4 and c["strategy"] == "optimizer_prediction")
+    case = dict(case, kind="sgdm")
+    a, sa = run_case(dict(case, strategy="optimizer_prediction"))
+    b, sb = run_case(dict(case, strategy="spectrain"))
+    assert a.losses == b.losses
+    assert [r.to_dict() for r in a.records] == [r.to_dict() for r in b.records]
+    for x, y in zip(sa, sb):
+        assert x.flat.data.equal(y.flat.data)
+    with pytest.raises(ValueError):
+        run_case(dict(case, kind="adam", strategy="spectrain"))
