@@ -680,8 +680,6 @@ def bench_config1_pipeline(torch_mod, dist, rank, world, device, n_batches: int 
             torch_mod.cuda.synchronize(device)
             dist.barrier()
             times.append(e0.elapsed_time(e1) / 1e3)
-            if fused is not None:
-                fused.close(dist, groups[k])
         t = torch_mod.tensor([times[-1]], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         out["gpipe_t4"] = {"samples_per_s": round(n_batches * BATCH / float(t.item()), 1), "s": round(float(t.item()), 4)}
@@ -761,8 +759,6 @@ def bench_module_pipeline(torch_mod, dist, rank, world, device, name: str, n_bat
             torch_mod.cuda.synchronize(device)
             dist.barrier()
             times.append(e0.elapsed_time(e1) / 1e3)
-            if fused is not None:
-                fused.close(dist, groups[k])
         t = torch_mod.tensor([times[-1]], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         key = "pred_on" if strategy == "optimizer_prediction" else "pred_off"
