@@ -43,7 +43,12 @@
 // prediction overhead rises from 1.9 % to 5.2 % and the per-stage unit times
 // do not improve, so stages.FUSE_WGRAD_UPDATE stays off by default (and the
 // path is for fp32 runs: with TF32 GEMMs allowed the library TF32 GEMM is
-// cheaper than 3xTF32).
+// cheaper than 3xTF32). A warp-specialised persistent form (one CTA per SM:
+// 4 producer warps, one MMA thread, 4 epilogue warps on two TMEM
+// accumulators, so a tile's update overlaps the next tile's loads and MMAs)
+// was slower — 44.5 / 18.8 us: one CTA's 4 + 4 warps have a quarter of the
+// split throughput and memory parallelism of two 8-warp CTAs — and was
+// dropped.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
