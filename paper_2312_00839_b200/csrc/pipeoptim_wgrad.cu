@@ -43,7 +43,13 @@
 // prediction overhead rises from 1.9 % to 5.2 % and the per-stage unit times
 // do not improve, so stages.FUSE_WGRAD_UPDATE stays off by default (and the
 // path is for fp32 runs: with TF32 GEMMs allowed the library TF32 GEMM is
-// cheaper than 3xTF32). A warp-specialised persistent form (one CTA per SM:
+// cheaper than 3xTF32). With programmatic dependent launch (prologue over
+// the previous kernel's tail) the 1F1B run gains 4.4 % with prediction on
+// (7.4 % off) at a 4.95 % overhead, but the stage-0 unit (the one-stage-per-
+// GPU bound) is still 48 / 51.5 us vs 45 / 47 us unfused: the 384 tiles
+// take 1.3 waves of 2 CTAs / SM, a latency the persistent GEMM + K3 avoid.
+// A 4-warp, 4-CTAs/SM variant (one wave) was slower (26.4 / 12.9 us).
+// A warp-specialised persistent form (one CTA per SM:
 // 4 producer warps, one MMA thread, 4 epilogue warps on two TMEM
 // accumulators, so a tile's update overlaps the next tile's loads and MMAs)
 // was slower — 44.5 / 18.8 us: one CTA's 4 + 4 warps have a quarter of the
@@ -216,6 +222,10 @@ __global__ void __launch_bounds__(kThreads, 2) wgrad_update_kernel(const WgradAr
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
+  // programmatic dependent launch: the set-up above overlapped the previous
+  // kernel's tail; everything it may have written is read only after this
+  // (a no-op when the launch carried no PDL attribute)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int nchunks = (int)((a.rows + kKC - 1) / kKC);
   for (int ch = 0; ch < nchunks; ++ch) {
@@ -306,6 +316,9 @@ __global__ void __launch_bounds__(kThreads, 2) wgrad_update_kernel(const WgradAr
 
   mbar_wait(&mma_bar, (uint32_t)((nchunks - 1) & 1));
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // the next kernel may be scheduled now (its own griddepcontrol.wait still
+  // waits for this grid to complete)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // TMEM -> shared memory: warp w reads lane quadrant w % 4 (32 rows) and
   // column half w / 4; the operand buffers are free once the MMAs completed
   float* tile = reinterpret_cast<float*>(smem);
@@ -370,6 +383,14 @@ __global__ void __launch_bounds__(kThreads, 2) wgrad_update_kernel(const WgradAr
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
 }
 
+// launched with programmatic dependent launch (its prologue — TMEM alloc,
+// barrier init — overlaps the previous kernel), like the library GEMMs
+#ifndef PO_WGRAD_NO_PDL
+constexpr bool kWgradPdl = true;
+#else
+constexpr bool kWgradPdl = false;
+#endif
+
 template <int KIND, bool PREDICT>
 cudaError_t launch(const WgradArgs& a, cudaStream_t s) {
   // the dynamic shared-memory opt-in (> 48 KB), once per instantiation
@@ -377,9 +398,17 @@ cudaError_t launch(const WgradArgs& a, cudaStream_t s) {
   static const cudaError_t attr = cudaFuncSetAttribute(wgrad_update_kernel<KIND, PREDICT>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   if (attr != cudaSuccess) return attr;
-  dim3 grid((unsigned)(a.out / kTN), (unsigned)(a.in / kTM));
-  wgrad_update_kernel<KIND, PREDICT><<<grid, kThreads, kSmem, s>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.out / kTN), (unsigned)(a.in / kTM));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = kWgradPdl ? 1 : 0;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, wgrad_update_kernel<KIND, PREDICT>, a);
 }
 
 bool aligned32(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
