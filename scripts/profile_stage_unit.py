@@ -19,7 +19,12 @@ from paper_2312_00839_b200.stages import build_layers, build_stages, torch_init 
 ap = argparse.ArgumentParser()
 ap.add_argument("--stage", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--fuse-wgrad", action="store_true", help="stages.FUSE_WGRAD_UPDATE on (po_wgrad_update)")
 a = ap.parse_args()
+if a.fuse_wgrad:
+    from paper_2312_00839_b200 import stages as _S
+
+    _S.FUSE_WGRAD_UPDATE = True
 torch.backends.cuda.matmul.allow_tf32 = False
 dev = torch.device("cuda", 0)
 data = bp.DeviceBatches(torch, dev)
