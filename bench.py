@@ -424,6 +424,11 @@ def e2e_leg(args, torch, dist, world, device):
     from paper_2312_00839_b200.optim import HostStreamer, OptimizerConfig, OptimizerState, predict_weights
 
     n = int(args.n_params)
+    if world > 2:
+        # 16 B/param of pinned host memory per rank: cap the sample at 2.5e8
+        # params (4 GB per rank) so 8 ranks do not pin 128 GB of host RAM —
+        # the metric is a rate, and 2.5e8 is still ~15 streamer chunks
+        n = min(n, 250_000_000)
     kind = args.kind
     pin = lambda: torch.empty(n, dtype=torch.float32).pin_memory()  # noqa: E731
     w_h, g_h, wo_h, wh_h = pin(), pin(), pin(), pin()
@@ -531,6 +536,7 @@ def e2e_leg(args, torch, dist, world, device):
         "h2d_bytes_per_step": 8 * n,
         "d2h_bytes_per_step": 8 * n,
         "ms_per_step": round(ms, 3),
+        "n_params": n,
         "wall_s": round(wall, 3),
         "path": "OptimizerState + HostStreamer.step_predict: pinned host W, G -> device (chunked) -> K3 against "
                 "device-resident m, v -> W', W_hat -> pinned host (H2D and D2H streams overlapped)",
