@@ -91,9 +91,11 @@ def _graphed_pair(torch, device, depth, n_batches, data, replays, trials=9, stre
     return {k: (graphs[k].report(), statistics.median(times[k]), graphs[k].launches, times[k]) for k in graphs}
 
 
-def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
-    """CUDA graph of stage k's work for one mini-batch: forward (+ loss on the
-    last stage) + backward + update (K3 when predictive and not last, else K2)."""
+def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth, units: int = 1):
+    """CUDA graph of stage k's work for `units` consecutive mini-batches:
+    forward (+ loss on the last stage) + backward + update (K3 when
+    predictive and not last, else K2), back to back as on the stage's own
+    GPU in the 1F1B steady state."""
     from .stages import loss_and_grad
 
     from .runtime import staging_in_grad_ok
@@ -147,7 +149,8 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
     from .runtime import capture
 
     with capture(graph):
-        unit()
+        for _ in range(units):
+            unit()
     graph.replay()
     torch.cuda.synchronize(device)
     # the graph replays into these addresses: keep the buffers allocated
@@ -156,13 +159,20 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth):
     return graph
 
 
-def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 40, trials: int = 9):
+UNITS_PER_GRAPH = 16
+
+
+def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 5, trials: int = 9,
+                     units: int | None = None):
     """Per-stage device time of one mini-batch's work — SURVEY.md §8d's
     t_f,k + t_b,k (+ t_u,k) — with prediction off (K2 update) and on (K3),
-    each captured in a CUDA graph on THROWAWAY stages from `make()` ->
+    each captured as `units` back-to-back units in one CUDA graph (the
+    stage's steady state on its own GPU; one unit per graph would add a
+    graph launch gap to every unit) on THROWAWAY stages from `make()` ->
     (stages, opts) (replays train them), the two modes replayed in
     alternation (`reps` replays per sample, median of `trials`) so that drift
     hits both alike. Returns {"pred_off": [s per stage], "pred_on": [...]}."""
+    units = UNITS_PER_GRAPH if units is None else units
     import statistics
 
     out = {"pred_off": [], "pred_on": []}
@@ -170,7 +180,7 @@ def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 40, trial
     depth = len(sets["pred_off"][0])
     for k in range(depth):
         graphs = {key: _unit_graph(torch, device, k, sets[key][0][k], sets[key][1][k], data, loss_kind,
-                                   key == "pred_on", depth) for key in out}
+                                   key == "pred_on", depth, units) for key in out}
         samples = {key: [] for key in out}
         for _ in range(trials):
             for key, graph in graphs.items():
@@ -180,7 +190,7 @@ def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 40, trial
                     graph.replay()
                 e1.record()
                 torch.cuda.synchronize(device)
-                samples[key].append(e0.elapsed_time(e1) / 1e3 / reps)
+                samples[key].append(e0.elapsed_time(e1) / 1e3 / (reps * units))
         for key in out:
             out[key].append(statistics.median(samples[key]))
         del graphs
@@ -495,7 +505,7 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
             kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
             return st, [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in st]
 
-        units = stage_unit_times(torch, device, make, data, "softmax_xent", reps=3, trials=3)
+        units = stage_unit_times(torch, device, make, data, "softmax_xent", reps=3, trials=3, units=4)
         from .roofline import module_pipeline_bounds
 
         arith = "bf16" if amp == "bf16" else ("tf32" if tf32 else "fast_fp32")
