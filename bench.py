@@ -494,7 +494,13 @@ def e2e_leg(args, torch, dist, world, device):
         d = lopt.prediction_direction(new)
         return predict_weights(new, 1e-3, 3, d)
 
-    list_step()
+    # two warm-up calls: the outputs are new pinned host tensors, and torch's
+    # caching host allocator hands a dropped output back only from the second
+    # call after it (its free-time event is still pending at the next
+    # allocation) — until then each call pins 16 B/param afresh at ~2.4 GB/s
+    # (scripts/list_api_probe.py, profiles/r2_list_api_probe.jsonl)
+    for _ in range(2):
+        list_step()
     torch.cuda.synchronize(device)
     l_steps = max(1, min(3, args.e2e_steps))
     t_l = time.perf_counter()
