@@ -118,7 +118,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and not jobs and LIB_PATH.exists() and not _stale(LIB_PATH, objs):
         return LIB_PATH
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc, *ARCH_FLAGS, "-shared", "-o", str(tmp), *map(str, objs), "-lcuda"]
+    cmd = [nvcc, *ARCH_FLAGS, "-shared", "-o", str(tmp), *map(str, objs)]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
