@@ -494,11 +494,10 @@ def e2e_leg(args, torch, dist, world, device):
         d = lopt.prediction_direction(new)
         return predict_weights(new, 1e-3, 3, d)
 
-    # two warm-up calls: the outputs are new pinned host tensors, and torch's
-    # caching host allocator hands a dropped output back only from the second
-    # call after it (its free-time event is still pending at the next
-    # allocation) — until then each call pins 16 B/param afresh at ~2.4 GB/s
-    # (scripts/list_api_probe.py, profiles/r2_list_api_probe.jsonl)
+    # warm-up calls: the outputs are new pinned host tensors; the first call
+    # pins them afresh (~0.4 s per GB), later calls get the outputs the caller
+    # dropped back from torch's pinned-host cache (scripts/list_api_probe.py,
+    # profiles/r2_list_api_probe.jsonl)
     for _ in range(2):
         list_step()
     torch.cuda.synchronize(device)

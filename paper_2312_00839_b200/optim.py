@@ -791,7 +791,10 @@ class HostStreamer:
                 ev.record(self.s_out)
                 self.ev_free[k] = ev
         cur.wait_stream(self.s_out)
-        self._chunks = chunks
+        # (offset, start, length) only: holding the chunks' host tensors here
+        # would keep the caller's dropped outputs out of torch's pinned-host
+        # cache until the next call, which would then pin fresh memory
+        self._chunks = [(off, lo, m) for off, _a, _b, _o1, _o2, lo, m in chunks]
         return len(chunks), bad
 
     def _raise_bad(self, opt, bad, where) -> None:
@@ -800,7 +803,7 @@ class HostStreamer:
         if not opt.eager_checks:
             return
         torch.cuda.current_stream(self.device).synchronize()
-        for (off, a, b, o1, o2, lo, m), v in zip(self._chunks, bad.cpu().tolist()):
+        for (off, lo, m), v in zip(self._chunks, bad.cpu().tolist()):
             if v != _INT64_MAX:
                 name = next((nm for o, n, nm in where if o <= off + lo + v < o + n), opt.names[0])
                 raise NumericError(f"optimizer step produced non-finite values in {name}")

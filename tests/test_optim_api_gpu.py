@@ -281,3 +281,29 @@ def test_host_list_api_streams_in_chunks():
     bad[2][4321] = float("inf")
     with pytest.raises(NumericError, match="in c"):
         opt.step(cur, bad, 1e-3)
+
+
+def test_host_list_api_keeps_no_reference_to_its_outputs():
+    """After step / prediction_direction / predict_weights on host lists
+    return, nothing inside the library holds their tensors: outputs the
+    caller drops go straight back to torch's pinned-host cache, so the next
+    call reuses them instead of pinning fresh memory
+    (profiles/r2_list_api_probe.jsonl)."""
+    import gc
+    import weakref
+
+    import torch
+
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState, predict_weights
+
+    dev = torch.device("cuda", 0)
+    opt = OptimizerState(OptimizerConfig("adam"), ["w"], device=dev)
+    w = torch.randn(10_000) * 0.02
+    g = torch.randn(10_000) * 1e-2
+    new, dirs = opt.step([w], [g], 1e-3)
+    d = opt.prediction_direction(new)
+    wh = predict_weights(new, 1e-3, 3, d)
+    refs = [weakref.ref(t) for t in (new[0], dirs[0], d[0], wh[0], w, g)]
+    del new, dirs, d, wh, w, g
+    gc.collect()
+    assert all(r() is None for r in refs)
