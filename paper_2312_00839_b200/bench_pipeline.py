@@ -168,15 +168,21 @@ def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 5, trials
     t_f,k + t_b,k (+ t_u,k) — with prediction off (K2 update) and on (K3),
     each captured as `units` back-to-back units in one CUDA graph (the
     stage's steady state on its own GPU; one unit per graph would add a
-    graph launch gap to every unit) on THROWAWAY stages from `make()` ->
-    (stages, opts) (replays train them), the two modes replayed in
-    alternation (`reps` replays per sample, median of `trials`) so that drift
-    hits both alike. Returns {"pred_off": [s per stage], "pred_on": [...]}."""
+    graph launch gap to every unit) on one set of THROWAWAY stages from
+    `make()` -> (stages, opts) shared by both modes (replays train them),
+    the two modes replayed in alternation (`reps` replays per sample, median
+    of `trials`) so that drift hits both alike. Returns {"pred_off": [s per stage], "pred_on": [...]}."""
     units = UNITS_PER_GRAPH if units is None else units
     import statistics
 
     out = {"pred_off": [], "pred_on": []}
-    sets = {key: make() for key in out}
+    # both modes on the SAME stage buffers: a separate build places them at
+    # other addresses (other L2 slices / pages), which moved a unit by
+    # ~0.5 us between builds — as much as the prediction's own cost
+    # (profiles/r2_unit_shape_probe.jsonl); replays of either graph only
+    # advance the shared weights and state, the work per unit is unchanged
+    shared = make()
+    sets = {key: shared for key in out}
     depth = len(sets["pred_off"][0])
     for k in range(depth):
         graphs = {key: _unit_graph(torch, device, k, sets[key][0][k], sets[key][1][k], data, loss_kind,
