@@ -163,26 +163,33 @@ UNITS_PER_GRAPH = 16
 
 
 def stage_unit_times(torch, device, make, data, loss_kind, reps: int = 5, trials: int = 9,
-                     units: int | None = None):
+                     units: int | None = None, shared: bool = True):
     """Per-stage device time of one mini-batch's work — SURVEY.md §8d's
     t_f,k + t_b,k (+ t_u,k) — with prediction off (K2 update) and on (K3),
     each captured as `units` back-to-back units in one CUDA graph (the
     stage's steady state on its own GPU; one unit per graph would add a
-    graph launch gap to every unit) on one set of THROWAWAY stages from
-    `make()` -> (stages, opts) shared by both modes (replays train them),
+    graph launch gap to every unit) on THROWAWAY stages from `make()` ->
+    (stages, opts) — one set shared by both modes unless shared=False —
+    (replays train them),
     the two modes replayed in alternation (`reps` replays per sample, median
     of `trials`) so that drift hits both alike. Returns {"pred_off": [s per stage], "pred_on": [...]}."""
     units = UNITS_PER_GRAPH if units is None else units
     import statistics
 
     out = {"pred_off": [], "pred_on": []}
-    # both modes on the SAME stage buffers: a separate build places them at
-    # other addresses (other L2 slices / pages), which moved a unit by
-    # ~0.5 us between builds — as much as the prediction's own cost
+    # shared: both modes on the SAME stage buffers — a separate build places
+    # them at other addresses (other L2 slices / pages), which moved a config-1
+    # unit by ~0.5 us between builds, as much as the prediction's own cost
     # (profiles/r2_unit_shape_probe.jsonl); replays of either graph only
-    # advance the shared weights and state, the work per unit is unchanged
-    shared = make()
-    sets = {key: shared for key in out}
+    # advance the shared weights and state. Module stages (configs 2-4) are
+    # measured on separate builds: one ModuleStage under two captured graphs
+    # slows both of GNMT-8's stage-0 units by the same 0.085 ms
+    # (profiles/r2_unit_times_shared_buffers.jsonl)
+    if shared:
+        one = make()
+        sets = {key: one for key in out}
+    else:
+        sets = {key: make() for key in out}
     depth = len(sets["pred_off"][0])
     for k in range(depth):
         graphs = {key: _unit_graph(torch, device, k, sets[key][0][k], sets[key][1][k], data, loss_kind,
@@ -511,7 +518,8 @@ def single_gpu_module_pipeline(torch, device, name: str, n_batches: int = 16, tf
             kw = {"weight_decay": 5e-4} if cfg["opt"] == "sgdm" else {}
             return st, [OptimizerState(OptimizerConfig(cfg["opt"], **kw), s.param_names, device=device) for s in st]
 
-        units = stage_unit_times(torch, device, make, data, "softmax_xent", reps=3, trials=3, units=4)
+        units = stage_unit_times(torch, device, make, data, "softmax_xent", reps=3, trials=3, units=4,
+                                 shared=False)
         from .roofline import module_pipeline_bounds
 
         arith = "bf16" if amp == "bf16" else ("tf32" if tf32 else "fast_fp32")
