@@ -304,6 +304,17 @@ int po_head_fwd(const float* x, int64_t rows, int64_t in, const float* w, const 
 int po_head_bwd(const float* x, int64_t rows, int64_t in, const float* g, int32_t classes, const float* w, float* dx,
                 float* dw, float* db, int32_t accumulate, void* stream);
 
+/* po_head_fwd_loss: po_head_fwd and po_loss_grad in ONE launch (the last
+ * stage's forward + loss + dL/dout, runtime.py:415-426 via stages.py:175-184
+ * and linalg.py:212-241): out = x @ W + b, then the loss of kind PO_LOSS_*
+ * against target (rows x classes) into *loss and its gradient into grad
+ * (rows x classes), bit-identical to the two separate calls (same
+ * expressions and reduction orders). scratch: po_loss_grad's layout (rows
+ * floats + one uint32 counter, zero before the first launch; re-armed). */
+int po_head_fwd_loss(const float* x, int64_t rows, int64_t in, const float* w, const float* b, int32_t classes,
+                     const float* target, int32_t kind, float* out, float* grad, float* loss, float* scratch,
+                     uint8_t* flags, int64_t flag_index, void* stream);
+
 /* ---- weight gradient + update in one kernel (pipeoptim_wgrad.cu) --------
  * g = x^T @ dpre for one MLP layer (x: rows x in, row-major, leading dim
  * ldx; dpre: rows x out, ldd) on the tcgen05 tensor cores (each fp32 operand

@@ -53,6 +53,7 @@ EXPORTS = (
     "po_nvls_free",
     "po_head_supported",
     "po_head_fwd",
+    "po_head_fwd_loss",
     "po_head_bwd",
     "po_wgrad_update_supported",
     "po_wgrad_update",
@@ -166,6 +167,8 @@ _SIGNATURES = {
     "po_nvls_free": (ctypes.c_int, [_P]),
     "po_head_supported": (ctypes.c_int, [_I64, _I64, _I64]),
     "po_head_fwd": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, _P, _I64, _P]),
+    "po_head_fwd_loss": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P,
+                                        _P, _P, _I64, _P]),
     "po_head_bwd": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int32, _P]),
     "po_wgrad_update_supported": (ctypes.c_int, [_I64, _I64, _I64]),
     "po_wgrad_update": (ctypes.c_int, [_HP, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _D, _D, _I64,

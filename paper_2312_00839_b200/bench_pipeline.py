@@ -96,8 +96,6 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth, u
     forward (+ loss on the last stage) + backward + update (K3 when
     predictive and not last, else K2), back to back as on the stage's own
     GPU in the 1F1B steady state."""
-    from .stages import loss_and_grad
-
     from .runtime import staging_in_grad_ok
 
     last = k == depth - 1
@@ -123,8 +121,11 @@ def _unit_graph(torch, device, k, st, opt, data, loss_kind, predictive, depth, u
     defer = _stages.FUSE_WGRAD_UPDATE and isinstance(st, StageModel)  # as the runners do
 
     def unit():
-        out = st.run_forward(fwd_weights, (0, 0), x, 1, check_finite=False)
-        g = loss_and_grad(out, y0, loss_kind)[1] if last else g_last
+        if last:
+            g = st.run_forward_loss(fwd_weights, (0, 0), x, 1, y0, loss_kind, check_finite=False)[2]
+        else:
+            st.run_forward(fwd_weights, (0, 0), x, 1, check_finite=False)
+            g = g_last
         if defer:
             st.run_backward(st.params, (0, 0), g, need_input_grad=k > 0, defer_wgrad=True)
             wg = st.take_deferred_wgrad()

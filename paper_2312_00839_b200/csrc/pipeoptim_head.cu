@@ -24,12 +24,50 @@ constexpr int kHeadThreads = 256;
 constexpr int kHeadMaxC = 32;
 constexpr int kGSmemFloats = 2048;  // g (rows x C) staged in shared memory up to 8 KB (static + dynamic <= 48 KB)
 
-template <int CMAX>
-__global__ void __launch_bounds__(kHeadThreads) head_fwd_kernel(const float* __restrict__ x, int64_t in,
-                                                                const float* __restrict__ w,
+// The reductions of loss_grad_kernel (pipeoptim_stage_ops.cu), restated so
+// that the fused forward + loss below produces the same bits: a lane-xor
+// butterfly inside each warp, then the warp totals in warp 0.
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  v = (threadIdx.x < blockDim.x / 32) ? sh[threadIdx.x] : 0.f;
+  if (w == 0) v = warp_sum(v);
+  if (threadIdx.x == 0) sh[32] = v;
+  __syncthreads();
+  return sh[32];
+}
+
+// Loss inputs of the fused forward (LOSS = true): one-hot / regression
+// targets (rows x C), the loss kind (PO_LOSS_*), dL/dout, the row partials +
+// last-CTA counter (po_loss_grad's scratch layout) and the scalar loss.
+struct LossArgs {
+  const float* target;
+  int kind;
+  float* grad;
+  float* row_part;
+  unsigned int* counter;
+  float* loss;
+};
+
+template <int CMAX, bool LOSS>
+__global__ void __launch_bounds__(kHeadThreads) head_fwd_kernel(const float* __restrict__ x, int64_t rows,
+                                                                int64_t in, const float* __restrict__ w,
                                                                 const float* __restrict__ b, int C,
                                                                 float* __restrict__ out, uint8_t* flags,
-                                                                int64_t flag_index) {
+                                                                int64_t flag_index, LossArgs la) {
   __shared__ float part[kHeadThreads / 32][CMAX];
   const int64_t r = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -50,13 +88,64 @@ __global__ void __launch_bounds__(kHeadThreads) head_fwd_kernel(const float* __r
     if (lane == 0) part[warp][c] = v;
   }
   __syncthreads();
+  float o = 0.f;
   if (tid < C) {
     float s = part[0][tid];
 #pragma unroll
     for (int q = 1; q < kHeadThreads / 32; ++q) s += part[q][tid];  // warp order
-    const float o = (b != nullptr ? b[tid] : 0.f) + s;
+    o = (b != nullptr ? b[tid] : 0.f) + s;
     out[r * C + tid] = o;
     if (flags != nullptr && !isfinite(o)) flags[flag_index] = 0;
+  }
+  if constexpr (LOSS) {
+    // the row's C <= 32 logits sit in warp 0's lanes 0..C-1 (column c = lane
+    // c, as in loss_grad_kernel); warps 1.. contribute exact zeros there
+    __shared__ float sh[33];
+    __shared__ bool last;
+    if (warp == 0) {
+      const bool on = tid < C;
+      const float y = on ? la.target[r * C + tid] : 0.f;
+      float* g = la.grad + r * C;
+      float row;
+      if (la.kind == PO_LOSS_SOFTMAX_XENT) {  // linalg.py:228-235
+        float m = -INFINITY;
+        if (on) m = fmaxf(m, o);
+        m = warp_max(m);
+        const float e = on ? expf(o - m) : 0.f;
+        const float ssum = warp_sum(e);
+        float picked = 0.f;
+        if (on) {
+          const float sm = expf(o - m) / ssum;
+          picked = sm * y;
+          g[tid] = (sm - y) * (1.0f / (float)rows);
+        }
+        row = -logf(warp_sum(picked));
+      } else {  // mse, linalg.py:223-227
+        float a = 0.f;
+        if (on) {
+          const float d = o - y;
+          a = d * d;
+          g[tid] = d * (2.0f / (float)(rows * C));
+        }
+        row = warp_sum(a);
+      }
+      if (tid == 0) {
+        la.row_part[r] = row;
+        __threadfence();
+        last = atomicAdd(la.counter, 1u) == (unsigned int)(rows - 1);
+      }
+    }
+    __syncthreads();
+    if (last) {  // fixed-order reduction of the row partials (loss_grad_kernel's)
+      __threadfence();
+      float a = 0.f;
+      for (int64_t i = tid; i < rows; i += kHeadThreads) a += ((volatile float*)la.row_part)[i];
+      a = block_sum(a, sh);
+      if (tid == 0) {
+        *la.loss = (la.kind == PO_LOSS_SOFTMAX_XENT) ? a / (float)rows : a / (float)(rows * C);
+        *la.counter = 0u;  // re-armed for the next launch (graph replays)
+      }
+    }
   }
 }
 
@@ -142,6 +231,26 @@ __global__ void __launch_bounds__(kHeadThreads) head_bwd_kernel(const float* __r
 
 int head_cmax(int C) { return C <= 8 ? 8 : C <= 16 ? 16 : 32; }
 
+template <bool LOSS>
+int launch_head_fwd(const float* x, int64_t rows, int64_t in, const float* w, const float* b, int32_t classes,
+                    float* out, uint8_t* flags, int64_t flag_index, LossArgs la, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 grid((unsigned)rows);
+  switch (head_cmax(classes)) {
+    case 8:
+      head_fwd_kernel<8, LOSS><<<grid, kHeadThreads, 0, s>>>(x, rows, in, w, b, classes, out, flags, flag_index, la);
+      break;
+    case 16:
+      head_fwd_kernel<16, LOSS><<<grid, kHeadThreads, 0, s>>>(x, rows, in, w, b, classes, out, flags, flag_index, la);
+      break;
+    default:
+      head_fwd_kernel<32, LOSS><<<grid, kHeadThreads, 0, s>>>(x, rows, in, w, b, classes, out, flags, flag_index, la);
+      break;
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -154,15 +263,20 @@ int po_head_fwd(const float* x, int64_t rows, int64_t in, const float* w, const 
                 float* out, uint8_t* flags, int64_t flag_index, void* stream) {
   if (!po_head_supported(rows, in, classes) || x == nullptr || w == nullptr || out == nullptr || flag_index < 0)
     return PO_EINVAL;
-  cudaStream_t s = (cudaStream_t)stream;
-  const dim3 grid((unsigned)rows);
-  switch (head_cmax(classes)) {
-    case 8: head_fwd_kernel<8><<<grid, kHeadThreads, 0, s>>>(x, in, w, b, classes, out, flags, flag_index); break;
-    case 16: head_fwd_kernel<16><<<grid, kHeadThreads, 0, s>>>(x, in, w, b, classes, out, flags, flag_index); break;
-    default: head_fwd_kernel<32><<<grid, kHeadThreads, 0, s>>>(x, in, w, b, classes, out, flags, flag_index); break;
-  }
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 0 : (int)e;
+  return launch_head_fwd<false>(x, rows, in, w, b, classes, out, flags, flag_index, LossArgs{}, stream);
+}
+
+int po_head_fwd_loss(const float* x, int64_t rows, int64_t in, const float* w, const float* b, int32_t classes,
+                     const float* target, int32_t kind, float* out, float* grad, float* loss, float* scratch,
+                     uint8_t* flags, int64_t flag_index, void* stream) {
+  if (!po_head_supported(rows, in, classes) || x == nullptr || w == nullptr || out == nullptr || flag_index < 0)
+    return PO_EINVAL;
+  if ((kind != PO_LOSS_MSE && kind != PO_LOSS_SOFTMAX_XENT) || target == nullptr || grad == nullptr ||
+      loss == nullptr || scratch == nullptr)
+    return PO_EINVAL;
+  // scratch: po_loss_grad's layout ([rows] row partials, then a uint32 counter zeroed once)
+  const LossArgs la{target, kind, grad, scratch, reinterpret_cast<unsigned int*>(scratch + rows), loss};
+  return launch_head_fwd<true>(x, rows, in, w, b, classes, out, flags, flag_index, la, stream);
 }
 
 int po_head_bwd(const float* x, int64_t rows, int64_t in, const float* g, int32_t classes, const float* w, float* dx,

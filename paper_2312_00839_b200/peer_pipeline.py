@@ -45,7 +45,6 @@ from .runtime import (
     staging_in_grad_ok,
 )
 from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
-from .stages import loss_and_grad
 
 # flag word offsets in each rank's int64 flag block
 _ACT_READY, _GRAD_READY, _ACT_ACK, _GRAD_ACK = 0, 1, 2, 3
@@ -325,14 +324,17 @@ class PeerStageRunner:
                 x = links.recv_act() if self.rank > 0 else self._shard(_to_device(self.data.batch(op.mb)[0],
                                                                                     self.device))
                 weights, fv, predicted, target = policy.forward_view(rt, op.mb, 0, lr_fn(op.mb))
-                out = st.run_forward(weights, (op.mb, 0), x, fv, check_finite=False, finite_flags=flags,
-                                     flag_index=wi)
+                if last:  # forward + loss (+ dL/dout) in one launch for a narrow output layer
+                    y = self._shard(_to_device(self.data.batch(op.mb)[1], self.device))
+                    out, loss, grad = st.run_forward_loss(weights, (op.mb, 0), x, fv, y, self.loss_kind,
+                                                          check_finite=False, finite_flags=flags, flag_index=wi)
+                else:
+                    out = st.run_forward(weights, (op.mb, 0), x, fv, check_finite=False, finite_flags=flags,
+                                         flag_index=wi)
                 rec = VersionRecord(op.mb, 0, self.rank, fv, predicted, target)
                 records[op.mb] = rec
                 order.append(rec)
                 if last:
-                    y = self._shard(_to_device(self.data.batch(op.mb)[1], self.device))
-                    loss, grad = loss_and_grad(out, y, self.loss_kind)
                     losses[op.mb - 1] = loss
                     local_grads[op.mb] = grad
                 else:

@@ -36,7 +36,7 @@ from .runtime import (
     staging_in_grad_ok,
 )
 from .schedule import BACKWARD, FORWARD, UPDATE, Timeline, stage_program, validate_timeline
-from .stages import StageModel, loss_and_grad
+from .stages import StageModel
 
 
 @dataclass
@@ -284,11 +284,11 @@ class _OpGraphs:
         last = r.rank == r.depth - 1
 
         def fn():
+            if last:
+                return st.run_forward_loss(weights, ("slot", slot), x, fv, y, r.loss_kind, check_finite=False,
+                                           finite_flags=flags, flag_index=flag_base + slot)
             out = st.run_forward(weights, ("slot", slot), x, fv, check_finite=False, finite_flags=flags,
                                  flag_index=flag_base + slot)
-            if last:
-                loss, grad = loss_and_grad(out, y, r.loss_kind)
-                return out, loss, grad
             return out, None, None
 
         return self._run(("F", slot, weights[0].data_ptr()), fn)
@@ -485,11 +485,14 @@ class PipelineStageRunner:
                     if g is not None:
                         out, loss, grad = g.forward(op, weights, x, y, fv, flags, len(work))
                     else:
-                        out = self.stage.run_forward(weights, (op.mb, op.micro), x, fv, check_finite=self.eager,
-                                                     finite_flags=flags, flag_index=wi)
-                        loss = grad = None
                         if last:
-                            loss, grad = loss_and_grad(out, y, self.loss_kind)
+                            out, loss, grad = self.stage.run_forward_loss(
+                                weights, (op.mb, op.micro), x, fv, y, self.loss_kind, check_finite=self.eager,
+                                finite_flags=flags, flag_index=wi)
+                        else:
+                            out = self.stage.run_forward(weights, (op.mb, op.micro), x, fv,
+                                                         check_finite=self.eager, finite_flags=flags, flag_index=wi)
+                            loss = grad = None
                 except NumericError as err:
                     raise NumericError(f"mb {op.mb} stage {self.rank}: {err}") from err
                 in_flight += 1

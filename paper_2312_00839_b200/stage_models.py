@@ -44,7 +44,7 @@ import torch.nn.functional as F
 from . import _lib
 from .errors import NumericError
 from .optim import FlatParams
-from .stages import ActivationStash, StashEntry, _splitk, record_finite
+from .stages import ActivationStash, StashEntry, _splitk, loss_and_grad, record_finite
 
 
 class _LiveLinearFn(torch.autograd.Function):
@@ -438,6 +438,13 @@ class ModuleStage:
         for p, v in zip(self._params, views):
             if p.data_ptr() != v.data_ptr():
                 p.data = v
+
+    def run_forward_loss(self, weights, key, x, version, target, loss_kind, check_finite=True, finite_flags=None,
+                         flag_index=0):
+        """Last-stage forward + loss (runtime.py:415-426): (out, loss, dL/dout)."""
+        out = self.run_forward(weights, key, x, version, check_finite, finite_flags, flag_index)
+        loss, grad = loss_and_grad(out, target, loss_kind)
+        return out, loss, grad
 
     def run_forward(self, weights, key, x, version, check_finite=True, finite_flags=None, flag_index=0):
         self._point(weights)

@@ -194,6 +194,19 @@ class StageModel:
     def run_forward(self, weights, key, x, version, check_finite=True, finite_flags=None, flag_index=0):
         return stage_forward(self, weights, key, x, version, check_finite, finite_flags, flag_index)
 
+    def run_forward_loss(self, weights, key, x, version, target, loss_kind, check_finite=True, finite_flags=None,
+                         flag_index=0):
+        """The last stage's forward followed by the loss (runtime.py:415-426):
+        (out, loss, dL/dout). A narrow output layer runs forward, loss and
+        gradient in one launch (po_head_fwd_loss, bit-identical to
+        run_forward + loss_and_grad); otherwise the two calls."""
+        req = {"y": target, "kind": loss_kind} if FUSED_HEAD_LOSS else None
+        out = stage_forward(self, weights, key, x, version, check_finite, finite_flags, flag_index, loss_req=req)
+        if req is not None and "loss" in req:
+            return out, req["loss"], req["grad"]
+        loss, grad = loss_and_grad(out, target, loss_kind)
+        return out, loss, grad
+
     def run_backward(self, weights, key, grad_out, accumulate=False, need_input_grad=True, defer_wgrad=False):
         return stage_backward(self, weights, key, grad_out, accumulate, need_input_grad, defer_wgrad)
 
@@ -311,6 +324,9 @@ def _splitk_reduce(part: torch.Tensor, bias, act: str, pre_out=None, flags=None,
 # Narrow linear layers (out <= 32: config 1's classifier) on po_head_fwd /
 # po_head_bwd — one launch each way — instead of the library GEMMs (A/B switch)
 FUSED_HEAD = True
+# ... and, on the last stage (run_forward_loss), its forward + loss + dL/dout
+# in ONE launch (po_head_fwd_loss) instead of po_head_fwd + po_loss_grad
+FUSED_HEAD_LOSS = True
 
 
 def _head_ok(h: torch.Tensor, w: torch.Tensor, act: str) -> bool:
@@ -320,11 +336,24 @@ def _head_ok(h: torch.Tensor, w: torch.Tensor, act: str) -> bool:
             and _lib.load().po_head_supported(h.shape[0], h.shape[1], w.shape[1]) == 1)
 
 
-def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str, flags=None, flag_index: int = 0):
+def _head_loss_ok(req, rows: int, n: int, device) -> bool:
+    """The fused head forward + loss applies: a valid loss kind and an fp32
+    contiguous target of the output's shape on the same device."""
+    if req is None or req["kind"] not in LOSS_KINDS:
+        return False
+    y = req["y"]
+    return (isinstance(y, torch.Tensor) and y.dtype == torch.float32 and y.is_contiguous()
+            and y.device == device and tuple(y.shape) == (rows, n))
+
+
+def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str, flags=None, flag_index: int = 0,
+            loss_req=None):
     """Device forward of one layer: (pre, h_out, checked) with the stash's
     convention — relu layers stash relu(pre) (its sign pattern is pre's),
     others pre. checked: the finiteness flag was already written (split-K
-    epilogue / head kernel)."""
+    epilogue / head kernel). loss_req ({"y", "kind"}, last layer only): a
+    narrow output layer also computes the loss and dL/dout in its launch
+    (po_head_fwd_loss) and stores them under "loss" / "grad"."""
     rows, k = h.shape
     n = w.shape[1]
     h = h if h.is_contiguous() else h.contiguous()
@@ -333,9 +362,23 @@ def _affine(h: torch.Tensor, w: torch.Tensor, b: torch.Tensor, act: str, flags=N
 
         out = torch.empty((rows, n), dtype=torch.float32, device=h.device)
         bias = b.reshape(-1)
-        rc = _lib.load().po_head_fwd(h.data_ptr(), rows, k, w.data_ptr(), bias.data_ptr(), n, out.data_ptr(),
-                                     None if flags is None else flags.data_ptr(), flag_index,
-                                     torch.cuda.current_stream(h.device).cuda_stream)
+        stream = torch.cuda.current_stream(h.device).cuda_stream
+        fl = None if flags is None else flags.data_ptr()
+        if _head_loss_ok(loss_req, rows, n, h.device):
+            key = (h.device, rows, stream)  # loss_and_grad's scratch (per device, rows, stream)
+            if key not in _LOSS_SCRATCH:
+                _LOSS_SCRATCH[key] = torch.zeros(rows + 1, dtype=torch.float32, device=h.device)
+            grad = torch.empty_like(out)
+            loss = torch.empty((), dtype=torch.float32, device=h.device)
+            code = _lib.PO_LOSS_MSE if loss_req["kind"] == "mse" else _lib.PO_LOSS_SOFTMAX_XENT
+            rc = _lib.load().po_head_fwd_loss(h.data_ptr(), rows, k, w.data_ptr(), bias.data_ptr(), n,
+                                              loss_req["y"].data_ptr(), code, out.data_ptr(), grad.data_ptr(),
+                                              loss.data_ptr(), _LOSS_SCRATCH[key].data_ptr(), fl, flag_index, stream)
+            _lib.check(rc, "po_head_fwd_loss")
+            loss_req["loss"], loss_req["grad"] = loss, grad
+            return out, out, flags is not None
+        rc = _lib.load().po_head_fwd(h.data_ptr(), rows, k, w.data_ptr(), bias.data_ptr(), n, out.data_ptr(), fl,
+                                     flag_index, stream)
         _lib.check(rc, "po_head_fwd")
         return out, out, flags is not None
     tc = n % 4 == 0 and k % 4 == 0 and _tc_ok(h, w)
@@ -410,7 +453,7 @@ def _side_stream(device) -> "torch.cuda.Stream":
 
 def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int,
                   check_finite: bool = True, finite_flags: torch.Tensor | None = None,
-                  flag_index: int = 0) -> torch.Tensor:
+                  flag_index: int = 0, loss_req: dict | None = None) -> torch.Tensor:
     """Run the stage's layers on x with the given weights view; stash the
     per-layer inputs and pre-activations (stages.py:156-184).
 
@@ -451,7 +494,8 @@ def stage_forward(stage: StageModel, weights, key, x: torch.Tensor, version: int
             # writes the deferred finiteness flag of the stage output), or bias
             # + ReLU in the cuBLASLt epilogue; relu layers stash relu(pre)
             want_flag = i == last and not check_finite and finite_flags is not None
-            pre, h, checked = _affine(h, w, b, spec.activation, finite_flags if want_flag else None, flag_index)
+            pre, h, checked = _affine(h, w, b, spec.activation, finite_flags if want_flag else None, flag_index,
+                                      loss_req if i == last else None)
             pres.append(pre)
             continue
         pre = torch.addmm(b, h, w)

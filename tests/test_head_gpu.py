@@ -105,3 +105,107 @@ def test_stage_with_head_matches_library_path():
             S.FUSED_HEAD = True
     for a, b in zip(res[False], res[True]):
         assert float((a - b).abs().max() / b.abs().max()) <= 2e-6
+
+
+@pytest.mark.parametrize("kind", ["softmax_xent", "mse"])
+@pytest.mark.parametrize("rows,fin,c", [(128, 1024, 10), (1, 6, 3), (300, 257, 32), (64, 1024, 1), (33, 64, 17),
+                                        (513, 512, 10)])
+def test_head_fwd_loss_is_bit_identical_to_two_launches(kind, rows, fin, c):
+    """po_head_fwd_loss (forward + loss + dL/dout in one launch) gives the
+    same bits as po_head_fwd followed by po_loss_grad: output, gradient,
+    scalar loss, finiteness flag; the scratch counter re-arms (two launches
+    in a row, and a CUDA-graph replay)."""
+    import torch
+
+    from paper_2312_00839_b200 import _lib as L
+
+    lib = _lib()
+    code = L.PO_LOSS_MSE if kind == "mse" else L.PO_LOSS_SOFTMAX_XENT
+    g0 = torch.Generator(device="cuda").manual_seed(rows * 7 + fin + c)
+    x = torch.randn(rows, fin, device="cuda", generator=g0)
+    w = torch.randn(fin, c, device="cuda", generator=g0) * 0.05
+    b = torch.randn(c, device="cuda", generator=g0)
+    if kind == "mse":
+        y = torch.randn(rows, c, device="cuda", generator=g0)
+    else:
+        y = torch.nn.functional.one_hot(torch.randint(0, c, (rows,), device="cuda", generator=g0), c).float()
+    s = torch.cuda.current_stream().cuda_stream
+
+    def two():
+        out, grad = torch.empty(rows, c, device="cuda"), torch.empty(rows, c, device="cuda")
+        loss, scratch = torch.empty((), device="cuda"), torch.zeros(rows + 1, device="cuda")
+        flags = torch.ones(1, dtype=torch.uint8, device="cuda")
+        assert lib.po_head_fwd(x.data_ptr(), rows, fin, w.data_ptr(), b.data_ptr(), c, out.data_ptr(),
+                               flags.data_ptr(), 0, s) == 0
+        assert lib.po_loss_grad(code, out.data_ptr(), y.data_ptr(), rows, c, grad.data_ptr(), loss.data_ptr(),
+                                scratch.data_ptr(), s) == 0
+        return out, grad, loss, flags
+
+    scratch = torch.zeros(rows + 1, device="cuda")
+    out, grad = torch.empty(rows, c, device="cuda"), torch.empty(rows, c, device="cuda")
+    loss = torch.empty((), device="cuda")
+    flags = torch.ones(1, dtype=torch.uint8, device="cuda")
+
+    def one():
+        assert lib.po_head_fwd_loss(x.data_ptr(), rows, fin, w.data_ptr(), b.data_ptr(), c, y.data_ptr(), code,
+                                    out.data_ptr(), grad.data_ptr(), loss.data_ptr(), scratch.data_ptr(),
+                                    flags.data_ptr(), 0, torch.cuda.current_stream().cuda_stream) == 0
+
+    want = two()
+    for _ in range(2):  # the counter re-arms
+        loss.fill_(float("nan"))
+        one()
+        torch.cuda.synchronize()
+        for got, ref in zip((out, grad, loss, flags), want):
+            assert torch.equal(got, ref), (kind, rows, fin, c)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        one()
+    loss.fill_(float("nan"))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(loss, want[2]) and torch.equal(grad, want[1])
+
+
+def test_head_fwd_loss_rejects_bad_arguments():
+    import torch
+
+    lib = _lib()
+    p = torch.zeros(64, device="cuda").data_ptr()
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.po_head_fwd_loss(p, 4, 4, p, None, 2, p, 7, p, p, p, p, None, 0, s) != 0  # loss kind
+    assert lib.po_head_fwd_loss(p, 4, 4, p, None, 2, None, 0, p, p, p, p, None, 0, s) != 0  # no target
+    assert lib.po_head_fwd_loss(p, 4, 4, p, None, 2, p, 0, p, p, p, None, None, 0, s) != 0  # no scratch
+    assert lib.po_head_fwd_loss(p, 4, 4, p, None, 33, p, 0, p, p, p, p, None, 0, s) != 0  # too wide
+
+
+@pytest.mark.parametrize("kind", ["softmax_xent", "mse"])
+def test_run_forward_loss_fused_equals_unfused(kind):
+    """StageModel.run_forward_loss with stages.FUSED_HEAD_LOSS on (one launch)
+    and off (run_forward + loss_and_grad): identical output, loss, gradient;
+    a target the fused kernel cannot take (float64) falls back."""
+    import torch
+
+    from paper_2312_00839_b200 import stages as S
+    from paper_2312_00839_b200.stages import StageModel, build_layers, partition_layers, torch_init
+
+    dev = torch.device("cuda", 0)
+    x = torch.randn(128, 1024, device=dev)
+    y = torch.nn.functional.one_hot(torch.arange(128, device=dev) % 10, 10).float()
+    if kind == "mse":
+        y = y * 0.5 + 0.1
+    res = {}
+    for fused in (False, True):
+        S.FUSED_HEAD_LOSS = fused
+        try:
+            st = StageModel(1, partition_layers(build_layers([512, 1024, 10], ["relu", "linear"]), 2)[1],
+                            torch_init(3, dev), dev)
+            res[fused] = st.run_forward_loss(st.params, (1, 0), x, 1, y, kind, check_finite=True)
+            res[(fused, "f64")] = st.run_forward_loss(st.params, (2, 0), x, 1, y.double(), kind, check_finite=True)
+        finally:
+            S.FUSED_HEAD_LOSS = True
+    torch.cuda.synchronize()
+    for a, b in zip(res[False], res[True]):
+        assert torch.equal(a, b)
+    for a, b in zip(res[(False, "f64")], res[(True, "f64")]):
+        assert torch.equal(a, b)
