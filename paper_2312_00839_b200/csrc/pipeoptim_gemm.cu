@@ -58,7 +58,11 @@ using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBui
     cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
     cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, ElementAcc, void, LayoutD, kAlign, float, LayoutD,
     kAlign, cutlass::epilogue::collective::EpilogueScheduleAuto>::CollectiveOp;
-constexpr int kEpiCarveout = static_cast<int>(sizeof(typename CollectiveEpilogue::SharedStorage));
+#ifndef PO_FASTF32_EXTRA_CARVEOUT  // bytes held back from the stage count (fewer stages, more CTAs per SM)
+#define PO_FASTF32_EXTRA_CARVEOUT 0
+#endif
+constexpr int kEpiCarveout =
+    static_cast<int>(sizeof(typename CollectiveEpilogue::SharedStorage)) + PO_FASTF32_EXTRA_CARVEOUT;
 
 #define PO_FAST_F32_GEMM(NAME, LAYOUT_A, LAYOUT_B, SCHEDULE)                                                       \
   namespace NAME {                                                                                                 \
@@ -122,6 +126,16 @@ using RowCol = row_col::G;
 }  // namespace
 
 extern "C" {
+
+#ifdef PO_PROBE_EXPORTS
+int po_probe_gemm_smem(int variant) {
+  switch (variant) {
+    case 0: return (int)sizeof(typename row_row::Kernel::SharedStorage);
+    case 1: return (int)sizeof(typename col_row::Kernel::SharedStorage);
+    default: return (int)sizeof(typename row_col::Kernel::SharedStorage);
+  }
+}
+#endif
 
 int po_gemm_f32x3_available(void) { return 1; }
 
