@@ -22,6 +22,7 @@ views (no separate accumulation pass for one micro-batch per update).
 
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 from typing import Callable
 
@@ -282,14 +283,38 @@ def _tc_ok(*tensors) -> bool:
             and _tc_built())
 
 
+# Most K slices of a tensor-core GEMM's split-K (forward and input gradient):
+# 8 is the latency-optimal count for a stage alone on its GPU; runners whose
+# stages share one GPU lower it (runtime.SHARED_GPU_SPLIT_CAP) through
+# gemm_split_cap(). The count only regroups fp32 partial sums.
+TC_SPLIT_CAP = 8
+_tc_split_cap = TC_SPLIT_CAP
+
+
+@contextlib.contextmanager
+def gemm_split_cap(cap: int):
+    """Cap the tensor-core GEMMs' K slices at `cap` (a power of two >= 1)
+    for the duration (decided when a forward / backward is issued or
+    captured into a CUDA graph)."""
+    global _tc_split_cap
+    cap = int(cap)
+    if cap < 1 or cap & (cap - 1):
+        raise ValueError(f"gemm split cap must be a power of two >= 1, got {cap}")
+    old, _tc_split_cap = _tc_split_cap, cap
+    try:
+        yield
+    finally:
+        _tc_split_cap = old
+
+
 def _splitk_tc(rows: int, k: int) -> int:
     """K slices for the tensor-core GEMM of a small-M long-K shape: <= 8
     slices of >= 128 (scripts/gemm_f32x3_check.py: 3072x1024 forward 14 us at
-    8 slices vs 19 us for the best SIMT split)."""
+    8 slices vs 19 us for the best SIMT split), capped by gemm_split_cap."""
     if rows > 512 or k < 256:
         return 1
     s = 1
-    while s < 8 and k % (s * 2) == 0 and k // (s * 2) >= 128:
+    while s < _tc_split_cap and k % (s * 2) == 0 and k // (s * 2) >= 128:
         s *= 2
     return s
 

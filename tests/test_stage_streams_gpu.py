@@ -11,7 +11,7 @@ from test_runtime_gpu import CONFIG1, EXTRA, SMALL, build, check_losses, rec_tup
 pytestmark = pytest.mark.gpu
 
 
-def _run(case, streams, checks="eager", fuse=True):
+def _run(case, streams, checks="eager", fuse=True, gemm_split_cap=None):
     from oracle import data_ref
     from paper_2312_00839_b200.runtime import execute
     from test_runtime_gpu import ArraySource, Source
@@ -23,7 +23,7 @@ def _run(case, streams, checks="eager", fuse=True):
         batches, loss = data_ref.config1(seed=case["data_seed"])
         src = ArraySource(batches)
     rep = execute(tl, stages, opts, case["strategy"], src, loss, lambda mb, lr=case["lr"]: lr,
-                  checks=checks, fuse=fuse, streams=streams)
+                  checks=checks, fuse=fuse, streams=streams, gemm_split_cap=gemm_split_cap)
     return rep, stages
 
 
@@ -50,10 +50,40 @@ def test_stage_streams_bit_identical_to_serial(case):
 @pytest.mark.parametrize("case", CONFIG1, ids=lambda c: c["strategy"])
 def test_config1_stage_streams_host_batches(case):
     """Host (numpy) batches: x and y are staged to the device on stage 0's
-    stream and consumed by the last stage's."""
-    a, sa = _run(case, "serial", checks="deferred")
+    stream and consumed by the last stage's. Under one GEMM split policy the
+    two runners agree bit for bit: the stage runner's default (the shared-GPU
+    cap, runtime.SHARED_GPU_SPLIT_CAP) == the serial runner at that cap, and
+    both runners at the latency cap (8) agree too; either policy meets the
+    reference goldens."""
+    from paper_2312_00839_b200 import runtime
+
+    a, sa = _run(case, "serial", checks="deferred", gemm_split_cap=runtime.SHARED_GPU_SPLIT_CAP)
     b, sb = _run(case, "stage", checks="deferred")
     _same(a, sa, b, sb)
+    c, sc = _run(case, "serial", checks="deferred")
+    d, sd = _run(case, "stage", checks="deferred", gemm_split_cap=8)
+    _same(c, sc, d, sd)
+    assert rec_tuples(b) == case["records"] and rec_tuples(c) == case["records"]
+    for rep in (b, c):
+        check_losses(rep.losses[:10], case["losses"][:10])
+        check_losses(rep.losses, case["losses"], rtol=5e-3)
+
+
+def test_gemm_split_cap_context():
+    """stages.gemm_split_cap bounds the tensor-core GEMM's K slices and
+    restores the previous cap; non-powers of two are refused."""
+    from paper_2312_00839_b200 import stages as S
+
+    assert S._splitk_tc(128, 3072) == 8
+    with S.gemm_split_cap(4):
+        assert S._splitk_tc(128, 3072) == 4 and S._splitk_tc(128, 256) == 2
+        with S.gemm_split_cap(1):
+            assert S._splitk_tc(128, 3072) == 1
+        assert S._splitk_tc(128, 3072) == 4
+    assert S._splitk_tc(128, 3072) == 8
+    with pytest.raises(ValueError):
+        with S.gemm_split_cap(3):
+            pass
 
 
 def test_stage_streams_unfused_and_eager_checks():
