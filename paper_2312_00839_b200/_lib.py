@@ -7,6 +7,7 @@ returned status code.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 from pathlib import Path
@@ -54,6 +55,8 @@ EXPORTS = (
     "po_head_supported",
     "po_head_fwd",
     "po_head_fwd_loss",
+    "po_set_pdl",
+    "po_get_pdl",
     "po_head_bwd",
     "po_wgrad_update_supported",
     "po_wgrad_update",
@@ -167,6 +170,8 @@ _SIGNATURES = {
     "po_nvls_free": (ctypes.c_int, [_P]),
     "po_head_supported": (ctypes.c_int, [_I64, _I64, _I64]),
     "po_head_fwd": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, _P, _I64, _P]),
+    "po_set_pdl": (None, [ctypes.c_int32]),
+    "po_get_pdl": (ctypes.c_int32, []),
     "po_head_fwd_loss": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P,
                                         _P, _P, _I64, _P]),
     "po_head_bwd": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int32, _P]),
@@ -229,3 +234,17 @@ def check(rc: int, what: str) -> None:
 
 def make_launch(block=0, ctas_per_sm=0, vec=0, cache=0, unroll=0):
     return po_launch(block, ctas_per_sm, vec, cache, unroll)
+
+
+@contextlib.contextmanager
+def pdl(on: bool):
+    """Programmatic dependent launch of the short stream kernels on / off for
+    the duration (po_set_pdl; process-wide, read when a kernel is launched or
+    captured). Results are unchanged either way."""
+    lib = load()
+    old = lib.po_get_pdl()
+    lib.po_set_pdl(1 if on else 0)
+    try:
+        yield
+    finally:
+        lib.po_set_pdl(old)

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "pipeoptim.h"
+#include "pipeoptim_pdl.cuh"
 
 namespace {
 
@@ -68,6 +69,8 @@ __global__ void __launch_bounds__(kHeadThreads) head_fwd_kernel(const float* __r
                                                                 const float* __restrict__ b, int C,
                                                                 float* __restrict__ out, uint8_t* flags,
                                                                 int64_t flag_index, LossArgs la) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float part[kHeadThreads / 32][CMAX];
   const int64_t r = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -155,6 +158,8 @@ __global__ void __launch_bounds__(kHeadThreads) head_bwd_kernel(const float* __r
                                                                 const float* __restrict__ w, float* __restrict__ dx,
                                                                 float* __restrict__ dw, float* __restrict__ db,
                                                                 int accumulate, int64_t dx_blocks) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float gs[];  // g (rows x C) when it fits, else one row
   const int tid = threadIdx.x;
   if ((int64_t)blockIdx.x < dx_blocks) {
@@ -238,13 +243,16 @@ int launch_head_fwd(const float* x, int64_t rows, int64_t in, const float* w, co
   const dim3 grid((unsigned)rows);
   switch (head_cmax(classes)) {
     case 8:
-      head_fwd_kernel<8, LOSS><<<grid, kHeadThreads, 0, s>>>(x, rows, in, w, b, classes, out, flags, flag_index, la);
+      pdl_launch(head_fwd_kernel<8, LOSS>, grid, dim3(kHeadThreads), 0, s, x, rows, in, w, b, classes, out, flags,
+                 flag_index, la);
       break;
     case 16:
-      head_fwd_kernel<16, LOSS><<<grid, kHeadThreads, 0, s>>>(x, rows, in, w, b, classes, out, flags, flag_index, la);
+      pdl_launch(head_fwd_kernel<16, LOSS>, grid, dim3(kHeadThreads), 0, s, x, rows, in, w, b, classes, out, flags,
+                 flag_index, la);
       break;
     default:
-      head_fwd_kernel<32, LOSS><<<grid, kHeadThreads, 0, s>>>(x, rows, in, w, b, classes, out, flags, flag_index, la);
+      pdl_launch(head_fwd_kernel<32, LOSS>, grid, dim3(kHeadThreads), 0, s, x, rows, in, w, b, classes, out, flags,
+                 flag_index, la);
       break;
   }
   cudaError_t e = cudaGetLastError();
@@ -292,16 +300,16 @@ int po_head_bwd(const float* x, int64_t rows, int64_t in, const float* g, int32_
   const dim3 grid((unsigned)(dx_blocks + dw_blocks));
   switch (head_cmax(classes)) {
     case 8:
-      head_bwd_kernel<8><<<grid, kHeadThreads, smem, s>>>(x, rows, in, g, classes, w, dx, dw, db, accumulate,
-                                                          dx_blocks);
+      pdl_launch(head_bwd_kernel<8>, grid, dim3(kHeadThreads), smem, s, x, rows, in, g, classes, w, dx, dw, db,
+                 accumulate, dx_blocks);
       break;
     case 16:
-      head_bwd_kernel<16><<<grid, kHeadThreads, smem, s>>>(x, rows, in, g, classes, w, dx, dw, db, accumulate,
-                                                           dx_blocks);
+      pdl_launch(head_bwd_kernel<16>, grid, dim3(kHeadThreads), smem, s, x, rows, in, g, classes, w, dx, dw, db,
+                 accumulate, dx_blocks);
       break;
     default:
-      head_bwd_kernel<32><<<grid, kHeadThreads, smem, s>>>(x, rows, in, g, classes, w, dx, dw, db, accumulate,
-                                                           dx_blocks);
+      pdl_launch(head_bwd_kernel<32>, grid, dim3(kHeadThreads), smem, s, x, rows, in, g, classes, w, dx, dw, db,
+                 accumulate, dx_blocks);
       break;
   }
   cudaError_t e = cudaGetLastError();

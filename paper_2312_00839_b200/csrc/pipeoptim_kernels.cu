@@ -27,6 +27,7 @@
 
 #include "pipeoptim.h"
 #include "pipeoptim_rules.cuh"
+#include "pipeoptim_pdl.cuh"
 
 namespace {
 
@@ -209,6 +210,8 @@ constexpr int kPrefetch = 3;
 // at ~6.5 TB/s x ~0.8 us needs ~5 MB in flight chip-wide, ~35 KB per SM).
 template <int KIND, int MODE, int VEC, int CACHE, int UNROLL>
 __global__ void __launch_bounds__(512) po_stream_kernel(const Args a) {
+  pdl_wait();  // PDL launches: the predecessor's writes (gradient, coefficients) are complete
+  pdl_trigger();
   const int64_t nv = a.n / VEC;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -341,13 +344,13 @@ template <int KIND, int MODE, int VEC, int CACHE>
 cudaError_t launch_unroll(const Args& a, const Shape& sh, dim3 grid, dim3 block, cudaStream_t s) {
   if constexpr (tunable(MODE) && VEC > 1) {
     switch (sh.unroll) {
-      case 1: po_stream_kernel<KIND, MODE, VEC, CACHE, 1><<<grid, block, 0, s>>>(a); break;
-      case kPrefetch: po_stream_kernel<KIND, MODE, VEC, CACHE, kPrefetch><<<grid, block, 0, s>>>(a); break;
-      case 4: po_stream_kernel<KIND, MODE, VEC, CACHE, 4><<<grid, block, 0, s>>>(a); break;
-      default: po_stream_kernel<KIND, MODE, VEC, CACHE, 2><<<grid, block, 0, s>>>(a); break;
+      case 1: pdl_launch(po_stream_kernel<KIND, MODE, VEC, CACHE, 1>, grid, block, 0, s, a); break;
+      case kPrefetch: pdl_launch(po_stream_kernel<KIND, MODE, VEC, CACHE, kPrefetch>, grid, block, 0, s, a); break;
+      case 4: pdl_launch(po_stream_kernel<KIND, MODE, VEC, CACHE, 4>, grid, block, 0, s, a); break;
+      default: pdl_launch(po_stream_kernel<KIND, MODE, VEC, CACHE, 2>, grid, block, 0, s, a); break;
     }
   } else {
-    po_stream_kernel<KIND, MODE, VEC, CACHE, (VEC > 1 ? 2 : 4)><<<grid, block, 0, s>>>(a);
+    pdl_launch(po_stream_kernel<KIND, MODE, VEC, CACHE, (VEC > 1 ? 2 : 4)>, grid, block, 0, s, a);
   }
   return cudaGetLastError();
 }
@@ -818,6 +821,10 @@ cudaError_t launch_dp(const DpArgs& d, int vec, dim3 grid, dim3 block, cudaStrea
 }  // namespace
 
 extern "C" {
+
+static int32_t g_pdl = 0;
+void po_set_pdl(int32_t on) { g_pdl = on ? 1 : 0; }
+int32_t po_get_pdl(void) { return g_pdl; }
 
 int po_abi_version(void) { return PO_ABI_VERSION; }
 

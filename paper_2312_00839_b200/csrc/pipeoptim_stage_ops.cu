@@ -26,10 +26,13 @@
 #include <stdint.h>
 
 #include "pipeoptim.h"
+#include "pipeoptim_pdl.cuh"
 
 namespace {
 
 __global__ void all_finite_kernel(const float* __restrict__ x, int64_t n, uint8_t* flags, int64_t index) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool bad = false;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -80,6 +83,8 @@ __device__ __forceinline__ float block_reduce_sum(float v, float* sh) {
 __global__ void loss_grad_kernel(const float* __restrict__ pred, const float* __restrict__ target, int64_t rows,
                                  int64_t cols, int kind, float* __restrict__ grad, float* __restrict__ row_part,
                                  unsigned int* counter, float* loss) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sh[33];
   __shared__ bool last;
   const int64_t r = blockIdx.x;
@@ -146,6 +151,8 @@ constexpr int kReluCols = 8, kReluLanes = 64;
 // by one thread)
 __global__ void relu_bwd_bias_kernel(const float* g, int splits, const float* __restrict__ h, int64_t rows,
                                      int64_t cols, float* dpre, float* __restrict__ db, int accumulate, int mask) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n = rows * cols;
   __shared__ float part[kReluLanes][kReluCols];
   const int cl = threadIdx.x % kReluCols, lane = threadIdx.x / kReluCols;
@@ -191,6 +198,8 @@ template <bool VEC4>
 __global__ void splitk_bias_act_kernel(const float* __restrict__ part, int S, int64_t n, int64_t cols,
                                        const float* __restrict__ bias, int act, float* __restrict__ out,
                                        float* __restrict__ pre_out, uint8_t* flags, int64_t flag_index) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   bool bad = false;
   if constexpr (VEC4) {
@@ -294,7 +303,7 @@ int po_all_finite(const float* x, int64_t n, uint8_t* flags, int64_t index, void
   const int block = 256;
   int64_t want = (n / 4 + block - 1) / block;
   int64_t grid = want < 1 ? 1 : (want > 4 * sms ? 4 * sms : want);
-  all_finite_kernel<<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(x, n, flags, index);
+  pdl_launch(all_finite_kernel, dim3((unsigned)grid), dim3(block), 0, (cudaStream_t)stream, x, n, flags, index);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }
@@ -315,12 +324,11 @@ int po_splitk_bias_act(const float* part, int32_t splits, int64_t rows, int64_t 
   int64_t want = ((vec ? n / 4 : n) + block - 1) / block;
   const int64_t grid = want > 8 * sms ? 8 * sms : want;
   if (vec)
-    splitk_bias_act_kernel<true><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(part, splits, n, cols, bias, act,
-                                                                                    out, pre_out, flags, flag_index);
+    pdl_launch(splitk_bias_act_kernel<true>, dim3((unsigned)grid), dim3(block), 0, (cudaStream_t)stream, part, splits, n,
+               cols, bias, act, out, pre_out, flags, flag_index);
   else
-    splitk_bias_act_kernel<false><<<(unsigned)grid, block, 0, (cudaStream_t)stream>>>(part, splits, n, cols, bias,
-                                                                                     act, out, pre_out, flags,
-                                                                                     flag_index);
+    pdl_launch(splitk_bias_act_kernel<false>, dim3((unsigned)grid), dim3(block), 0, (cudaStream_t)stream, part, splits,
+               n, cols, bias, act, out, pre_out, flags, flag_index);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }
@@ -343,9 +351,8 @@ int po_act_bwd_bias(int32_t act, const float* g, int32_t splits, const float* h,
   if (g == nullptr || (act == 1 && h == nullptr) || dpre == nullptr || db == nullptr) return PO_EINVAL;
   const int64_t grid = (cols + kReluCols - 1) / kReluCols;
   if (grid > 0x7fffffff) return PO_EINVAL;
-  relu_bwd_bias_kernel<<<(unsigned)grid, kReluCols * kReluLanes, 0, (cudaStream_t)stream>>>(g, splits, h, rows,
-                                                                                           cols, dpre, db,
-                                                                                           accumulate, act);
+  pdl_launch(relu_bwd_bias_kernel, dim3((unsigned)grid), dim3(kReluCols * kReluLanes), 0, (cudaStream_t)stream, g,
+             splits, h, rows, cols, dpre, db, accumulate, act);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }
@@ -358,8 +365,8 @@ int po_loss_grad(int32_t kind, const float* pred, const float* target, int64_t r
   if (rows > 0x7fffffff) return PO_EINVAL;
   // scratch layout: [rows] float row partials, then one uint32 counter (caller zeroes it once)
   unsigned int* counter = reinterpret_cast<unsigned int*>(scratch + rows);
-  loss_grad_kernel<<<(unsigned)rows, kLossThreads, 0, (cudaStream_t)stream>>>(pred, target, rows, cols, kind, grad,
-                                                                             scratch, counter, loss);
+  pdl_launch(loss_grad_kernel, dim3((unsigned)rows), dim3(kLossThreads), 0, (cudaStream_t)stream, pred, target, rows,
+             cols, kind, grad, scratch, counter, loss);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : (int)e;
 }

@@ -223,3 +223,39 @@ def test_traced_run_device_timeline(tmp_path, streams):
     lines = out.read_text().splitlines()
     assert lines[0] == reports.DEVICE_TIMELINE_CSV_HEADER and len(lines) == 1 + len(tl.events)
     torch.cuda.synchronize()
+
+
+def test_pdl_switch_leaves_results_bit_identical():
+    """po_set_pdl(1) (programmatic dependent launch of the short stream
+    kernels; every kernel waits for its predecessor before touching memory)
+    gives the same bits as plain launches: a config-1-shaped graphed run with
+    the switch on vs off; the _lib.pdl context restores the setting."""
+    import torch
+
+    from paper_2312_00839_b200 import _lib
+    from paper_2312_00839_b200.bench_pipeline import DeviceBatches
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import GraphedExecute, build_timeline, execute
+    from paper_2312_00839_b200.stages import build_layers, build_stages, torch_init
+
+    dev = torch.device("cuda", 0)
+    dims, acts = [1024, 512, 512, 10], ["relu", "relu", "linear"]
+    data = DeviceBatches(torch, dev, dims=dims)
+    tl = build_timeline("optimizer_prediction", 3, 9)
+    assert _lib.load().po_get_pdl() == 0
+    out = {}
+    for on in (False, True):
+        with _lib.pdl(on):
+            assert _lib.load().po_get_pdl() == int(on)
+            stages = build_stages(build_layers(dims, acts), 3, torch_init(2, dev), device=dev)
+            opts = [OptimizerState(OptimizerConfig("adamw"), s.param_names, device=dev) for s in stages]
+            rep = execute(tl, stages, opts, "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-3,
+                          checks="deferred")
+            g = GraphedExecute(tl, stages, opts, "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-3)
+            g.replay()
+            torch.cuda.synchronize()
+            out[on] = (rep.losses, g.report().losses, [s.flat.data.clone() for s in stages])
+    assert _lib.load().po_get_pdl() == 0
+    assert out[False][0] == out[True][0] and out[False][1] == out[True][1]
+    for x, y in zip(out[False][2], out[True][2]):
+        assert torch.equal(x, y)
