@@ -308,10 +308,10 @@ int po_head_bwd(const float* x, int64_t rows, int64_t in, const float* g, int32_
  * po_splitk_bias_act, po_relu_bwd_bias / po_act_bwd_bias, po_head_*,
  * po_loss_grad): po_set_pdl(1) launches them with the programmatic
  * stream-serialisation attribute (each waits for its predecessor before
- * touching memory: results unchanged); process-wide, default 0.
+ * touching memory: results unchanged); process-wide, default 0; returns 0.
  * po_get_pdl returns the current setting. */
-void po_set_pdl(int32_t on);
-int32_t po_get_pdl(void);
+int po_set_pdl(int32_t on);
+int po_get_pdl(void);
 
 /* po_head_fwd_loss: po_head_fwd and po_loss_grad in ONE launch (the last
  * stage's forward + loss + dL/dout, runtime.py:415-426 via stages.py:175-184

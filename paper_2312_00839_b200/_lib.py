@@ -170,8 +170,8 @@ _SIGNATURES = {
     "po_nvls_free": (ctypes.c_int, [_P]),
     "po_head_supported": (ctypes.c_int, [_I64, _I64, _I64]),
     "po_head_fwd": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, _P, _I64, _P]),
-    "po_set_pdl": (None, [ctypes.c_int32]),
-    "po_get_pdl": (ctypes.c_int32, []),
+    "po_set_pdl": (ctypes.c_int, [ctypes.c_int32]),
+    "po_get_pdl": (ctypes.c_int, []),
     "po_head_fwd_loss": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P,
                                         _P, _P, _I64, _P]),
     "po_head_bwd": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.c_int32, _P, _P, _P, _P, ctypes.c_int32, _P]),

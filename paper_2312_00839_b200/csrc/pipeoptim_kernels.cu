@@ -823,8 +823,11 @@ cudaError_t launch_dp(const DpArgs& d, int vec, dim3 grid, dim3 block, cudaStrea
 extern "C" {
 
 static int32_t g_pdl = 0;
-void po_set_pdl(int32_t on) { g_pdl = on ? 1 : 0; }
-int32_t po_get_pdl(void) { return g_pdl; }
+int po_set_pdl(int32_t on) {
+  g_pdl = on ? 1 : 0;
+  return 0;
+}
+int po_get_pdl(void) { return g_pdl; }
 
 int po_abi_version(void) { return PO_ABI_VERSION; }
 
