@@ -17,11 +17,12 @@ from paper_2312_00839_b200.stages import build_layers, build_stages, torch_init 
 dev = torch.device("cuda", 0)
 data = DeviceBatches(torch, dev)
 n = 64
+STREAMS = sys.argv[1] if len(sys.argv) > 1 else "stage"
 variants = {"default": None}
-for block, cps, unroll in ((128, 16, 1), (256, 8, 1)):
+for block, cps, unroll in ((128, 16, 1), (256, 8, 1), (128, 8, 1), (256, 4, 1), (512, 2, 1), (128, 4, 2)):
     for cache in (1, 4):
         variants[f"{block}x{cps}u{unroll}c{cache}"] = (block, cps, 8, cache, unroll)
-for tf32 in (False, True):
+for tf32 in (False,):
     torch.cuda.empty_cache()
     torch.backends.cuda.matmul.allow_tf32 = tf32
     for name, la in variants.items():
@@ -31,7 +32,7 @@ for tf32 in (False, True):
             launch = _lib.make_launch(*la) if la else None
             opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=dev, launch=launch) for s in stages]
             g = GraphedExecute(build_timeline(strategy, 4, n), stages, opts, strategy, data, "softmax_xent",
-                               lambda mb: 1e-4, warmup_runs=1)
+                               lambda mb: 1e-4, warmup_runs=1, streams=STREAMS)
             g.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

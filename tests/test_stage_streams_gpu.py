@@ -259,3 +259,43 @@ def test_pdl_switch_leaves_results_bit_identical():
     assert out[False][0] == out[True][0] and out[False][1] == out[True][1]
     for x, y in zip(out[False][2], out[True][2]):
         assert torch.equal(x, y)
+
+
+def test_shared_gpu_optimizer_launch_is_scoped_to_the_run():
+    """With >= 4 stages sharing the GPU the runner launches the stages' K2/K3
+    in its shared-GPU shape (runtime.SHARED_GPU_OPT_LAUNCH) only for the run,
+    never over a caller's own launch shape; results equal a run with the
+    default shape, bit for bit."""
+    import torch
+
+    from paper_2312_00839_b200 import _lib, runtime
+    from paper_2312_00839_b200.bench_pipeline import DeviceBatches
+    from paper_2312_00839_b200.optim import OptimizerConfig, OptimizerState
+    from paper_2312_00839_b200.runtime import build_timeline, execute
+    from paper_2312_00839_b200.stages import build_layers, build_stages, torch_init
+
+    dev = torch.device("cuda", 0)
+    dims, acts = [512, 384, 384, 256, 10], ["relu", "relu", "relu", "linear"]
+    data = DeviceBatches(torch, dev, dims=dims)
+    tl = build_timeline("optimizer_prediction", 4, 10)
+    own = _lib.make_launch(256, 4, 8, 1, 1)
+    out = {}
+    for shape in (runtime.SHARED_GPU_OPT_LAUNCH, None):
+        old = runtime.SHARED_GPU_OPT_LAUNCH
+        runtime.SHARED_GPU_OPT_LAUNCH = shape
+        try:
+            stages = build_stages(build_layers(dims, acts), 4, torch_init(4, dev), device=dev)
+            opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=dev,
+                                   launch=own if i == 1 else None) for i, s in enumerate(stages)]
+            rep = execute(tl, stages, opts, "optimizer_prediction", data, "softmax_xent", lambda mb: 1e-3,
+                          checks="deferred", streams="stage")
+            torch.cuda.synchronize()
+        finally:
+            runtime.SHARED_GPU_OPT_LAUNCH = old
+        assert [o._launch is None for o in opts] == [True, False, True, True]
+        assert opts[1]._launch is own
+        out[shape] = (rep.losses, [s.flat.data.clone() for s in stages])
+    a, b = out.values()
+    assert a[0] == b[0]
+    for x, y in zip(a[1], b[1]):
+        assert torch.equal(x, y)
