@@ -365,6 +365,16 @@ int po_gemm_f32x3(int32_t a_col_major, int32_t b_col_major, const float* a, int6
 #define PO_ENOSYS (-38)
 int po_gemm_f32x3_available(void);
 
+/* Tile width (64 or 128 output columns per 128-row CTA tile) of the next
+ * po_gemm_f32x3 calls, process-wide, read at launch / capture time: 64 (the
+ * default) gives the most CTAs and the lowest latency for a stage alone on
+ * its GPU; 128 halves the CTAs (less SM time per GEMM), faster when several
+ * stages share one GPU. Results differ only in fp32 summation grouping
+ * inside a tile (both <= 2e-6 of the largest output vs float64).
+ * po_set_gemm_tile: PO_EINVAL for other widths. */
+int po_set_gemm_tile(int32_t tile_n);
+int po_get_gemm_tile(void);
+
 /* ---- peer-memory boundary transport (pipeoptim_p2p.cu) ------------------
  * Replaces the simulated hand-off dicts of the reference executor
  * (runtime.py:390-391, 420-433): one direction of a pipeline boundary is a

@@ -56,6 +56,8 @@ EXPORTS = (
     "po_head_fwd",
     "po_head_fwd_loss",
     "po_set_pdl",
+    "po_set_gemm_tile",
+    "po_get_gemm_tile",
     "po_get_pdl",
     "po_head_bwd",
     "po_wgrad_update_supported",
@@ -170,6 +172,8 @@ _SIGNATURES = {
     "po_nvls_free": (ctypes.c_int, [_P]),
     "po_head_supported": (ctypes.c_int, [_I64, _I64, _I64]),
     "po_head_fwd": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, _P, _I64, _P]),
+    "po_set_gemm_tile": (ctypes.c_int, [ctypes.c_int32]),
+    "po_get_gemm_tile": (ctypes.c_int, []),
     "po_set_pdl": (ctypes.c_int, [ctypes.c_int32]),
     "po_get_pdl": (ctypes.c_int, []),
     "po_head_fwd_loss": (ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int32, _P, ctypes.c_int32, _P, _P, _P,

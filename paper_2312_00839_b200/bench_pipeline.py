@@ -247,7 +247,7 @@ def single_gpu_pipeline(torch, device, n_batches: int = 64, depth: int = 4, repl
     out = {"config": f"config1 MLP {CONFIG1_DIMS}, B={BATCH}, Adam lr 1e-4, 1F1B D={depth} on 1 GPU "
                      f"(single-process runner, one CUDA stream per stage, CUDA-graph replay of whole "
                      f"{n_batches}-mini-batch runs), {'TF32' if tf32 else 'fp32 (TF32 off)'} GEMMs"
-                     f"{'' if tf32 or depth < 4 else ' (split-K <= 4 K slices while the stages share the GPU)'}, "
+                     f"{'' if tf32 or depth < 4 else ' (4 K slices, 128-wide tiles while the stages share the GPU)'}, "
                      f"fp32 master weights"}
     launches = 0
     pair = _graphed_pair(torch, device, depth, n_batches, data, replays)

@@ -39,7 +39,7 @@ using ElementAcc = float;
 using LayoutD = cutlass::layout::RowMajor;
 constexpr int kAlign = 4;  // 16-byte TMA alignment in floats
 
-#ifndef PO_FASTF32_TILE_N
+#ifndef PO_FASTF32_TILE_N  // the default tile width (po_set_gemm_tile selects 64 or 128 at run time)
 #define PO_FASTF32_TILE_N 64
 #endif
 #ifndef PO_FASTF32_TILE_K
@@ -48,41 +48,46 @@ constexpr int kAlign = 4;  // 16-byte TMA alignment in floats
 #ifndef PO_FASTF32_KMAJOR_A_SCHEDULE  // K-major A: bf16 pieces staged in shared memory (Smem) or TMEM
 #define PO_FASTF32_KMAJOR_A_SCHEDULE KernelTmaWarpSpecialized1SmFastFP32SmemSm100
 #endif
-using MmaTileShape = Shape<_128, Int<PO_FASTF32_TILE_N>, Int<PO_FASTF32_TILE_K>>;
-using ClusterShape = Shape<_1, _1, _1>;
-
-// The epilogue is layout-independent; one mainloop per operand-major pair.
-// (Written out per variant, not as a class template: nvcc's host stubs lose
-// the dependent `typename` of a templated CollectiveBuilder chain.)
-using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
-    cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
-    cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, ElementAcc, void, LayoutD, kAlign, float, LayoutD,
-    kAlign, cutlass::epilogue::collective::EpilogueScheduleAuto>::CollectiveOp;
 #ifndef PO_FASTF32_EXTRA_CARVEOUT  // bytes held back from the stage count (fewer stages, more CTAs per SM)
 #define PO_FASTF32_EXTRA_CARVEOUT 0
 #endif
-constexpr int kEpiCarveout =
-    static_cast<int>(sizeof(typename CollectiveEpilogue::SharedStorage)) + PO_FASTF32_EXTRA_CARVEOUT;
+using ClusterShape = Shape<_1, _1, _1>;
 
-#define PO_FAST_F32_GEMM(NAME, LAYOUT_A, LAYOUT_B, SCHEDULE)                                                       \
-  namespace NAME {                                                                                                 \
-  using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<                                         \
-      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, LAYOUT_A, kAlign, float, LAYOUT_B, kAlign,      \
-      ElementAcc, MmaTileShape, ClusterShape, cutlass::gemm::collective::StageCountAutoCarveout<kEpiCarveout>,      \
-      cutlass::gemm::SCHEDULE>::CollectiveOp;                                                                      \
-  using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop, CollectiveEpilogue,    \
-                                                      void>;                                                       \
-  struct G {                                                                                                       \
-    using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;                                              \
-  };                                                                                                               \
-  }
+// One epilogue per tile shape; one mainloop per (tile width, operand-major
+// pair). Two tile widths: 128 x 64 (more CTAs: the lowest latency for a
+// stage alone on its GPU) and 128 x 128 (half the CTAs: less SM time per
+// GEMM, the faster choice when several stages share one GPU —
+// profiles/r2_gemm_tile_shared_gpu.jsonl).
+template <int TN>
+struct Tiles {
+  using MmaTileShape = Shape<_128, Int<TN>, Int<PO_FASTF32_TILE_K>>;
+  using CollectiveEpilogue = typename cutlass::epilogue::collective::CollectiveBuilder<
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, MmaTileShape, ClusterShape,
+      cutlass::epilogue::collective::EpilogueTileAuto, ElementAcc, ElementAcc, void, LayoutD, kAlign, float,
+      LayoutD, kAlign, cutlass::epilogue::collective::EpilogueScheduleAuto>::CollectiveOp;
+  static constexpr int kEpiCarveout =
+      static_cast<int>(sizeof(typename CollectiveEpilogue::SharedStorage)) + PO_FASTF32_EXTRA_CARVEOUT;
+};
 
-PO_FAST_F32_GEMM(row_row, cutlass::layout::RowMajor, cutlass::layout::RowMajor, PO_FASTF32_KMAJOR_A_SCHEDULE)  // x@W
-PO_FAST_F32_GEMM(col_row, cutlass::layout::ColumnMajor, cutlass::layout::RowMajor,
-                 KernelTmaWarpSpecialized1SmFastFP32SmemSm100)  // x^T @ dpre (M-major A: shared-memory staging)
-PO_FAST_F32_GEMM(row_col, cutlass::layout::RowMajor, cutlass::layout::ColumnMajor,
-                 PO_FASTF32_KMAJOR_A_SCHEDULE)  // dpre @ W^T
-#undef PO_FAST_F32_GEMM
+template <int TN, class LayoutA, class LayoutB, class Schedule>
+struct FastF32Gemm {
+  using T = Tiles<TN>;
+  using Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<
+      cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, LayoutA, kAlign, float, LayoutB, kAlign,
+      ElementAcc, typename T::MmaTileShape, ClusterShape,
+      cutlass::gemm::collective::StageCountAutoCarveout<T::kEpiCarveout>, Schedule>::CollectiveOp;
+  using Kernel = cutlass::gemm::kernel::GemmUniversal<Shape<int, int, int, int>, Mainloop,
+                                                      typename T::CollectiveEpilogue, void>;
+  using Gemm = cutlass::gemm::device::GemmUniversalAdapter<Kernel>;
+};
+
+using cutlass::layout::ColumnMajor;
+using cutlass::layout::RowMajor;
+using SmemSched = cutlass::gemm::KernelTmaWarpSpecialized1SmFastFP32SmemSm100;
+using KmajSched = cutlass::gemm::PO_FASTF32_KMAJOR_A_SCHEDULE;
+template <int TN> using RowRowT = FastF32Gemm<TN, RowMajor, RowMajor, KmajSched>;     // x @ W
+template <int TN> using ColRowT = FastF32Gemm<TN, ColumnMajor, RowMajor, SmemSched>;  // x^T @ dpre (M-major A)
+template <int TN> using RowColT = FastF32Gemm<TN, RowMajor, ColumnMajor, KmajSched>;  // dpre @ W^T
 
 template <class G>
 int run_gemm(typename G::Gemm::GemmKernel::StrideA sa_, typename G::Gemm::GemmKernel::StrideB sb_, const float* a,
@@ -119,9 +124,33 @@ int run_gemm(typename G::Gemm::GemmKernel::StrideA sa_, typename G::Gemm::GemmKe
   return e == cudaSuccess ? 0 : (int)e;
 }
 
-using RowRow = row_row::G;
-using ColRow = col_row::G;
-using RowCol = row_col::G;
+// tile width of the next po_gemm_f32x3 calls (po_set_gemm_tile; process-wide)
+int g_tile_n = PO_FASTF32_TILE_N;
+
+template <int TN>
+int dispatch_gemm(int32_t a_col_major, int32_t b_col_major, const float* a, int64_t lda, int64_t sa, const float* b,
+                  int64_t ldb, int64_t sb, float* d, int64_t m, int64_t n, int64_t k, int64_t batch,
+                  void* workspace, int64_t workspace_bytes, cudaStream_t s) {
+  if (!a_col_major && !b_col_major) {  // A (m,k) at m*lda + k; B (k,n) at k*ldb + n
+    if (lda < k || ldb < n) return PO_EINVAL;
+    return run_gemm<RowRowT<TN>>(cute::make_stride(lda, cute::Int<1>{}, sa),
+                                 cute::make_stride(cute::Int<1>{}, ldb, sb), a, b, d, m, n, k, batch, workspace,
+                                 workspace_bytes, s);
+  }
+  if (a_col_major && !b_col_major) {  // A (m,k) at m + k*lda
+    if (lda < m || ldb < n) return PO_EINVAL;
+    return run_gemm<ColRowT<TN>>(cute::make_stride(cute::Int<1>{}, lda, sa),
+                                 cute::make_stride(cute::Int<1>{}, ldb, sb), a, b, d, m, n, k, batch, workspace,
+                                 workspace_bytes, s);
+  }
+  if (!a_col_major && b_col_major) {  // B (k,n) at k + n*ldb
+    if (lda < k || ldb < k) return PO_EINVAL;
+    return run_gemm<RowColT<TN>>(cute::make_stride(lda, cute::Int<1>{}, sa),
+                                 cute::make_stride(ldb, cute::Int<1>{}, sb), a, b, d, m, n, k, batch, workspace,
+                                 workspace_bytes, s);
+  }
+  return PO_EINVAL;
+}
 
 }  // namespace
 
@@ -130,12 +159,20 @@ extern "C" {
 #ifdef PO_PROBE_EXPORTS
 int po_probe_gemm_smem(int variant) {
   switch (variant) {
-    case 0: return (int)sizeof(typename row_row::Kernel::SharedStorage);
-    case 1: return (int)sizeof(typename col_row::Kernel::SharedStorage);
-    default: return (int)sizeof(typename row_col::Kernel::SharedStorage);
+    case 0: return (int)sizeof(typename RowRowT<PO_FASTF32_TILE_N>::Kernel::SharedStorage);
+    case 1: return (int)sizeof(typename ColRowT<PO_FASTF32_TILE_N>::Kernel::SharedStorage);
+    default: return (int)sizeof(typename RowColT<PO_FASTF32_TILE_N>::Kernel::SharedStorage);
   }
 }
 #endif
+
+int po_set_gemm_tile(int32_t tile_n) {
+  if (tile_n != 64 && tile_n != 128) return PO_EINVAL;
+  g_tile_n = tile_n;
+  return 0;
+}
+
+int po_get_gemm_tile(void) { return g_tile_n; }
 
 int po_gemm_f32x3_available(void) { return 1; }
 
@@ -145,22 +182,11 @@ int po_gemm_f32x3(int32_t a_col_major, int32_t b_col_major, const float* a, int6
   if (m < 1 || n < 1 || k < 1 || batch < 1 || a == nullptr || b == nullptr || d == nullptr) return PO_EINVAL;
   if (lda % kAlign || ldb % kAlign || n % kAlign || sa % kAlign || sb % kAlign) return PO_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  if (!a_col_major && !b_col_major) {  // A (m,k) at m*lda + k; B (k,n) at k*ldb + n
-    if (lda < k || ldb < n) return PO_EINVAL;
-    return run_gemm<RowRow>(cute::make_stride(lda, cute::Int<1>{}, sa), cute::make_stride(cute::Int<1>{}, ldb, sb),
-                            a, b, d, m, n, k, batch, workspace, workspace_bytes, s);
-  }
-  if (a_col_major && !b_col_major) {  // A (m,k) at m + k*lda
-    if (lda < m || ldb < n) return PO_EINVAL;
-    return run_gemm<ColRow>(cute::make_stride(cute::Int<1>{}, lda, sa), cute::make_stride(cute::Int<1>{}, ldb, sb),
-                            a, b, d, m, n, k, batch, workspace, workspace_bytes, s);
-  }
-  if (!a_col_major && b_col_major) {  // B (k,n) at k + n*ldb
-    if (lda < k || ldb < k) return PO_EINVAL;
-    return run_gemm<RowCol>(cute::make_stride(lda, cute::Int<1>{}, sa), cute::make_stride(ldb, cute::Int<1>{}, sb),
-                            a, b, d, m, n, k, batch, workspace, workspace_bytes, s);
-  }
-  return PO_EINVAL;
+  if (g_tile_n == 128)
+    return dispatch_gemm<128>(a_col_major, b_col_major, a, lda, sa, b, ldb, sb, d, m, n, k, batch, workspace,
+                              workspace_bytes, s);
+  return dispatch_gemm<64>(a_col_major, b_col_major, a, lda, sa, b, ldb, sb, d, m, n, k, batch, workspace,
+                           workspace_bytes, s);
 }
 
 }  // extern "C"

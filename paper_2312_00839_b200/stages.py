@@ -307,6 +307,26 @@ def gemm_split_cap(cap: int):
         _tc_split_cap = old
 
 
+@contextlib.contextmanager
+def gemm_tile(tile_n: int | None):
+    """Tile width (64 or 128 output columns) of the tensor-core GEMMs for the
+    duration (po_set_gemm_tile; None leaves the current one). 64: most CTAs,
+    lowest latency (a stage alone on its GPU); 128: half the CTAs, less SM
+    time (stages sharing one GPU)."""
+    if tile_n is None:
+        yield
+        return
+    from . import _lib
+
+    lib = _lib.load()
+    old = lib.po_get_gemm_tile()
+    _lib.check(lib.po_set_gemm_tile(int(tile_n)), "po_set_gemm_tile")
+    try:
+        yield
+    finally:
+        lib.po_set_gemm_tile(old)
+
+
 def _splitk_tc(rows: int, k: int) -> int:
     """K slices for the tensor-core GEMM of a small-M long-K shape: <= 8
     slices of >= 128 (scripts/gemm_f32x3_check.py: 3072x1024 forward 14 us at

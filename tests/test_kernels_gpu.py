@@ -537,9 +537,10 @@ def test_empty_and_tiny_buffers(lib):
         assert np.array_equal(f32(dw), ew) and np.array_equal(f32(out), ewh)
 
 
+@pytest.mark.parametrize("tile_n", [64, 128])
 @pytest.mark.parametrize("variant", ["row_row", "col_row", "row_col"])
 @pytest.mark.parametrize("m,n,k,batch", [(128, 1024, 384, 8), (7, 20, 36, 1), (300, 64, 129, 3)])
-def test_fast_fp32_gemm_matches_float64(variant, m, n, k, batch):
+def test_fast_fp32_gemm_matches_float64(variant, m, n, k, batch, tile_n):
     """po_gemm_f32x3 (tcgen05, 3x bf16 split, fp32 accumulation) vs float64 on
     every operand-major variant, batched: fp32-level accuracy (<= 2e-6
     relative to the largest output, the SIMT SGEMM's level)."""
@@ -557,9 +558,15 @@ def test_fast_fp32_gemm_matches_float64(variant, m, n, k, batch):
     if lda % 4 or ldb % 4 or n % 4:
         pytest.skip("operand strides must be 16-byte aligned")
     d = torch.empty(batch, m, n, device="cuda")
-    rc = _lib.load().po_gemm_f32x3(a_col, b_col, a.data_ptr(), lda, a[0].numel(), b.data_ptr(), ldb, b[0].numel(),
-                                   d.data_ptr(), m, n, k, batch, None, 0, torch.cuda.current_stream().cuda_stream)
-    assert rc == 0
+    from paper_2312_00839_b200.stages import gemm_tile
+
+    with gemm_tile(tile_n):
+        assert _lib.load().po_get_gemm_tile() == tile_n
+        rc = _lib.load().po_gemm_f32x3(a_col, b_col, a.data_ptr(), lda, a[0].numel(), b.data_ptr(), ldb,
+                                       b[0].numel(), d.data_ptr(), m, n, k, batch, None, 0,
+                                       torch.cuda.current_stream().cuda_stream)
+    assert rc == 0 and _lib.load().po_get_gemm_tile() == 64
+    assert _lib.load().po_set_gemm_tile(96) == _lib.PO_EINVAL
     A = a.double().transpose(1, 2) if a_col else a.double()
     B = b.double().transpose(1, 2) if b_col else b.double()
     want = A @ B

@@ -11,7 +11,7 @@ from test_runtime_gpu import CONFIG1, EXTRA, SMALL, build, check_losses, rec_tup
 pytestmark = pytest.mark.gpu
 
 
-def _run(case, streams, checks="eager", fuse=True, gemm_split_cap=None):
+def _run(case, streams, checks="eager", fuse=True, gemm_split_cap=None, gemm_tile_n=None):
     from oracle import data_ref
     from paper_2312_00839_b200.runtime import execute
     from test_runtime_gpu import ArraySource, Source
@@ -23,7 +23,8 @@ def _run(case, streams, checks="eager", fuse=True, gemm_split_cap=None):
         batches, loss = data_ref.config1(seed=case["data_seed"])
         src = ArraySource(batches)
     rep = execute(tl, stages, opts, case["strategy"], src, loss, lambda mb, lr=case["lr"]: lr,
-                  checks=checks, fuse=fuse, streams=streams, gemm_split_cap=gemm_split_cap)
+                  checks=checks, fuse=fuse, streams=streams, gemm_split_cap=gemm_split_cap,
+                  gemm_tile_n=gemm_tile_n)
     return rep, stages
 
 
@@ -50,18 +51,19 @@ def test_stage_streams_bit_identical_to_serial(case):
 @pytest.mark.parametrize("case", CONFIG1, ids=lambda c: c["strategy"])
 def test_config1_stage_streams_host_batches(case):
     """Host (numpy) batches: x and y are staged to the device on stage 0's
-    stream and consumed by the last stage's. Under one GEMM split policy the
-    two runners agree bit for bit: the stage runner's default (the shared-GPU
-    cap, runtime.SHARED_GPU_SPLIT_CAP) == the serial runner at that cap, and
-    both runners at the latency cap (8) agree too; either policy meets the
-    reference goldens."""
+    stream and consumed by the last stage's. Under one GEMM policy (split
+    cap, tile width) the two runners agree bit for bit: the stage runner's
+    default (the shared-GPU policy: 4 slices, 128-wide tiles) == the serial
+    runner under it, and both runners under the latency policy (8, 64)
+    agree too; either policy meets the reference goldens."""
     from paper_2312_00839_b200 import runtime
 
-    a, sa = _run(case, "serial", checks="deferred", gemm_split_cap=runtime.SHARED_GPU_SPLIT_CAP)
+    a, sa = _run(case, "serial", checks="deferred", gemm_split_cap=runtime.SHARED_GPU_SPLIT_CAP,
+                 gemm_tile_n=runtime.SHARED_GPU_GEMM_TILE_N)
     b, sb = _run(case, "stage", checks="deferred")
     _same(a, sa, b, sb)
     c, sc = _run(case, "serial", checks="deferred")
-    d, sd = _run(case, "stage", checks="deferred", gemm_split_cap=8)
+    d, sd = _run(case, "stage", checks="deferred", gemm_split_cap=8, gemm_tile_n=64)
     _same(c, sc, d, sd)
     assert rec_tuples(b) == case["records"] and rec_tuples(c) == case["records"]
     for rep in (b, c):
