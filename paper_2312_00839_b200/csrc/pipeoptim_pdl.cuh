@@ -5,13 +5,13 @@
 // while this one drains, and every kernel waits (griddepcontrol.wait) for its
 // predecessor's completion and memory before touching global memory — so the
 // results are those of plain stream order (bit-identical runs, measured).
-// Off by default, and no runner turns it on: under stage concurrency
-// early-launched CTAs hold SM slots the other stages need (round 1: -2.4 %),
-// and where a stage is alone on its GPU the CUDA graphs already leave no
-// launch gaps — config-1 units -0.15 us on stages 0-2, +2.5 us on the head
-// stage, serial runs -1 % (profiles/r2_pdl_alone_probe.jsonl). Kept as a
-// switch for GPUs / runners where the launch latency is exposed. Without
-// the launch attribute griddepcontrol.wait is a no-op.
+// Off by default. Where a stage is alone on its GPU the CUDA graphs already
+// leave no launch gaps — config-1 units -0.15 us on stages 0-2, +2.5 us on
+// the head stage, serial runs -1 % (profiles/r2_pdl_alone_probe.jsonl) — so
+// only the stage-concurrent runner turns it on (runtime.SHARED_GPU_PDL,
+// together with its shared-GPU GEMM and launch-shape policies: +2-3 %,
+// profiles/r2_shared_gpu_pdl_probe.jsonl; round 1's shapes lost 2.4 % with
+// it). Without the launch attribute griddepcontrol.wait is a no-op.
 #pragma once
 
 #include <cuda_runtime.h>

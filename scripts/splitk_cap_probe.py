@@ -39,14 +39,20 @@ def capped(cap):
     return f
 
 
+import os  # noqa: E402
+
+from paper_2312_00839_b200 import _lib  # noqa: E402
+
+PDL = os.environ.get("PDL") == "1"  # short stream kernels with programmatic dependent launch
 graphs = {}
 for cap in CAPS:
     S._splitk_tc = capped(cap)
     for strategy in ("async_raw", "optimizer_prediction"):
         stages = build_stages(build_layers(CONFIG1_DIMS, CONFIG1_ACTS), 4, torch_init(0, dev), device=dev)
         opts = [OptimizerState(OptimizerConfig("adam"), s.param_names, device=dev) for s in stages]
-        g = GraphedExecute(build_timeline(strategy, 4, n), stages, opts, strategy, data, "softmax_xent",
-                           lambda mb: 1e-4, warmup_runs=1, streams=STREAMS)
+        with _lib.pdl(PDL):
+            g = GraphedExecute(build_timeline(strategy, 4, n), stages, opts, strategy, data, "softmax_xent",
+                               lambda mb: 1e-4, warmup_runs=1, streams=STREAMS)
         g.replay()
         graphs[(cap, strategy)] = (g, stages, opts)
 S._splitk_tc = orig
@@ -64,5 +70,5 @@ for _ in range(5):
 for cap in CAPS:
     off = n * BATCH / statistics.median(times[(cap, "async_raw")])
     on = n * BATCH / statistics.median(times[(cap, "optimizer_prediction")])
-    print(json.dumps({"streams": STREAMS, "splitk_cap": cap, "pred_off": round(off), "pred_on": round(on),
+    print(json.dumps({"streams": STREAMS, "pdl_short_kernels": PDL, "splitk_cap": cap, "pred_off": round(off), "pred_on": round(on),
                       "overhead": round(1 - on / off, 4)}), flush=True)
